@@ -1,0 +1,346 @@
+"""Benchmark of the B200 search engine (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[4], the configuration the metric is quoted on
+at 1-8 GPUs): exhaustive evaluation of a synthetic tuning space of the
+paper's OpenCL use-case model (abstract kernel, size 1024 — the largest
+Table-1 size — gmt 4), generalised from the reference's (wg, ts) space to
+  wg = 2^1..2^9 x ts = 2^1..2^9 x np (work-items per unit) = 2^0..2^9
+  x nu = 1..64 x nd = 1..160000            (8.29e9 configurations)
+A step finds the minimal-model-time configuration of the job's shard: every
+rank evaluates its own 10^9 configurations (weak scaling) with the cost-model
+kernel, and the packed (time << 33 | index) key is min-reduced over ranks with
+one NCCL all-reduce.  `value` = configurations evaluated per second by the
+whole job; `e2e` is the same through the host-buffer C-ABI call
+mctb_space_argmin (descriptor in, winner out, copies + sync in the region).
+
+--impl reference runs the reference's own CPU path for a configuration's
+model time (Machine::run, the exhaustive_sweep evaluator, machine.cpp:788-825)
+on a bounded random sample of the same space with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PER_RANK = 10 ** 9
+SPACE = dict(kernel=0, size=1024, gmt=4, nd=(1, 160000), nu=(1, 64), log2np=(0, 9),
+             log2wg=(1, 9), log2ts=(1, 9))
+METRIC = "tuning configs explored/sec (exhaustive argmin of model time)"
+UNIT = "configs/s"
+WORKLOAD = ("synthetic 8.29e9-configuration tuning space of the paper's abstract OpenCL "
+            "use-case model (size 1024, gmt 4; wg x ts x np x nu x nd), 1e9 configurations per "
+            "GPU, allreduce-min of the packed argmin key")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-sample-secs", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference
+def reference_sample(secs, seed=1, max_index=PER_RANK, threads=None):
+    """The reference's CPU evaluator (Machine::run RoundRobin via oracle/_ref, or the
+    oracle port when the reference is not built on this machine) on random
+    configurations of the benchmark space, all host cores, for ~secs seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import checkers
+    kind = "reference"
+    try:
+        chk = checkers.Ref() if os.path.exists(checkers.REF_SO) else None
+    except OSError:
+        chk = None
+    if chk is None:
+        chk, kind = checkers.Oracle(), "port"
+    threads = threads or os.cpu_count() or 1
+    deadline = time.perf_counter() + secs
+    counts = [0] * threads
+    steps = [0] * threads
+
+    def worker(w):
+        rng = random.Random(seed * 1000 + w)
+        while time.perf_counter() < deadline:
+            idx = rng.randrange(max_index)
+            plat, params = decode(idx)
+            r = chk.simulate(plat, SPACE["size"], SPACE["kernel"], params[0], params[1], 0, 0)
+            counts[w] += 1  # in-flight work finishing after the deadline is counted and
+            steps[w] += r["steps"]  # its time is inside `el` as well
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(worker, range(threads)))
+    el = time.perf_counter() - t0
+    return sum(counts) / el, kind, threads, sum(counts), sum(steps), el
+
+
+def decode(index):
+    """Index -> ((nd, nu, np, gmt), (wg, ts)) in the documented order (no GPU needed)."""
+    s = SPACE
+    n_nd = s["nd"][1] - s["nd"][0] + 1
+    n_nu = s["nu"][1] - s["nu"][0] + 1
+    n_np = s["log2np"][1] - s["log2np"][0] + 1
+    n_ts = s["log2ts"][1] - s["log2ts"][0] + 1
+    index, nd = divmod(index, n_nd)
+    index, nu = divmod(index, n_nu)
+    index, lnp = divmod(index, n_np)
+    wg_d, ts_d = divmod(index, n_ts)
+    return ((s["nd"][0] + nd, s["nu"][0] + nu, 1 << (s["log2np"][0] + lnp), s["gmt"]),
+            (1 << (s["log2wg"][1] - wg_d), 1 << (s["log2ts"][1] - ts_d)))
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = []
+    for k in range(args.warmup + args.steps):
+        secs = 1.0 if k < args.warmup else max(2.0, min(args.cpu_sample_secs,
+                                                          120.0 / max(1, args.steps)))
+        v, kind, thr, n, st, el = reference_sample(secs, seed=k + 1)
+        if k >= args.warmup:
+            per_step.append((v, n, st, el))
+    value = statistics.mean(p[0] for p in per_step)
+    n_tot = sum(p[1] for p in per_step)
+    el_tot = sum(p[3] for p in per_step)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el_tot / max(1, len(per_step)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "space": SPACE, "per_rank_configs": PER_RANK},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": kind,
+                             "sample": f"{n_tot} random configurations of the space evaluated by "
+                                       f"Machine::run (RoundRobin) in {el_tot:.1f} s"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ b200
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2305_09130_b200 as m
+    from paper_2305_09130_b200._lib import lib
+    from paper_2305_09130_b200.space import space_argmin_async
+    import ctypes as C
+
+    space = m.Space(**SPACE)
+    total = space.count
+    assert world * PER_RANK <= total, "space too small for this many ranks"
+    first = rank * PER_RANK
+    desc = space.desc()
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    key = torch.empty(1, dtype=torch.int64, device="cuda")
+    none_key = torch.tensor([1 << 62], dtype=torch.int64, device="cuda")  # > every real key
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 256 MB > L2
+    launches_per_step = 1  # argmin kernel (the key reset is a torch copy)
+
+    def step():
+        key.copy_(none_key)
+        space_argmin_async(space, first, PER_RANK, key.data_ptr(), sptr, desc)
+        if world > 1:
+            dist.all_reduce(key, op=dist.ReduceOp.MIN)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(k)  # L2 flush between timed steps (outside the events)
+        e0, e1, e2 = ev[k]
+        e0.record(stream)
+        key.copy_(none_key)
+        space_argmin_async(space, first, PER_RANK, key.data_ptr(), sptr, desc)
+        e1.record(stream)
+        if world > 1:
+            dist.all_reduce(key, op=dist.ReduceOp.MIN)
+        e2.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    kern_ms = [a.elapsed_time(b) for a, b, c in ev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = tot.item()
+    best_key = key.item()
+    value = world * PER_RANK * args.steps / (total_ms * 1e-3)
+
+    # winner, exact (GPU point evaluation through the host API on rank 0's view)
+    idx = best_key & ((1 << m.KEY_INDEX_BITS) - 1)
+    win = m.space_argmin(space, idx, 1)
+
+    # ---- end to end through the host-buffer C ABI (descriptor in, winner out)
+    hkey = C.c_uint64()
+    hout = (C.c_int64 * 8)()
+    e2e_dev = torch.empty(1, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        lib.mctb_space_argmin(desc, first, PER_RANK, C.byref(hkey), hout)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_times = []
+    for k in range(args.steps):
+        flush.fill_(k)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rc = lib.mctb_space_argmin(desc, first, PER_RANK, C.byref(hkey), hout)
+        if world > 1:
+            e2e_dev.fill_(hkey.value)  # H2D of the local key, NCCL min, D2H of the winner
+            dist.all_reduce(e2e_dev, op=dist.ReduceOp.MIN)
+            _ = e2e_dev.item()
+        e2e_times.append(time.perf_counter() - t0)
+        assert rc == 0
+    e2e_tot = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
+    e2e_value = world * PER_RANK * args.steps / e2e_tot.item()
+
+    # ---- roofline of the cost-model kernel: integer issue vs the measured INT32 peak
+    peak_ops, _ = C.c_double(), C.c_double()
+    lib.mctb_int32_peak(C.byref(peak_ops), C.byref(_))
+    kern_avg_s = statistics.mean(kern_ms) * 1e-3
+    ops_per_cfg = INT_OPS_PER_CONFIG
+    achieved = PER_RANK * ops_per_cfg / kern_avg_s
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "space": SPACE, "per_rank_configs": PER_RANK,
+                       "time_to_optimum_ms": total_ms / args.steps,
+                       "l2": "256 MB flush between timed steps; kernel reads no DRAM",
+                       "parallelism": f"shard{world}"},
+            "result": {"t_min": win.time, "index": idx, "platform": win.platform.__dict__,
+                       "params": win.params.__dict__, "steps": win.steps},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 13 * 8,
+                    "d2h_bytes_per_step": 8 + 8 * 8},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "int32", "achieved": achieved / 1e12,
+                         "peak": peak_ops.value / 1e12, "unit": "Tops/s",
+                         "frac": achieved / peak_ops.value, "traffic": None,
+                         "kernel": "space_argmin_kernel<0>", "kernel_ms": statistics.mean(kern_ms),
+                         "ops_per_config": ops_per_cfg,
+                         "peak_source": "measured: mctb_int32_peak IMAD+LOP3 probe, same run"},
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, kind, thr, n, st, el = reference_sample(args.cpu_sample_secs)
+            line["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": thr, "kind": kind,
+                "sample": f"{n} random configurations of the space ({st} transitions) evaluated "
+                          f"by the reference's Machine::run (RoundRobin) in {el:.1f} s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# SASS instructions (thread level) per configuration of the nd-loop body of
+# space_argmin_kernel<0> (cuobjdump: 136 instructions for a 4x-unrolled body),
+# see DESIGN.md §4 and profiles/.
+INT_OPS_PER_CONFIG = 34
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,102 @@
+/* mctune_b200 — B200-native search engine for the model-checking auto-tuner of
+ * arXiv:2305.09130 ("Model Checking-based Performance Prediction and Tuning of
+ * OpenCL programs").  C ABI: plain pointers and sizes only.
+ *
+ * Each entry point replaces one interface of the reference C++ core
+ * (/root/reference/proj/include/mctune/*.hpp); the citation is on the
+ * declaration.  Conventions shared by all calls:
+ *   plat   : int[4] = {nd, nu, np, gmt}                 (model.hpp:37-44 PlatformConfig)
+ *   size   : input length, a power of two >= 4           (model.hpp:53-64 ProblemSpec)
+ *   kernel : 0 = abstract, 1 = minimum                   (model.hpp:46 KernelKind)
+ *   input  : int64[size] or NULL (minimum kernel; NULL = glob[i] = size - i)
+ *   trace  : int32[4 * cap], one transition = {actor, peer, op, arg}
+ *            (machine.hpp:78-88 Transition; op = ordinal of mctune::Op)
+ *   return : MCTB_OK, or the error class of the reference exception
+ *            (ConfigError -> MCTB_CONFIG_ERROR, ModelBug -> MCTB_MODEL_BUG,
+ *             CorruptTrace -> MCTB_CORRUPT_TRACE); text via mctb_last_error().
+ * Every compute call runs on the current CUDA device; there is no CPU path —
+ * calls fail with MCTB_NO_DEVICE when no sm_100 device is present.
+ */
+#ifndef MCTUNE_B200_H
+#define MCTUNE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCTB_OK 0
+#define MCTB_MODEL_BUG 1
+#define MCTB_CONFIG_ERROR 2
+#define MCTB_CORRUPT_TRACE 3
+#define MCTB_LIMIT 4
+#define MCTB_NO_DEVICE 5
+#define MCTB_CUDA_ERROR 6
+
+/* scheduling policies for mctb_simulate (machine.hpp:219 SchedPolicy + ours) */
+#define MCTB_POLICY_ROUND_ROBIN 0 /* SchedPolicy::RoundRobin */
+#define MCTB_POLICY_MT19937 1     /* SchedPolicy::SeededRandom (std::mt19937_64) */
+#define MCTB_POLICY_FIRST 2       /* first enabled: the first DFS path of explore_machine */
+#define MCTB_POLICY_PHILOX 3      /* swarm trajectory: Philox4x32-10 counter-based choice */
+
+/* argmin key: (min(time, 2^30-1) << 33) | config index  (index < 2^33) */
+#define MCTB_KEY_TIME_BITS 30
+#define MCTB_KEY_INDEX_BITS 33
+
+const char* mctb_last_error(void);
+int mctb_version(void);
+/* number of sm_100 devices visible (0 -> every compute call fails with MCTB_NO_DEVICE) */
+int mctb_device_count(void);
+
+/* derive_launch (model.hpp:75, model.cpp:161-177); out = {wgs, nwd, nwu, nwe, all_nwe} */
+int mctb_derive_launch(const int* plat, int size, int wg, int ts, int* out);
+
+/* ---------------------------------------------------------------------------
+ * Exhaustive evaluation of a tuning space (north-star subsystem 1).
+ * Space descriptor sd = int64[13]:
+ *   {kernel, size, gmt, nd_lo, nd_hi, nu_lo, nu_hi,
+ *    log2np_lo, log2np_hi, log2wg_lo, log2wg_hi, log2ts_lo, log2ts_hi}
+ * Index order (least index = preferred on ties): wg descending, ts descending,
+ * then np, nu, nd ascending — for a single platform this is exactly the
+ * reference's preference "largest wg, then largest ts" (search.hpp:367-369,
+ * explore.cpp:64-72).  The reference's own space for (plat, size) is
+ *   {kernel, size, gmt, nd, nd, nu, nu, log2 np, log2 np, 1, n-1, 1, n-1}.
+ */
+uint64_t mctb_space_count(const int64_t* sd);
+
+/* Device-resident argmin: atomically min-combines the packed key of
+ * [first, first+count) into *d_key (device pointer).  No host sync, no
+ * allocation; stream is a cudaStream_t (NULL = legacy default stream).
+ * Replaces the config loop of check_overtime (explore.cpp:171-200). */
+int mctb_space_argmin_async(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* d_key,
+                            void* stream);
+
+/* Host-buffer argmin (end to end, including the host<->device copies).
+ * out = {time, steps, nd, nu, np, gmt, wg, ts} of the winning configuration. */
+int mctb_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* key,
+                      int64_t* out);
+
+/* Per-configuration table: d_time[i], d_steps[i] for index first+i (device
+ * pointers; time = -1 for infeasible configurations). */
+int mctb_space_eval_async(const int64_t* sd, uint64_t first, uint64_t count, int64_t* d_time,
+                          int64_t* d_steps, void* stream);
+
+/* Measured INT32 issue rate of the current device (integer ops/s over the chip;
+ * IMAD + IADD3 chains) — the roofline denominator of the cost-model kernel. */
+int mctb_int32_peak(double* ops_per_sec, double* ms);
+
+/* ---------------------------------------------------------------------------
+ * Reference-compatible drivers (host buffers).
+ */
+
+/* exhaustive_sweep (search.hpp:384, search.cpp:214-246).
+ * rows = int64[6 * cap]: {wg, ts, time, transitions, ok, note(0 none, 1 infeasible, 2 deadlock)},
+ * sorted exactly like the reference. */
+int mctb_sweep(const int* plat, int size, int kernel, const int64_t* input, int64_t* rows,
+               int64_t cap, int64_t* n_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,23 @@
+"""B200-native search engine for the model-checking auto-tuner of arXiv:2305.09130.
+
+Drop-in for the reference's tuning path (mctune: model / explore / search):
+the configuration-space evaluation, the schedule trajectories, the
+interleaving exploration and the bound-lowering driver run as sm_100a CUDA
+kernels behind the C ABI in include/mctune_b200.h.
+"""
+from ._lib import (ConfigError, CorruptTrace, CudaError, LimitError, MctuneError, ModelBug,
+                   NoDeviceError, device_count)
+from .model import (ABSTRACT, MINIMUM, LaunchPlan, PlatformConfig, ProblemSpec, TuningParams,
+                    config_feasible, derive_launch, enumerate_configs, kernel_kind_from_string,
+                    log2_exact, validate_params)
+from .search import SweepRow, exhaustive_sweep
+from .space import KEY_INDEX_BITS, KEY_SAT, KEY_TIME_BITS, Space, SpaceResult, space_argmin
+
+__all__ = [
+    "ABSTRACT", "MINIMUM", "ConfigError", "CorruptTrace", "CudaError", "LimitError",
+    "MctuneError", "ModelBug", "NoDeviceError", "LaunchPlan", "PlatformConfig", "ProblemSpec",
+    "TuningParams", "SweepRow", "Space", "SpaceResult", "KEY_INDEX_BITS", "KEY_SAT",
+    "KEY_TIME_BITS", "config_feasible", "derive_launch", "device_count", "enumerate_configs",
+    "exhaustive_sweep", "kernel_kind_from_string", "log2_exact", "space_argmin",
+    "validate_params",
+]

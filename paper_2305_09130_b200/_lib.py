@@ -1,0 +1,93 @@
+"""Loader for the in-tree CUDA library (libmctune_b200.so) and its C ABI.
+
+There is no CPU implementation behind this package: if the library is missing
+the import fails, and every compute call fails with NoDeviceError when no
+sm_100 GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmctune_b200.so")
+
+
+class MctuneError(RuntimeError):
+    """Base class of the engine's errors."""
+
+
+class ConfigError(MctuneError):
+    """Invalid user input (reference: mctune::ConfigError, model.hpp:16)."""
+
+
+class ModelBug(MctuneError):
+    """Internal contract violation (reference: mctune::ModelBug, model.hpp:21)."""
+
+
+class CorruptTrace(MctuneError):
+    """A trace failed to replay (reference: mctune::CorruptTrace, explore.hpp:14)."""
+
+
+class LimitError(MctuneError):
+    """A capacity limit of the GPU engine was hit."""
+
+
+class NoDeviceError(MctuneError):
+    """No sm_100 (B200) device: the engine has no CPU path."""
+
+
+class CudaError(MctuneError):
+    """A CUDA runtime call failed."""
+
+
+_ERRORS = {1: ModelBug, 2: ConfigError, 3: CorruptTrace, 4: LimitError, 5: NoDeviceError,
+           6: CudaError}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is not built; run `python -m paper_2305_09130_b200.build` "
+        "(nvcc, sm_100a).  There is no CPU fallback.")
+
+lib = C.CDLL(LIB_PATH)
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+u64p = C.POINTER(C.c_uint64)
+vp = C.c_void_p
+
+lib.mctb_last_error.restype = C.c_char_p
+lib.mctb_version.restype = C.c_int
+lib.mctb_device_count.restype = C.c_int
+lib.mctb_derive_launch.argtypes = [i32p, C.c_int, C.c_int, C.c_int, i32p]
+lib.mctb_space_count.argtypes = [i64p]
+lib.mctb_space_count.restype = C.c_uint64
+lib.mctb_space_argmin_async.argtypes = [i64p, C.c_uint64, C.c_uint64, vp, vp]
+lib.mctb_space_argmin.argtypes = [i64p, C.c_uint64, C.c_uint64, u64p, i64p]
+lib.mctb_space_eval_async.argtypes = [i64p, C.c_uint64, C.c_uint64, vp, vp, vp]
+lib.mctb_int32_peak.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
+lib.mctb_sweep.argtypes = [i32p, C.c_int, C.c_int, i64p, i64p, C.c_int64, i64p]
+
+EXPORTED = [
+    "mctb_last_error", "mctb_version", "mctb_device_count", "mctb_derive_launch",
+    "mctb_space_count", "mctb_space_argmin_async", "mctb_space_argmin",
+    "mctb_space_eval_async", "mctb_sweep", "mctb_int32_peak",
+]
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib.mctb_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, MctuneError)(msg)
+
+
+def i32arr(vals):
+    return (C.c_int32 * len(vals))(*vals)
+
+
+def i64arr(vals):
+    return (C.c_int64 * len(vals))(*vals)
+
+
+def device_count() -> int:
+    return lib.mctb_device_count()

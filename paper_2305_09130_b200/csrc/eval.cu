@@ -1,0 +1,285 @@
+// Exhaustive evaluation of a tuning space on B200 (north-star subsystem 1).
+//
+// One thread evaluates a contiguous run of configuration indices with the
+// lock-step cost model (cost_model.cuh) in integer model time, keeps the
+// lexicographic minimum of (saturated time, index), reduces it across the
+// warp with shuffles and across the CTA in shared memory, and min-combines
+// one packed 64-bit key per CTA with atomicMin:
+//     key = (min(time, 2^30 - 1) << 33) | index.
+// The index order puts the reference's preferred configuration (largest wg,
+// then largest ts — explore.cpp:64-72, search.cpp:451-453) first, so the
+// minimum key breaks ties exactly as bisect_min_time does.
+//
+// Nothing here reads memory on the hot path: the kernel is bound by integer
+// issue (one u32 division and ~30 IADD3/IMAD/ISETP per configuration), so the
+// grid is a multiple of the 148 SMs and each thread amortises its index decode
+// over thousands of configurations (nd is the fastest digit; per-(wg, ts, np,
+// nu) quantities are hoisted out of the nd loop).
+#include "common.cuh"
+#include "cost_model.cuh"
+
+namespace mctb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// a << sh, saturating at INT64_MAX (a >= 0)
+__device__ __forceinline__ int64_t shl_sat(int64_t a, int sh) {
+    return (sh >= 62 || (a >> (62 - sh)) != 0) ? INT64_MAX : (a << sh);
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ void cta_min_commit(uint64_t key, unsigned long long* out) {
+    __shared__ uint64_t warp_best[kThreads / 32];
+    key = warp_min_u64(key);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) warp_best[warp] = key;
+    __syncthreads();
+    if (warp == 0) {
+        key = lane < kThreads / 32 ? warp_best[lane] : kKeyNone;
+        key = warp_min_u64(key);
+        if (lane == 0 && key != kKeyNone) atomicMin(out, (unsigned long long)key);
+    }
+}
+
+template <int KERNEL>
+__global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uint64_t first,
+                                                                uint64_t count,
+                                                                uint64_t per_thread,
+                                                                unsigned long long* out_key) {
+    const uint64_t tid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    uint64_t pos = tid * per_thread;
+    const uint64_t end = min(pos + per_thread, count);
+    uint32_t best_tf = kKeySat + 1;  // "nothing yet": above every real (saturated) time
+    uint64_t best_idx = 0;
+    if (pos < end) {
+        const Config c0 = decode(sd, first + pos);
+        uint32_t nd_d = (uint32_t)(c0.nd - sd.nd_lo);
+        int nu = c0.nu, lognp = c0.lognp, logwg = c0.logwg, logts = c0.logts;
+        const int64_t size = 1ll << sd.logn;
+        const int64_t gmt = sd.gmt;
+        const int64_t A = size * (gmt + 1) + gmt;  // abstract: (size/ts)(gmt ts + ts) + gmt
+        while (pos < end) {
+            // ---- quantities fixed along the nd digit
+            const int s = logwg + logts;
+            const uint32_t wgs = s < sd.logn ? (1u << (sd.logn - s)) : 1u;
+            const uint32_t q = wgs / (uint32_t)nu;
+            const uint32_t nwu = wgs <= (uint32_t)nu ? wgs : (uint32_t)nu;
+            const int lognwe = logwg < lognp ? logwg : lognp;
+            const uint32_t dr = max(wgs / nwu, 1u);
+            const uint32_t nd_thr = (wgs + (uint32_t)nu - 1) / (uint32_t)nu;  // wgs <= nu*nd
+            int64_t D;
+            bool feasible = true;
+            if (KERNEL == 0) {
+                D = shl_sat(A, logwg - lognwe);
+            } else {
+                feasible = s <= sd.logn;
+                D = shl_sat(gmt, logts + logwg - lognwe);
+                if (D != INT64_MAX) D += (1ll << lognwe) - 1 + gmt;
+            }
+            const uint32_t run = (uint32_t)min((uint64_t)(sd.n_nd - nd_d), end - pos);
+            if (!feasible || D >= (int64_t)kKeySat) {
+                if (best_tf > kKeySat) {  // only reachable before any real time
+                    best_tf = kKeySat;
+                    best_idx = first + pos;
+                }
+            } else {
+                const uint32_t D32 = (uint32_t)D;
+                uint32_t nd = (uint32_t)sd.nd_lo + nd_d;
+                const uint64_t base = first + pos;
+                for (uint32_t k = 0; k < run; ++k, ++nd) {
+                    const uint32_t nwd = q == 0 ? 1u : (nd >= nd_thr ? q : nd);
+                    const uint32_t waves = (dr + nwd - 1) / nwd;
+                    const uint64_t t = (uint64_t)waves * D32;
+                    const uint32_t tf = t < kKeySat ? (uint32_t)t : kKeySat;
+                    if (tf < best_tf) {
+                        best_tf = tf;
+                        best_idx = base + k;
+                    }
+                }
+            }
+            pos += run;
+            // ---- odometer: advance nu, np, ts, wg digits
+            nd_d = 0;
+            if (++nu > sd.nu_hi) {
+                nu = sd.nu_lo;
+                if (++lognp > sd.lognp_hi) {
+                    lognp = sd.lognp_lo;
+                    if (--logts < sd.logts_lo) {
+                        logts = sd.logts_hi;
+                        --logwg;
+                    }
+                }
+            }
+        }
+    }
+    const uint64_t key =
+        best_tf > kKeySat ? kKeyNone : (((uint64_t)best_tf << MCTB_KEY_INDEX_BITS) | best_idx);
+    cta_min_commit(key, out_key);
+}
+
+__global__ void space_eval_kernel(SpaceDev sd, int kernel, uint64_t first, uint64_t count,
+                                  int64_t* __restrict__ time, int64_t* __restrict__ steps) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const Cost c = lockstep_cost(kernel, sd.logn, sd.gmt, decode(sd, first + i));
+    time[i] = c.time;
+    steps[i] = c.steps;
+}
+
+// Exact evaluation of the winning index: out = {time, steps, nd, nu, np, gmt, wg, ts}
+__global__ void space_point_kernel(SpaceDev sd, int kernel, const unsigned long long* key,
+                                   int64_t* out) {
+    const uint64_t k = *key;
+    if (k == kKeyNone) {
+        out[0] = -2;
+        return;
+    }
+    const Config c = decode(sd, k & kKeyIndexMask);
+    const Cost r = lockstep_cost(kernel, sd.logn, sd.gmt, c);
+    out[0] = r.time;
+    out[1] = r.steps;
+    out[2] = c.nd;
+    out[3] = c.nu;
+    out[4] = 1ll << c.lognp;
+    out[5] = sd.gmt;
+    out[6] = 1ll << c.logwg;
+    out[7] = 1ll << c.logts;
+}
+
+__global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace
+
+// Validates the descriptor and fills the device view.  The ranges must keep
+// every configuration inside validate_params (model.cpp:151-159).
+int make_space(const int64_t* sd, SpaceDev* out) {
+    const int64_t kernel = sd[0], size = sd[1];
+    if (kernel != 0 && kernel != 1) {
+        set_error("kernel must be 0 (abstract) or 1 (minimum)");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (size < 4 || (size & (size - 1)) || size > (1ll << 30)) {
+        set_error("size must be a power of two in [4, 2^30]");
+        return MCTB_CONFIG_ERROR;
+    }
+    int logn = 0;
+    while ((1ll << logn) < size) ++logn;
+    if (sd[2] < 1 || sd[2] > (1 << 20)) {
+        set_error("gmt must be in [1, 2^20]");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (sd[3] < 1 || sd[4] < sd[3] || sd[4] > (1 << 24) || sd[5] < 1 || sd[6] < sd[5] ||
+        sd[6] > (1 << 24)) {
+        set_error("nd and nu ranges must satisfy 1 <= lo <= hi <= 2^24");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (sd[7] < 0 || sd[8] < sd[7] || sd[8] > 24) {
+        set_error("log2 np range must satisfy 0 <= lo <= hi <= 24");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (sd[9] < 1 || sd[10] < sd[9] || sd[10] > logn - 1 || sd[11] < 1 || sd[12] < sd[11] ||
+        sd[12] > logn - 1) {
+        set_error("log2 wg and log2 ts ranges must lie in [1, log2(size) - 1]");
+        return MCTB_CONFIG_ERROR;
+    }
+    SpaceDev s;
+    s.kernel = (int32_t)kernel;
+    s.logn = logn;
+    s.gmt = (int32_t)sd[2];
+    s.nd_lo = (int32_t)sd[3];
+    s.nd_hi = (int32_t)sd[4];
+    s.nu_lo = (int32_t)sd[5];
+    s.nu_hi = (int32_t)sd[6];
+    s.lognp_lo = (int32_t)sd[7];
+    s.lognp_hi = (int32_t)sd[8];
+    s.logwg_lo = (int32_t)sd[9];
+    s.logwg_hi = (int32_t)sd[10];
+    s.logts_lo = (int32_t)sd[11];
+    s.logts_hi = (int32_t)sd[12];
+    s.n_nd = (uint32_t)(s.nd_hi - s.nd_lo + 1);
+    s.n_nu = (uint32_t)(s.nu_hi - s.nu_lo + 1);
+    s.n_np = (uint32_t)(s.lognp_hi - s.lognp_lo + 1);
+    s.n_ts = (uint32_t)(s.logts_hi - s.logts_lo + 1);
+    s.n_wg = (uint32_t)(s.logwg_hi - s.logwg_lo + 1);
+    const double total = (double)s.n_nd * s.n_nu * s.n_np * s.n_ts * s.n_wg;
+    if (total >= (double)(1ull << MCTB_KEY_INDEX_BITS)) {
+        set_error("tuning space exceeds 2^33 configurations");
+        return MCTB_CONFIG_ERROR;
+    }
+    *out = s;
+    return MCTB_OK;
+}
+
+uint64_t space_count(const SpaceDev& s) {
+    return (uint64_t)s.n_nd * s.n_nu * s.n_np * s.n_ts * s.n_wg;
+}
+
+int launch_space_argmin(const SpaceDev& s, uint64_t first, uint64_t count, uint64_t* d_key,
+                        cudaStream_t stream) {
+    if (first + count > space_count(s)) {
+        set_error("index range outside the tuning space");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (count == 0) return MCTB_OK;
+    // persistent-style grid: 8 CTAs of 256 threads per SM, each thread a
+    // contiguous run of >= 16 indices
+    const uint64_t max_threads = (uint64_t)sm_count() * 8 * kThreads;
+    uint64_t per_thread = (count + max_threads - 1) / max_threads;
+    if (per_thread < 16) per_thread = 16;
+    const uint64_t threads = (count + per_thread - 1) / per_thread;
+    const unsigned blocks = (unsigned)((threads + kThreads - 1) / kThreads);
+    auto* key = reinterpret_cast<unsigned long long*>(d_key);
+    if (s.kernel == 0)
+        space_argmin_kernel<0><<<blocks, kThreads, 0, stream>>>(s, first, count, per_thread, key);
+    else
+        space_argmin_kernel<1><<<blocks, kThreads, 0, stream>>>(s, first, count, per_thread, key);
+    return cuda_check(cudaGetLastError(), "space_argmin_kernel");
+}
+
+int launch_space_eval(const SpaceDev& s, uint64_t first, uint64_t count, int64_t* d_time,
+                      int64_t* d_steps, cudaStream_t stream) {
+    if (first + count > space_count(s)) {
+        set_error("index range outside the tuning space");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (count == 0) return MCTB_OK;
+    const unsigned blocks = (unsigned)((count + 255) / 256);
+    space_eval_kernel<<<blocks, 256, 0, stream>>>(s, s.kernel, first, count, d_time, d_steps);
+    return cuda_check(cudaGetLastError(), "space_eval_kernel");
+}
+
+int launch_space_point(const SpaceDev& s, const uint64_t* d_key, int64_t* d_out,
+                       cudaStream_t stream) {
+    space_point_kernel<<<1, 1, 0, stream>>>(s, s.kernel,
+                                           reinterpret_cast<const unsigned long long*>(d_key),
+                                           d_out);
+    return cuda_check(cudaGetLastError(), "space_point_kernel");
+}
+
+int launch_fill_key(uint64_t* d_key, cudaStream_t stream) {
+    fill_u64_kernel<<<1, 1, 0, stream>>>(reinterpret_cast<unsigned long long*>(d_key), kKeyNone);
+    return cuda_check(cudaGetLastError(), "fill_u64_kernel");
+}
+
+}  // namespace mctb
