@@ -96,6 +96,31 @@ int mctb_int32_peak(double* ops_per_sec, double* ms);
 int mctb_sweep(const int* plat, int size, int kernel, const int64_t* input, int64_t* rows,
                int64_t cap, int64_t* n_rows);
 
+/* Machine::run (machine.hpp:224-227, machine.cpp:788-825) on the GPU, with one of the
+ * MCTB_POLICY_* schedulers (traj = trajectory id for MCTB_POLICY_PHILOX).
+ * out = {time, steps, result (INT64_MIN for abstract), process_count}. */
+int mctb_simulate(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                  int policy, uint64_t seed, uint64_t traj, int64_t* out, int32_t* trace,
+                  int64_t cap, int64_t* trace_len);
+
+/* Batched trajectories (north-star subsystem 2; the swarm_worker runs of
+ * explore.hpp:295-299 re-designed as counter-based random schedules):
+ * trajectory t (= traj0 + i) runs configuration configs[t % n_configs]
+ * (configs = int32[2 * n_configs] of (wg, ts)).
+ * out = int64[6 * n_traj]: {time, steps, result, status, fnv1a64(trace), config}. */
+int mctb_trajectories(const int* plat, int size, int kernel, const int64_t* input,
+                      const int32_t* configs, int n_configs, int policy, uint64_t seed,
+                      uint64_t traj0, uint64_t n_traj, int64_t max_steps, int64_t* out);
+
+/* replay (explore.hpp:301-304, explore.cpp:283-300) on the GPU; out = {final_time, result} */
+int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                const int32_t* trace, int64_t len, int64_t final_time, int64_t* out);
+
+/* trace_to_text (report.hpp:435-440, report.cpp:82-97): returns the text length and
+ * copies at most cap-1 bytes + NUL into buf; -1 on error. */
+int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* input, int wg,
+                        int ts, const int32_t* trace, int64_t len, char* buf, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

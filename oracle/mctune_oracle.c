@@ -1690,3 +1690,51 @@ int mo_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_t*
     *best_time = (int64_t)(best >> MO_KEY_INDEX_BITS);
     return MO_OK;
 }
+
+/* Bulk CPU replay of GPU trajectories (checker for mctb_trajectories):
+ * trajectory t = traj0 + i runs configs[t % n_configs] under `policy`;
+ * out = int64[6 * n]: {time, steps, result, status, fnv1a64(trace words), config}. */
+static uint64_t fnv_words(uint64_t h, const mo_transition* t) {
+    const int32_t w[4] = {t->actor, t->peer, t->op, t->arg};
+    for (int k = 0; k < 4; ++k)
+        for (int i = 0; i < 4; ++i) {
+            h ^= ((uint32_t)w[k] >> (8 * i)) & 0xff;
+            h *= 0x100000001b3ull;
+        }
+    return h;
+}
+
+int mo_trajectories(const int* plat, int size, int kernel, const int64_t* input,
+                    const int32_t* configs, int n_configs, int policy, uint64_t seed,
+                    uint64_t traj0, uint64_t n, int64_t* out) {
+    int64_t cap = 1 << 20;
+    mo_transition* tr = (mo_transition*)malloc(sizeof(mo_transition) * (size_t)cap);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t t = traj0 + i;
+        const int c = (int)(t % (uint64_t)n_configs);
+        int64_t o[4], len = 0;
+        int rc = mo_simulate(plat, size, kernel, input, configs[2 * c], configs[2 * c + 1], policy,
+                             seed, t, o, tr, cap, &len);
+        if (rc == MO_OK && len > cap) {
+            cap = len;
+            tr = (mo_transition*)realloc(tr, sizeof(mo_transition) * (size_t)cap);
+            rc = mo_simulate(plat, size, kernel, input, configs[2 * c], configs[2 * c + 1], policy,
+                             seed, t, o, tr, cap, &len);
+        }
+        if (rc) {
+            free(tr);
+            return rc;
+        }
+        uint64_t h = 0xcbf29ce484222325ull;
+        for (int64_t k = 0; k < len; ++k) h = fnv_words(h, &tr[k]);
+        int64_t* r = out + 6 * i;
+        r[0] = o[0];
+        r[1] = o[1];
+        r[2] = o[2];
+        r[3] = 0;
+        r[4] = (int64_t)h;
+        r[5] = c;
+    }
+    free(tr);
+    return MO_OK;
+}

@@ -85,6 +85,11 @@ int mo_space_argmin(const int64_t* space_desc, uint64_t first, uint64_t count,
                     uint64_t* best_key, int64_t* best_time, uint64_t* best_index);
 int mo_space_decode(const int64_t* space_desc, uint64_t index, int* cfg /* nd,nu,np,gmt,size,kernel,wg,ts */);
 
+/* Bulk CPU replay of trajectories (checker for mctb_trajectories) */
+int mo_trajectories(const int* plat, int size, int kernel, const int64_t* input,
+                    const int32_t* configs, int n_configs, int policy, uint64_t seed,
+                    uint64_t traj0, uint64_t n, int64_t* out);
+
 /* Philox4x32-10 (Salmon et al., SC'11), counter (c0..c3), key (k0,k1) -> out[4] */
 void mo_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out);
 

@@ -10,6 +10,8 @@ from ._lib import (ConfigError, CorruptTrace, CudaError, LimitError, MctuneError
 from .model import (ABSTRACT, MINIMUM, LaunchPlan, PlatformConfig, ProblemSpec, TuningParams,
                     config_feasible, derive_launch, enumerate_configs, kernel_kind_from_string,
                     log2_exact, validate_params)
+from .machine import (FIRST, MT19937, PHILOX, ROUND_ROBIN, SEEDED_RANDOM, Machine, RunOutcome,
+                      Trace, TrajectoryBatch, replay, trace_to_text, trajectories)
 from .search import SweepRow, exhaustive_sweep
 from .space import KEY_INDEX_BITS, KEY_SAT, KEY_TIME_BITS, Space, SpaceResult, space_argmin
 
@@ -19,5 +21,6 @@ __all__ = [
     "TuningParams", "SweepRow", "Space", "SpaceResult", "KEY_INDEX_BITS", "KEY_SAT",
     "KEY_TIME_BITS", "config_feasible", "derive_launch", "device_count", "enumerate_configs",
     "exhaustive_sweep", "kernel_kind_from_string", "log2_exact", "space_argmin",
-    "validate_params",
+    "validate_params", "FIRST", "MT19937", "PHILOX", "ROUND_ROBIN", "SEEDED_RANDOM", "Machine",
+    "RunOutcome", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
 ]

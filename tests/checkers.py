@@ -158,6 +158,17 @@ class Oracle(_Base):
                                            C.byref(idx)))
         return key.value, t.value, idx.value
 
+    def trajectories(self, plat, size, kernel, configs, policy, seed, traj0, n, inp=None):
+        cfg = (C.c_int32 * (2 * len(configs)))(*[v for c in configs for v in c])
+        out = (C.c_int64 * (6 * n))()
+        self._chk(self.lib.mo_trajectories(_plat(plat), size, kernel, _inp(size, kernel, inp), cfg,
+                                           len(configs), policy, C.c_uint64(seed),
+                                           C.c_uint64(traj0), C.c_uint64(n), out))
+        cols = [list(out[k::6]) for k in range(6)]
+        cols[4] = [v & ((1 << 64) - 1) for v in cols[4]]
+        cols[2] = [None if v == -(1 << 63) else v for v in cols[2]]
+        return cols
+
     def philox(self, ctr, key):
         out = (C.c_uint32 * 4)()
         self.lib.mo_philox4x32_10((C.c_uint32 * 4)(*ctr), (C.c_uint32 * 2)(*key), out)
