@@ -12,6 +12,7 @@ from .model import (ABSTRACT, MINIMUM, LaunchPlan, PlatformConfig, ProblemSpec, 
                     log2_exact, validate_params)
 from .machine import (FIRST, MT19937, PHILOX, ROUND_ROBIN, SEEDED_RANDOM, Machine, RunOutcome,
                       Trace, TrajectoryBatch, replay, trace_to_text, trajectories)
+from .explore import ExploreStats, SweepInfo, explore_configs, explore_machine
 from .search import SweepRow, exhaustive_sweep
 from .space import KEY_INDEX_BITS, KEY_SAT, KEY_TIME_BITS, Space, SpaceResult, space_argmin
 
@@ -22,5 +23,5 @@ __all__ = [
     "KEY_TIME_BITS", "config_feasible", "derive_launch", "device_count", "enumerate_configs",
     "exhaustive_sweep", "kernel_kind_from_string", "log2_exact", "space_argmin",
     "validate_params", "FIRST", "MT19937", "PHILOX", "ROUND_ROBIN", "SEEDED_RANDOM", "Machine",
-    "RunOutcome", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
+    "RunOutcome", "ExploreStats", "SweepInfo", "explore_configs", "explore_machine", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
 ]

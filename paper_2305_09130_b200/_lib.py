@@ -101,3 +101,6 @@ def i64arr(vals):
 
 def device_count() -> int:
     return lib.mctb_device_count()
+
+lib.mctb_explore.argtypes = [i32p, C.c_int, C.c_int, i64p, i32p, C.c_int, C.c_int64, i64p, i64p]
+EXPORTED.append("mctb_explore")

@@ -184,6 +184,27 @@ __host__ __device__ inline void initial_state(const MachDesc& m, MState& s) {
         for (int i = 0; i < m.n_units * m.np; ++i) s.loc[i] = m.max_id;
 }
 
+// Copies the live part of a state (the arrays are sized for the capacity).
+__host__ __device__ inline void copy_state(const MachDesc& m, MState& d, const MState& s) {
+    d.time = s.time;
+    d.nrp_work = s.nrp_work;
+    d.all_nwe = s.all_nwe;
+    d.fin = s.fin;
+    d.next_wg = s.next_wg;
+    d.host_pc = s.host_pc;
+    d.host_k = s.host_k;
+    d.clock = s.clock;
+    d.glob0 = s.glob0;
+    for (int i = 0; i < m.nwd; ++i) d.dev[i] = s.dev[i];
+    for (int g = 0; g < m.n_units; ++g) {
+        d.unit[g] = s.unit[g];
+        d.bar[g] = s.bar[g];
+    }
+    for (int p = 0; p < m.n_pex; ++p) d.pex[p] = s.pex[p];
+    if (m.kernel == 1)
+        for (int i = 0; i < m.n_units * m.np; ++i) d.loc[i] = s.loc[i];
+}
+
 // Machine::place_pex, machine.cpp:136-162
 __host__ __device__ inline void place_pex(const MachDesc& m, PexS& px) {
     const Instr in = instr_at(m, px.phase, px.cursor);

@@ -1,0 +1,55 @@
+"""Exhaustive interleaving exploration on the GPU (reference: include/mctune/explore.hpp).
+
+`explore_configs` runs the frontier-parallel BFS over the full state spaces of
+one or more configurations of a (platform, problem) in one sweep and returns
+the reference's ExploreStats fields per configuration, plus the range of
+terminal model times (a proof of the minimal time over all interleavings).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Sequence
+
+from ._lib import check, i32arr, lib
+from .model import PlatformConfig, ProblemSpec, TuningParams
+
+
+@dataclass
+class ExploreStats:
+    """(explore.hpp:235-245) + terminal-time range."""
+    complete: bool
+    states_visited: int
+    transitions_applied: int
+    max_depth_reached: int
+    min_time: int
+    max_time: int
+    terminals: int
+    deadlocks: int
+
+
+@dataclass
+class SweepInfo:
+    levels: int
+    states: int
+    key_words: int
+    kernel_us: int
+
+
+def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
+                    configs: Sequence[TuningParams], max_states: int = 5_000_000,
+                    info: list | None = None) -> List[ExploreStats]:
+    cfg = i32arr([v for c in configs for v in (c.wg, c.ts)])
+    out = (C.c_int64 * (8 * len(configs)))()
+    inf = (C.c_int64 * 4)()
+    check(lib.mctb_explore(platform.as_array(), problem.size, problem.kernel,
+                           problem.input_array(), cfg, len(configs), max_states, out, inf))
+    if info is not None:
+        info.append(SweepInfo(*inf))
+    return [ExploreStats(bool(out[8 * i]), *out[8 * i + 1:8 * i + 8]) for i in range(len(configs))]
+
+
+def explore_machine(platform: PlatformConfig, problem: ProblemSpec, params: TuningParams,
+                    max_states: int = 5_000_000) -> ExploreStats:
+    """Every interleaving of one machine (explore.hpp:272-277)."""
+    return explore_configs(platform, problem, [params], max_states)[0]

@@ -1,0 +1,57 @@
+"""GPU interleaving exploration against the reference's exhaustive DFS."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(m, size, kernel):
+    return m.ProblemSpec.abstract(size) if kernel == 0 else m.ProblemSpec.minimum(size)
+
+
+def test_state_counts_equal_reference(engine, gold):
+    """states_visited, transitions_applied, max_depth_reached and the terminal-time
+    range of every configuration equal explore_machine's (explore.json)."""
+    m = engine
+    groups = {}
+    for c in gold("explore.json"):
+        groups.setdefault((tuple(c["plat"]), c["size"], c["kernel"]), []).append(c)
+    for (plat, size, kernel), cases in groups.items():
+        cfgs = [m.TuningParams(c["wg"], c["ts"]) for c in cases]
+        got = m.explore_configs(m.PlatformConfig(*plat), problem(m, size, kernel), cfgs)
+        for c, g in zip(cases, got):
+            key = (plat, size, kernel, c["wg"], c["ts"])
+            assert g.complete and g.deadlocks == 0, key
+            assert g.states_visited == c["states"], key
+            assert g.transitions_applied == c["transitions"], key
+            assert g.max_depth_reached == c["max_depth"], key
+            assert (g.min_time, g.max_time) == (c["min_time"], c["max_time"]), key
+            assert g.terminals == c["n_terminal"], key
+
+
+def test_each_config_alone_equals_batched(engine):
+    m = engine
+    plat, prob = m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(16)
+    cfgs = m.enumerate_configs(16)
+    batched = m.explore_configs(plat, prob, cfgs)
+    for c, b in zip(cfgs, batched):
+        assert m.explore_machine(plat, prob, c) == b
+
+
+def test_larger_spaces_against_oracle(engine, oracle):
+    m = engine
+    for plat, size, kernel, wg, ts in [((1, 1, 4, 4), 32, 0, 16, 2), ((1, 1, 8, 2), 16, 0, 8, 2),
+                                       ((2, 1, 2, 4), 32, 0, 2, 2), ((1, 2, 4, 3), 32, 1, 8, 2),
+                                       ((1, 1, 4, 4), 64, 1, 32, 2)]:
+        g = m.explore_machine(m.PlatformConfig(*plat), problem(m, size, kernel),
+                              m.TuningParams(wg, ts))
+        o = oracle.explore(plat, size, kernel, wg, ts)
+        assert (g.states_visited, g.transitions_applied, g.max_depth_reached, g.min_time,
+                g.max_time) == (o["states"], o["transitions"], o["max_depth"], o["min_time"],
+                                o["max_time"]), (plat, size, kernel, wg, ts)
+
+
+def test_state_limit_is_reported(engine):
+    m = engine
+    r = m.explore_machine(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(32),
+                          m.TuningParams(16, 2), max_states=1000)
+    assert not r.complete
