@@ -40,7 +40,7 @@ def test_each_config_alone_equals_batched(engine):
 def test_larger_spaces_against_oracle(engine, oracle):
     m = engine
     for plat, size, kernel, wg, ts in [((1, 1, 4, 4), 32, 0, 16, 2), ((1, 1, 8, 2), 16, 0, 8, 2),
-                                       ((2, 1, 2, 4), 32, 0, 2, 2), ((1, 2, 4, 3), 32, 1, 8, 2),
+                                       ((2, 1, 2, 4), 16, 0, 2, 2), ((1, 2, 4, 3), 32, 1, 8, 2),
                                        ((1, 1, 4, 4), 64, 1, 32, 2)]:
         g = m.explore_machine(m.PlatformConfig(*plat), problem(m, size, kernel),
                               m.TuningParams(wg, ts))
