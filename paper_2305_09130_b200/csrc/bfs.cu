@@ -95,73 +95,128 @@ __device__ void note_terminal(BfsStats& st, long long time) {
     atomicMax(&st.max_time, time);
 }
 
-__global__ void __launch_bounds__(256) bfs_kernel(BfsArgs a) {
-    cg::grid_group grid = cg::this_grid();
-    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    MState s, t;
-    Transition en[kMaxEnabled];
-    uint32_t key[kMaxWords];
-    for (uint64_t level = 0;; ++level) {
-        const int cur = (int)(level % 3), nxt = (int)((level + 1) % 3), old = (int)((level + 2) % 3);
-        const uint64_t n = *(volatile unsigned long long*)&a.counters[cur];
-        // errors raised during level L-1 (written before the last grid barrier)
-        if (n == 0 || *(volatile int*)&a.errflag[(level + 1) & 1]) break;
-        int* err_now = &a.errflag[level & 1];
-        if (tid == 0) a.counters[old] = 0;
-        const uint32_t* fr = a.frontier[level & 1];
-        uint32_t* fw = a.frontier[(level + 1) & 1];
-        for (uint64_t j = tid; j < n; j += nthreads) {
-            const uint64_t slot = fr[j];
-            const uint32_t* src = a.keys + slot * (uint64_t)a.words;
-            const int cfg = peek_cfg(src, a.descs[0].l.cfg);
-            const BfsDesc& d = a.descs[cfg];
-            unpack(d, src, s);
-            const int ne = enabled(d.m, s, en);
-            BfsStats& st = a.stats[cfg];
-            if (ne == 0) {
-                if (is_terminal(d.m, s)) note_terminal(st, s.time);
-                else {
+constexpr int kBfsThreads = 512;
+constexpr uint64_t kNarrow = 2 * (kBfsThreads / 32);  // frontier handled by one CTA
+
+// Expands frontier entries [warp, n) with stride `nwarps`: one warp per state,
+// one lane per enabled transition.  Successor slots are appended to `fw`
+// through one warp-aggregated atomicAdd per 32 successors.
+__device__ void expand_level(const BfsArgs& a, const uint32_t* fr, uint32_t* fw, uint64_t n,
+                             unsigned long long* next_count, int* err_now, uint64_t warp,
+                             uint64_t nwarps, MState& s, MState& t, Transition* en,
+                             uint32_t* key) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t j = warp; j < n; j += nwarps) {
+        const uint64_t slot = fr[j];
+        const uint32_t* src = a.keys + slot * (uint64_t)a.words;
+        const int cfg = peek_cfg(src, a.descs[0].l.cfg);
+        const BfsDesc& d = a.descs[cfg];
+        unpack(d, src, s);
+        const int ne = enabled(d.m, s, en);
+        BfsStats& st = a.stats[cfg];
+        if (ne == 0) {
+            if (lane == 0) {
+                if (is_terminal(d.m, s)) {
+                    note_terminal(st, s.time);
+                } else {
                     atomicAdd(&st.deadlocks, 1ull);
                     atomicExch(a.error, 3);
                     atomicExch(err_now, 1);
                 }
-                continue;
             }
-            atomicAdd(&st.transitions, (unsigned long long)ne);
-            for (int e = 0; e < ne; ++e) {
+            continue;
+        }
+        if (lane == 0) atomicAdd(&st.transitions, (unsigned long long)ne);
+        for (int base = 0; base < ne; base += 32) {
+            const int e = base + lane;
+            long long ins = -1;
+            if (e < ne) {
                 copy_state(d.m, t, s);
                 if (!apply(d.m, t, en[e])) {
                     atomicExch(a.error, 3);
                     atomicExch(err_now, 1);
-                    break;
+                } else {
+                    pack(d, cfg, t, key);
+                    for (int k = d.l.words; k < a.words; ++k) key[k] = 0;
+                    ins = table_insert(a, key, hash_words(key, a.words));
+                    if (ins == -2) {
+                        atomicExch(a.error, 1);
+                        atomicExch(err_now, 1);
+                    }
                 }
-                pack(d, cfg, t, key);
-                for (int k = d.l.words; k < a.words; ++k) key[k] = 0;
-                const long long ins = table_insert(a, key, hash_words(key, a.words));
-                if (ins == -1) continue;
-                if (ins == -2) {
-                    atomicExch(a.error, 1);
+            }
+            const bool fresh = ins >= 0;
+            const unsigned mask = __ballot_sync(0xffffffffu, fresh);
+            if (!mask) continue;
+            unsigned long long pos0 = 0;
+            const int leader = __ffs(mask) - 1;
+            if (lane == leader) {
+                const unsigned cnt = __popc(mask);
+                pos0 = atomicAdd(next_count, (unsigned long long)cnt);
+                atomicAdd(&st.states, (unsigned long long)cnt);
+                const unsigned long long total = atomicAdd(a.inserted, (unsigned long long)cnt) + cnt;
+                if (total > a.max_states || pos0 + cnt > a.frontier_cap) {
+                    atomicExch(a.error, pos0 + cnt > a.frontier_cap ? 2 : 1);
                     atomicExch(err_now, 1);
-                    break;
                 }
-                atomicAdd(&st.states, 1ull);
-                const unsigned long long total = atomicAdd(a.inserted, 1ull) + 1;
-                if (total > a.max_states) {
-                    atomicExch(a.error, 1);
-                    atomicExch(err_now, 1);
-                }
-                const unsigned long long pos = atomicAdd(&a.counters[nxt], 1ull);
-                if (pos >= a.frontier_cap) {
-                    atomicExch(a.error, 2);
-                    atomicExch(err_now, 1);
-                    break;
-                }
-                fw[pos] = (uint32_t)ins;
+            }
+            pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+            if (fresh) {
+                const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1));
+                if (pos < a.frontier_cap) fw[pos] = (uint32_t)ins;
             }
         }
+    }
+}
+
+__global__ void __launch_bounds__(kBfsThreads) bfs_kernel(BfsArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kBfsThreads / 32);
+    const uint64_t warp = (uint64_t)blockIdx.x * (kBfsThreads / 32) + (threadIdx.x >> 5);
+    const bool t0 = blockIdx.x == 0 && threadIdx.x == 0;
+    MState s, t;
+    Transition en[kMaxEnabled];
+    uint32_t key[kMaxWords];
+    __shared__ unsigned long long narrow_level;
+    uint64_t level = 0;
+    for (;;) {
+        const int cur = (int)(level % 3);
+        const uint64_t n = *(volatile unsigned long long*)&a.counters[cur];
+        // errors raised in the previous level (written before the last grid barrier;
+        // the current level's flag may already be written by faster warps)
+        if (n == 0 || *(volatile int*)&a.errflag[(level + 1) & 1]) break;
+        if (n <= kNarrow) {
+            // narrow frontier: CTA 0 sweeps levels with block barriers only
+            if (blockIdx.x == 0) {
+                uint64_t lv = level, m = n;
+                for (;;) {
+                    const int c = (int)(lv % 3), x = (int)((lv + 1) % 3), o = (int)((lv + 2) % 3);
+                    if (threadIdx.x == 0) a.counters[o] = 0;
+                    expand_level(a, a.frontier[lv & 1], a.frontier[(lv + 1) & 1], m,
+                                 &a.counters[x], &a.errflag[lv & 1], threadIdx.x >> 5,
+                                 kBfsThreads / 32, s, t, en, key);
+                    __syncthreads();
+                    ++lv;
+                    m = *(volatile unsigned long long*)&a.counters[x];
+                    const bool err = *(volatile int*)&a.errflag[0] || *(volatile int*)&a.errflag[1];
+                    __syncthreads();
+                    if (m == 0 || m > kNarrow || err) break;
+                }
+                if (threadIdx.x == 0) narrow_level = lv;
+                __syncthreads();
+                if (threadIdx.x == 0) *a.levels = lv;
+            }
+            grid.sync();
+            level = *(volatile unsigned long long*)a.levels;
+            continue;
+        }
+        if (t0) a.counters[(level + 2) % 3] = 0;
+        expand_level(a, a.frontier[level & 1], a.frontier[(level + 1) & 1], n,
+                     &a.counters[(level + 1) % 3], &a.errflag[level & 1], warp, nwarps, s, t, en,
+                     key);
         grid.sync();
-        if (tid == 0) *a.levels = level + 1;
+        ++level;
+        if (t0) *a.levels = level;
     }
 }
 
@@ -274,9 +329,9 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, BfsResult* res, cuda
     int dev = 0, sms = 0, per_sm = 0;
     MCTB_CUDA(cudaGetDevice(&dev));
     MCTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, 256, 0));
+    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, kBfsThreads, 0));
     if (per_sm < 1) per_sm = 1;
-    const dim3 grid((unsigned)(sms * per_sm)), block(256);
+    const dim3 grid((unsigned)(sms * per_sm)), block(kBfsThreads);
     void* params[] = {&a};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
