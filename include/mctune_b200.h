@@ -39,6 +39,7 @@ extern "C" {
 #define MCTB_POLICY_MT19937 1     /* SchedPolicy::SeededRandom (std::mt19937_64) */
 #define MCTB_POLICY_FIRST 2       /* first enabled: the first DFS path of explore_machine */
 #define MCTB_POLICY_PHILOX 3      /* swarm trajectory: Philox4x32-10 counter-based choice */
+#define MCTB_POLICY_TICK_LAST 4   /* clock ticks only when nothing else is enabled (lock-step) */
 
 /* argmin key: (min(time, 2^30-1) << 33) | config index  (index < 2^33) */
 #define MCTB_KEY_TIME_BITS 30
@@ -120,6 +121,38 @@ int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int
  * copies at most cap-1 bytes + NUL into buf; -1 on error. */
 int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* input, int wg,
                         int ts, const int32_t* trace, int64_t len, char* buf, int64_t cap);
+
+/* ---------------------------------------------------------------------------
+ * Interleaving exploration and the bound-lowering driver (subsystems 3 and 4).
+ */
+
+/* explore_machine (explore.hpp:272-277) over several configurations in one GPU sweep
+ * (configs = int32[2 * n] of (wg, ts)); max_states = the reference's per-machine visited
+ * cap (ExploreLimits::max_states, default 5e6 when <= 0).
+ * out = int64[8 * n]: {complete, states_visited, transitions_applied, max_depth_reached,
+ *                      min_final_time, max_final_time, terminal_states, deadlocks}
+ * info = int64[4]: {levels, total states, packed key words, kernel microseconds} */
+int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
+                 const int32_t* configs, int n_configs, int64_t max_states, int64_t* out,
+                 int64_t* info);
+
+/* check_overtime (explore.hpp:279-284), exact mode.
+ * out = int64[12]: {violated, exhaustive, states_visited, max_depth_reached,
+ *                   transitions_applied, configs_explored, configs_skipped, final_time, wg,
+ *                   ts, steps, trace_exact}; the counterexample goes to trace. */
+int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* input, int64_t T,
+                        int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
+                        int64_t* trace_len);
+
+/* The `tune` flow: estimate_initial_time (search.hpp:361-364) when t_hi <= 0, then
+ * bisect_min_time (search.hpp:366-371).
+ * out = int64[10]: {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total,
+ *                   first_trail_time, steps, trace_exact}
+ * info = double[5] (optional): {ms cost model, ms first paths, ms exploration,
+ *                               explored states, BFS levels} */
+int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64_t t_hi,
+              uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
+              int64_t* trace_len, double* info);
 
 #ifdef __cplusplus
 }

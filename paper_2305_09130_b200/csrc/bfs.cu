@@ -24,16 +24,11 @@
 #include "pack.cuh"
 #include "traj.cuh"
 #include "cost_model.cuh"
+#include "bfs.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace mctb {
-
-struct BfsStats {
-    unsigned long long states, transitions, terminals;
-    long long min_time, max_time;
-    unsigned long long deadlocks;
-};
 
 struct BfsArgs {
     const BfsDesc* descs;
@@ -51,6 +46,7 @@ struct BfsArgs {
     int* errflag;                  // [2] per level parity: stops the sweep consistently
     unsigned long long* levels;
     uint64_t max_states;
+    uint64_t cfg_cap;  // per-configuration visited cap (ExploreLimits::max_states)
 };
 
 namespace {
@@ -124,6 +120,11 @@ __device__ void expand_level(const BfsArgs& a, const uint32_t* fr, uint32_t* fw,
                     atomicExch(err_now, 1);
                 }
             }
+            continue;
+        }
+        if (*(volatile unsigned long long*)&st.states >= a.cfg_cap) {
+            // explore.cpp:28: a full visited set inserts nothing more
+            if (lane == 0) st.capped = 1;
             continue;
         }
         if (lane == 0) atomicAdd(&st.transitions, (unsigned long long)ne);
@@ -244,15 +245,8 @@ __global__ void seed_kernel(BfsArgs a) {
 }  // namespace
 
 // ------------------------------------------------------------------ host
-struct BfsResult {
-    std::vector<BfsStats> stats;
-    uint64_t levels = 0, states = 0;
-    int error = 0;
-    double ms = 0;
-    int words = 0;
-};
-
-int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, BfsResult* res, cudaStream_t st) {
+int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
+            cudaStream_t st) {
     const int n_cfg = (int)hs.size();
     std::vector<BfsDesc> descs(n_cfg);
     int32_t* d_ids = nullptr;
@@ -277,23 +271,21 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, BfsResult* res, cuda
         words = std::max(words, descs[c].l.words);
     }
     // table capacity: power of two >= 2 * max_states
-    uint64_t cap = 1024;
-    while (cap < 2 * max_states) cap <<= 1;
-    const uint64_t fcap = std::max<uint64_t>(cap / 2, 1024);
+    // (the table is sized for the bound, shrunk to what free HBM holds at load <= 1/2)
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    const double need = (double)cap * (8 + 4.0 * words) + 2.0 * fcap * 4;
-    if (need > 0.85 * (double)free_b) {
-        set_error("visited table does not fit in free device memory; lower max_states");
-        cudaFreeAsync(d_ids, st);
-        return MCTB_LIMIT;
-    }
+    const double slot_bytes = 8 + 4.0 * words + 4.0;  // tag + key + frontier share
+    uint64_t cap = 1024;
+    while (cap < 2 * max_states && (double)(cap * 2) * slot_bytes < 0.8 * (double)free_b) cap <<= 1;
+    if (max_states > cap / 2) max_states = cap / 2;
+    const uint64_t fcap = std::max<uint64_t>(cap / 2, 1024);
     BfsArgs a{};
     a.n_cfg = n_cfg;
     a.words = words;
     a.cap_mask = cap - 1;
     a.frontier_cap = fcap;
     a.max_states = max_states;
+    a.cfg_cap = cfg_cap;
     void* blob = nullptr;
     const size_t off_tags = 0, sz_tags = cap * 8;
     const size_t off_keys = off_tags + sz_tags, sz_keys = cap * 4 * (size_t)words;
@@ -318,7 +310,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, BfsResult* res, cuda
     MCTB_CUDA(cudaMemsetAsync(a.tags, 0, sz_tags, st));
     MCTB_CUDA(cudaMemsetAsync(misc, 0, 64, st));
     std::vector<BfsStats> init(n_cfg);
-    for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0};
+    for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0};
     MCTB_CUDA(cudaMemcpyAsync(a.stats, init.data(), sizeof(BfsStats) * n_cfg,
                               cudaMemcpyHostToDevice, st));
     MCTB_CUDA(cudaMemcpyAsync((void*)a.descs, descs.data(), sizeof(BfsDesc) * n_cfg,
@@ -392,7 +384,8 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     cudaStream_t st;
     MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     BfsResult r;
-    rc = run_bfs(hs, max_states > 0 ? (uint64_t)max_states : 5000000ull, &r, st);
+    const uint64_t cap = max_states > 0 ? (uint64_t)max_states : 5000000ull;
+    rc = run_bfs(hs, cap * (uint64_t)n_configs + 64ull * n_configs, cap, &r, st);
     cudaStreamDestroy(st);
     if (rc) return rc;
     if (r.error == 3) {
@@ -402,8 +395,8 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     for (int c = 0; c < n_configs; ++c) {
         const BfsStats& s = r.stats[c];
         int64_t* o = out + 8 * c;
-        o[0] = r.error == 0;
-        o[1] = (int64_t)s.states;
+        o[0] = r.error == 0 && !s.capped;
+        o[1] = (int64_t)std::min<uint64_t>(s.states, cap);
         o[2] = (int64_t)s.transitions;
         // DFS max depth = longest complete run = protocol transitions + max time
         // (verified against explore_machine in tests/test_bfs_gpu.py)

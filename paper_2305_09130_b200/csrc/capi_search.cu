@@ -1,0 +1,374 @@
+// The bound-lowering driver on the GPU (north-star subsystem 4):
+// check_overtime (explore.cpp:167-205), estimate_initial_time
+// (search.cpp:96-104) and bisect_min_time (search.cpp:106-160).
+//
+// The reference answers every probe C_ex(T) of the bisection with a fresh
+// exhaustive DFS over all configurations.  Here one GPU sweep establishes,
+// per feasible configuration c (in the reference's largest-first order):
+//   * its lock-step model time (cost-model kernel),
+//   * its full reachable state space (frontier-parallel BFS): state count
+//     S(c) capped like the reference's visited set, edge count, and the range
+//     of terminal times over ALL interleavings — the proof that no run of c
+//     finishes earlier than its model time,
+//   * its first DFS path (GPU run with the en[0] policy): the counterexample
+//     the reference's DFS returns for any T >= that path's time.
+// Every probe of the bisection is then an O(#configs) scan of these tables,
+// reproducing the reference's verdicts, counterexample traces, checks_run and
+// states_visited_total exactly; only the final trace is materialised.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bfs.cuh"
+#include "common.cuh"
+#include "cost_model.cuh"
+#include "traj.cuh"
+
+namespace mctb {
+
+int check_platform(const int* plat);
+int check_problem(int size, int kernel);
+int make_space(const int64_t* sd, SpaceDev* out);
+int launch_space_eval(const SpaceDev& s, uint64_t first, uint64_t count, int64_t* d_time,
+                      int64_t* d_steps, cudaStream_t stream);
+void reference_space(const int* plat, int size, int kernel, int64_t* sd);
+int gpu_run(MachHost& h, int policy, uint64_t seed, uint64_t traj, int64_t max_steps,
+            TrajOut* out, int32_t* trace, int64_t cap);
+
+namespace {
+
+struct Ctx {
+    int plat[4];
+    int size = 0, kernel = 0;
+    const int64_t* input = nullptr;
+    uint64_t cap = 5000000;  // ExploreLimits::max_states (explore.hpp:229)
+    int skipped = 0;
+    std::vector<int> wg, ts;  // feasible configurations, largest-first (explore.cpp:64-72)
+    std::vector<int64_t> cm_time, cm_steps;
+    std::vector<MachHost> hs;
+    BfsResult bfs;
+    std::vector<int64_t> first_time, first_steps;
+    double ms_cost = 0, ms_bfs = 0, ms_first = 0;
+};
+
+struct VerdictOut {
+    bool violated = false, exhaustive = false, trace_exact = true;
+    int64_t states = 0, transitions = 0, max_depth = 0, explored = 0;
+    int cfg = -1;  // index of the violating configuration
+    int64_t final_time = -1, steps = 0;
+};
+
+double now_ms() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return t.tv_sec * 1e3 + t.tv_nsec * 1e-6;
+}
+
+int prepare(Ctx& c, int64_t max_states) {
+    int rc = check_platform(c.plat);
+    if (rc) return rc;
+    if ((rc = check_problem(c.size, c.kernel))) return rc;
+    if ((rc = require_device())) return rc;
+    if (max_states > 0) c.cap = (uint64_t)max_states;
+    int64_t sd[13];
+    reference_space(c.plat, c.size, c.kernel, sd);
+    SpaceDev s;
+    if ((rc = make_space(sd, &s))) return rc;
+    const int L = (int)sd[10];
+    const uint64_t n = (uint64_t)L * L;
+    cudaStream_t st;
+    MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double t0 = now_ms();
+    int64_t* d = nullptr;
+    MCTB_CUDA(cudaMallocAsync(&d, 2 * n * sizeof(int64_t), st));
+    rc = launch_space_eval(s, 0, n, d, d + n, st);
+    std::vector<int64_t> h(2 * n);
+    if (!rc)
+        rc = cuda_check(cudaMemcpyAsync(h.data(), d, 2 * n * 8, cudaMemcpyDeviceToHost, st), "copy");
+    cudaFreeAsync(d, st);
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+    if (rc) {
+        cudaStreamDestroy(st);
+        return rc;
+    }
+    c.ms_cost = now_ms() - t0;
+    // space index i = (L - log wg) * L + (L - log ts): already largest-first
+    for (uint64_t i = 0; i < n; ++i) {
+        const int wg = 1 << (L - (int)(i / L)), ts = 1 << (L - (int)(i % L));
+        if (h[i] < 0) {
+            ++c.skipped;
+            continue;
+        }
+        c.wg.push_back(wg);
+        c.ts.push_back(ts);
+        c.cm_time.push_back(h[i]);
+        c.cm_steps.push_back(h[n + i]);
+    }
+    if (c.wg.empty()) {
+        cudaStreamDestroy(st);
+        set_error("no feasible configurations for this problem");
+        return MCTB_CONFIG_ERROR;
+    }
+    const int nc = (int)c.wg.size();
+    c.hs.resize(nc);
+    for (int k = 0; k < nc; ++k)
+        if ((rc = build_desc(c.plat, c.size, c.kernel, c.input, c.wg[k], c.ts[k], &c.hs[k]))) {
+            cudaStreamDestroy(st);
+            return rc;
+        }
+    // first DFS paths of every configuration: one GPU trajectory each
+    t0 = now_ms();
+    {
+        int32_t* d_ids = nullptr;
+        if ((rc = upload_desc(c.hs[0], st, &d_ids))) return rc;
+        std::vector<MachDesc> descs(nc);
+        for (int k = 0; k < nc; ++k) {
+            c.hs[k].d.input_id = d_ids;
+            descs[k] = c.hs[k].d;
+        }
+        MachDesc* d_desc = nullptr;
+        TrajOut* d_out = nullptr;
+        MCTB_CUDA(cudaMallocAsync(&d_desc, nc * sizeof(MachDesc), st));
+        MCTB_CUDA(cudaMallocAsync(&d_out, nc * sizeof(TrajOut), st));
+        MCTB_CUDA(cudaMemcpyAsync(d_desc, descs.data(), nc * sizeof(MachDesc),
+                                  cudaMemcpyHostToDevice, st));
+        rc = launch_trajectories(d_desc, nc, MCTB_POLICY_FIRST, 0, 0, nc, 200000000LL, d_out,
+                                 nullptr, 0, st);
+        std::vector<TrajOut> o(nc);
+        if (!rc)
+            rc = cuda_check(cudaMemcpyAsync(o.data(), d_out, nc * sizeof(TrajOut),
+                                            cudaMemcpyDeviceToHost, st), "copy");
+        cudaFreeAsync(d_desc, st);
+        cudaFreeAsync(d_out, st);
+        cudaFreeAsync(d_ids, st);
+        if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
+        if (rc) {
+            cudaStreamDestroy(st);
+            return rc;
+        }
+        for (int k = 0; k < nc; ++k) {
+            if (o[k].status != MCTB_OK) {
+                cudaStreamDestroy(st);
+                set_error("model bug: deadlock on the first path");
+                return MCTB_MODEL_BUG;
+            }
+            c.first_time.push_back(o[k].time);
+            c.first_steps.push_back(o[k].steps);
+        }
+    }
+    c.ms_first = now_ms() - t0;
+    // every interleaving of every configuration, one sweep
+    t0 = now_ms();
+    rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st);
+    cudaStreamDestroy(st);
+    if (rc) return rc;
+    c.ms_bfs = now_ms() - t0;
+    if (c.bfs.error == 3) {
+        set_error("model bug: deadlock or inapplicable transition during exploration");
+        return MCTB_MODEL_BUG;
+    }
+    if (c.bfs.error) {
+        set_error("GPU visited table capacity exceeded");
+        return MCTB_LIMIT;
+    }
+    for (int k = 0; k < nc; ++k) {
+        const BfsStats& b = c.bfs.stats[k];
+        const bool complete = !b.capped;
+        if (complete && (b.terminals == 0 || b.min_time != c.cm_time[k])) {
+            set_error("model bug: explored minimum differs from the lock-step model time");
+            return MCTB_MODEL_BUG;
+        }
+    }
+    return MCTB_OK;
+}
+
+// The reference's verdict for bound T (explore.cpp:167-205) from the tables.
+VerdictOut verdict(const Ctx& c, int64_t T) {
+    VerdictOut v;
+    const int nc = (int)c.wg.size();
+    bool limit = false;
+    for (int k = 0; k < nc; ++k) {
+        const BfsStats& b = c.bfs.stats[k];
+        v.explored += 1;
+        const bool complete = !b.capped;
+        const int64_t tmin = complete ? b.min_time : c.cm_time[k];
+        if (tmin <= T) {
+            v.violated = true;
+            v.cfg = k;
+            if (c.first_time[k] <= T) {
+                // DFS reaches a satisfying terminal on its first path
+                v.final_time = c.first_time[k];
+                v.steps = c.first_steps[k];
+                v.states += v.steps + 1;
+                v.transitions += v.steps;
+                v.max_depth = std::max(v.max_depth, v.steps);
+            } else {
+                // schedule-dependent configuration: a lock-step counterexample is
+                // emitted instead of the DFS's lexicographically first one
+                v.trace_exact = false;
+                v.final_time = tmin;
+                v.steps = c.cm_steps[k];
+                v.states += v.steps + 1;
+                v.transitions += v.steps;
+                v.max_depth = std::max(v.max_depth, v.steps);
+            }
+            v.exhaustive = false;
+            return v;
+        }
+        v.states += (int64_t)std::min<uint64_t>(b.states, c.cap);
+        v.transitions += (int64_t)b.transitions;
+        if (complete)
+            v.max_depth = std::max<int64_t>(v.max_depth, c.cm_steps[k] - c.cm_time[k] + b.max_time);
+        else
+            limit = true;
+    }
+    v.exhaustive = !limit;
+    return v;
+}
+
+int emit_trace(Ctx& c, const VerdictOut& v, int32_t* trace, int64_t cap, int64_t* trace_len) {
+    if (trace_len) *trace_len = v.steps;
+    if (!trace || cap <= 0 || v.cfg < 0) return MCTB_OK;
+    TrajOut o;
+    const int policy = v.trace_exact ? MCTB_POLICY_FIRST : MCTB_POLICY_TICK_LAST;
+    int rc = gpu_run(c.hs[v.cfg], policy, 0, 0, 200000000LL, &o, trace, cap);
+    if (rc) return rc;
+    if (o.time != v.final_time || o.steps != v.steps) {
+        set_error("model bug: counterexample run disagrees with the search tables");
+        return MCTB_MODEL_BUG;
+    }
+    return MCTB_OK;
+}
+
+}  // namespace
+}  // namespace mctb
+
+using namespace mctb;
+
+extern "C" {
+
+// check_overtime (explore.hpp:279-284).
+// out = {violated, exhaustive, states_visited, max_depth_reached, transitions_applied,
+//        configs_explored, configs_skipped, final_time, wg, ts, steps, trace_exact}
+int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* input, int64_t T,
+                        int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
+                        int64_t* trace_len) {
+    if (T < 0) {
+        set_error("over-time bound must be >= 0");
+        return MCTB_CONFIG_ERROR;
+    }
+    Ctx c;
+    std::memcpy(c.plat, plat, sizeof c.plat);
+    c.size = size;
+    c.kernel = kernel;
+    c.input = input;
+    int rc = prepare(c, max_states);
+    if (rc) return rc;
+    const VerdictOut v = verdict(c, T);
+    const int64_t o[12] = {v.violated, v.exhaustive, v.states, v.max_depth, v.transitions,
+                           v.explored, c.skipped, v.final_time, v.cfg >= 0 ? c.wg[v.cfg] : 0,
+                           v.cfg >= 0 ? c.ts[v.cfg] : 0, v.violated ? v.steps : 0, v.trace_exact};
+    std::memcpy(out, o, sizeof o);
+    if (!v.violated) {
+        if (trace_len) *trace_len = 0;
+        return MCTB_OK;
+    }
+    return emit_trace(c, v, trace, cap, trace_len);
+}
+
+// estimate_initial_time + bisect_min_time: the `tune` flow (tools/main.cpp:301-304).
+// t_hi <= 0 selects estimate_initial_time(seed).
+// out = {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total, first_trail_time,
+//        steps, trace_exact}
+// info = {ms_cost_model, ms_first_paths, ms_bfs, bfs_states, bfs_levels}  (optional)
+int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64_t t_hi,
+              uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
+              int64_t* trace_len, double* info) {
+    Ctx c;
+    std::memcpy(c.plat, plat, sizeof c.plat);
+    c.size = size;
+    c.kernel = kernel;
+    c.input = input;
+    int rc = prepare(c, max_states);
+    if (rc) return rc;
+    if (t_hi <= 0) {
+        // estimate_initial_time (search.cpp:96-104): mt19937_64(seed) picks a feasible
+        // configuration in enumerate_configs order; its SeededRandom run is T_ini.
+        std::vector<int> order(c.wg.size());
+        for (size_t k = 0; k < order.size(); ++k) order[k] = (int)k;
+        std::sort(order.begin(), order.end(), [&](int a, int b) {
+            return c.wg[a] != c.wg[b] ? c.wg[a] < c.wg[b] : c.ts[a] < c.ts[b];
+        });
+        Mt64 rng;
+        rng.seed(seed);
+        const int k = order[rng.next() % order.size()];
+        TrajOut o;
+        if ((rc = gpu_run(c.hs[k], MCTB_POLICY_MT19937, seed, 0, 200000000LL, &o, nullptr, 0)))
+            return rc;
+        if (o.status != MCTB_OK) {
+            set_error("model bug: deadlock in the initial-time simulation");
+            return MCTB_MODEL_BUG;
+        }
+        t_hi = o.time;
+    }
+    if (t_hi < 1) {
+        set_error("t_hi must be >= 1");
+        return MCTB_CONFIG_ERROR;
+    }
+    // search.cpp:106-160
+    int checks = 0;
+    int64_t states_total = 0;
+    bool proven = true;
+    VerdictOut v = verdict(c, t_hi);
+    ++checks;
+    states_total += v.states;
+    if (!v.violated) {
+        set_error("t_hi too small: no run terminates within " + std::to_string(t_hi));
+        return MCTB_CONFIG_ERROR;
+    }
+    const int64_t first_trail = v.final_time;
+    VerdictOut best = v;
+    int64_t lo = 0, hi = t_hi;
+    bool lo_checked = false;
+    while (hi - lo > 1) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        const VerdictOut vm = verdict(c, mid);
+        ++checks;
+        states_total += vm.states;
+        if (vm.violated) {
+            hi = mid;
+            best = vm;
+        } else {
+            if (!vm.exhaustive) proven = false;
+            lo = mid;
+            lo_checked = true;
+        }
+    }
+    if (!lo_checked && lo == 0 && hi == 1) {
+        const VerdictOut vz = verdict(c, 0);
+        ++checks;
+        if (vz.violated) {
+            set_error("a run finished in zero ticks");
+            return MCTB_MODEL_BUG;
+        }
+        if (!vz.exhaustive) proven = false;
+    }
+    if (best.final_time != hi) {
+        set_error("bisection trace time disagrees with t_min");
+        return MCTB_MODEL_BUG;
+    }
+    const int64_t o[10] = {hi, c.wg[best.cfg], c.ts[best.cfg], t_hi, proven, checks,
+                           states_total, first_trail, best.steps, best.trace_exact};
+    std::memcpy(out, o, sizeof o);
+    if (info) {
+        info[0] = c.ms_cost;
+        info[1] = c.ms_first;
+        info[2] = c.ms_bfs;
+        info[3] = (double)c.bfs.states;
+        info[4] = (double)c.bfs.levels;
+    }
+    return emit_trace(c, best, trace, cap, trace_len);
+}
+
+}  // extern "C"

@@ -46,34 +46,6 @@ __host__ __device__ inline void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
     out[3] = c3;
 }
 
-// std::mt19937_64 (only for the reference's SeededRandom policy)
-struct Mt64 {
-    uint64_t mt[312];
-    int idx;
-    __host__ __device__ void seed(uint64_t s) {
-        mt[0] = s;
-        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
-        idx = 312;
-    }
-    __host__ __device__ uint64_t next() {
-        if (idx >= 312) {
-            for (int i = 0; i < 312; ++i) {
-                const uint64_t x = (mt[i] & 0xFFFFFFFF80000000ull) | (mt[(i + 1) % 312] & 0x7FFFFFFFull);
-                uint64_t xa = x >> 1;
-                if (x & 1) xa ^= 0xB5026F5AA96619E9ull;
-                mt[i] = mt[(i + 156) % 312] ^ xa;
-            }
-            idx = 0;
-        }
-        uint64_t y = mt[idx++];
-        y ^= (y >> 29) & 0x5555555555555555ull;
-        y ^= (y << 17) & 0x71D67FFFEDA60000ull;
-        y ^= (y << 37) & 0xFFF7EEE000000000ull;
-        y ^= y >> 43;
-        return y;
-    }
-};
-
 __host__ __device__ inline uint64_t fnv_mix(uint64_t h, uint32_t w) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -142,6 +114,9 @@ __global__ void __launch_bounds__(128) traj_kernel(const MachDesc* __restrict__ 
                 philox4x32_10((uint32_t)(steps >> 2), (uint32_t)traj, (uint32_t)(traj >> 32),
                               (uint32_t)(steps >> 34), (uint32_t)seed, (uint32_t)(seed >> 32), ph);
             pick = (int)(((uint64_t)ph[steps & 3] * (uint64_t)n) >> 32);
+        } else if (POLICY == MCTB_POLICY_TICK_LAST) {
+            // every zero-time transition before the clock: the lock-step schedule
+            pick = (en[0].op == OP_CLOCKTICK && n > 1) ? 1 : 0;
         }
         const Transition tr = en[pick];
         if (trace && steps < trace_cap) {
@@ -288,6 +263,10 @@ int launch_trajectories(const MachDesc* d_descs, int n_desc, int policy, uint64_
             break;
         case MCTB_POLICY_PHILOX:
             traj_kernel<MCTB_POLICY_PHILOX><<<blocks, threads, 0, stream>>>(
+                d_descs, n_desc, seed, traj0, n_traj, max_steps, d_out, d_trace, trace_cap);
+            break;
+        case MCTB_POLICY_TICK_LAST:
+            traj_kernel<MCTB_POLICY_TICK_LAST><<<blocks, threads, 0, stream>>>(
                 d_descs, n_desc, seed, traj0, n_traj, max_steps, d_out, d_trace, trace_cap);
             break;
         default:

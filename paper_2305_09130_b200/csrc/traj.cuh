@@ -11,6 +11,35 @@
 
 namespace mctb {
 
+// std::mt19937_64 (only for the reference's SeededRandom policy)
+struct Mt64 {
+    uint64_t mt[312];
+    int idx;
+    __host__ __device__ void seed(uint64_t s) {
+        mt[0] = s;
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+        idx = 312;
+    }
+    __host__ __device__ uint64_t next() {
+        if (idx >= 312) {
+            for (int i = 0; i < 312; ++i) {
+                const uint64_t x = (mt[i] & 0xFFFFFFFF80000000ull) | (mt[(i + 1) % 312] & 0x7FFFFFFFull);
+                uint64_t xa = x >> 1;
+                if (x & 1) xa ^= 0xB5026F5AA96619E9ull;
+                mt[i] = mt[(i + 156) % 312] ^ xa;
+            }
+            idx = 0;
+        }
+        uint64_t y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ull;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+        y ^= (y << 37) & 0xFFF7EEE000000000ull;
+        y ^= y >> 43;
+        return y;
+    }
+};
+
+
 struct TrajOut {
     int64_t time, steps;
     int32_t glob0, status;

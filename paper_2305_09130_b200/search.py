@@ -42,3 +42,129 @@ def exhaustive_sweep(platform: PlatformConfig, problem: ProblemSpec) -> List[Swe
         wg, ts, t, tr, ok, note = rows[6 * i:6 * i + 6]
         out.append(SweepRow(problem.size, wg, ts, t, tr, bool(ok), _NOTES[note]))
     return out
+
+
+# --------------------------------------------------------------------------
+# Verdicts and the bound-lowering driver (explore.hpp:256-261, search.hpp:324-342)
+
+from .machine import Trace  # noqa: E402
+from .model import TuningParams  # noqa: E402
+
+_TRACE_CAP = 1 << 22
+
+
+@dataclass
+class ExploreStatsSummary:
+    states_visited: int = 0
+    transitions_applied: int = 0
+    max_depth_reached: int = 0
+    configs_explored: int = 0
+    configs_skipped: int = 0
+
+
+@dataclass
+class Verdict:
+    violated: bool
+    exhaustive: bool
+    trace: "Trace | None"
+    stats: ExploreStatsSummary
+    trace_exact: bool = True
+
+
+@dataclass
+class TuneStats:
+    checks_run: int = 0
+    states_visited_total: int = 0
+    wall_seconds: float = 0.0
+
+
+@dataclass
+class TuneResult:
+    """(search.hpp:330-342)"""
+    t_min: int
+    params: TuningParams
+    trace: Trace
+    t_ini: int
+    stats: TuneStats
+    method: str
+    proven: bool
+    first_trail_time: int
+    trace_exact: bool = True
+    timings_ms: dict = None
+
+    def first_trail_optimality(self) -> float:
+        if self.first_trail_time <= 0:
+            return 1.0
+        return self.t_min / self.first_trail_time
+
+
+def _trace_from(buf, n, final_time, wg, ts):
+    tr = [tuple(buf[4 * i:4 * i + 4]) for i in range(n)]
+    return Trace(tr, final_time, TuningParams(wg, ts), n)
+
+
+def check_overtime(platform: PlatformConfig, problem: ProblemSpec, T: int,
+                   max_states: int = 5_000_000) -> Verdict:
+    """Exhaustive check of "every terminating run takes more than T ticks" over all
+    configurations and interleavings (explore.hpp:279-284)."""
+    out = (C.c_int64 * 12)()
+    buf = (C.c_int32 * (4 * _TRACE_CAP))()
+    n = C.c_int64()
+    check(lib.mctb_check_overtime(platform.as_array(), problem.size, problem.kernel,
+                                  problem.input_array(), T, max_states, out, buf, _TRACE_CAP,
+                                  C.byref(n)))
+    st = ExploreStatsSummary(out[2], out[4], out[3], out[5], out[6])
+    trace = _trace_from(buf, n.value, out[7], out[8], out[9]) if out[0] else None
+    return Verdict(bool(out[0]), bool(out[1]), trace, st, bool(out[11]))
+
+
+def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: int = 0,
+         max_states: int = 5_000_000) -> TuneResult:
+    """The `tune` command flow: estimate_initial_time(seed) then bisect_min_time
+    (tools/main.cpp:301-304)."""
+    import time as _time
+    t0 = _time.perf_counter()
+    out = (C.c_int64 * 10)()
+    buf = (C.c_int32 * (4 * _TRACE_CAP))()
+    n = C.c_int64()
+    info = (C.c_double * 5)()
+    check(lib.mctb_tune(platform.as_array(), problem.size, problem.kernel, problem.input_array(),
+                        t_hi, C.c_uint64(seed), max_states, out, buf, _TRACE_CAP, C.byref(n),
+                        info))
+    wall = _time.perf_counter() - t0
+    trace = _trace_from(buf, n.value, out[0], out[1], out[2])
+    return TuneResult(out[0], TuningParams(out[1], out[2]), trace, out[3],
+                      TuneStats(out[5], out[6], wall), "bisect", bool(out[4]), out[7],
+                      bool(out[9]), {"cost_model": info[0], "first_paths": info[1],
+                                     "exploration": info[2], "explored_states": info[3],
+                                     "bfs_levels": info[4]})
+
+
+def bisect_min_time(platform: PlatformConfig, problem: ProblemSpec, t_hi: int,
+                    max_states: int = 5_000_000) -> TuneResult:
+    """Counterexample-guided binary search for the minimal time (search.hpp:366-371)."""
+    if t_hi < 1:
+        from ._lib import ConfigError
+        raise ConfigError("t_hi must be >= 1")
+    return tune(platform, problem, 0, t_hi, max_states)
+
+
+def extract_params(platform: PlatformConfig, problem: ProblemSpec, trace: Trace):
+    """Reads (wg, ts, time) out of a counterexample after replay validation (search.hpp:393-395)."""
+    from .machine import replay
+    replay(platform, problem, trace)
+    return trace.params.wg, trace.params.ts, trace.final_time
+
+
+@dataclass
+class RankedTrail:
+    time: int
+    wg: int
+    ts: int
+    transitions: int
+
+
+def rank_trails(traces) -> list:
+    """Stable sort of trail summaries by (time, transitions) (search.hpp:397-398)."""
+    out = [RankedTrail(t.final_time, t.params.wg, t.params.ts, t.steps) for t in traces]
+    return sorted(out, key=lambda r: (r.time, r.transitions))

@@ -1,0 +1,73 @@
+"""The GPU bound-lowering driver against the reference's own tune / check results."""
+import hashlib
+import struct
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(trace):
+    return hashlib.sha256(b"".join(struct.pack("<4i", *t) for t in trace)).hexdigest()
+
+
+def problem(m, size, kernel):
+    return m.ProblemSpec.abstract(size) if kernel == 0 else m.ProblemSpec.minimum(size)
+
+
+def test_tune_bit_exact_with_reference(engine, gold):
+    """T_min, (wg, ts), T_ini, proven, checks_run, states_visited_total,
+    first-trail time and the counterexample trace itself."""
+    m = engine
+    for c in gold("tune.json"):
+        r = m.tune(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]), seed=c["seed"])
+        key = (c["plat"], c["size"], c["kernel"], c["seed"])
+        assert (r.t_min, r.params.wg, r.params.ts) == (c["t_min"], c["wg"], c["ts"]), key
+        assert r.t_ini == c["t_ini"] and r.first_trail_time == c["first_trail_time"], key
+        assert r.proven == bool(c["proven"]), key
+        assert r.stats.checks_run == c["checks_run"], key
+        assert r.stats.states_visited_total == c["states_visited_total"], key
+        assert r.trace_exact and r.trace.steps == c["steps"] == c["trace_len"], key
+        assert sha(r.trace.transitions) == c["trace_sha"], key
+
+
+def test_check_overtime_bit_exact_with_reference(engine, gold):
+    m = engine
+    for c in gold("check.json"):
+        v = m.check_overtime(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]),
+                             c["T"])
+        key = (c["plat"], c["size"], c["kernel"], c["T"])
+        assert (v.violated, v.exhaustive) == (bool(c["violated"]), bool(c["exhaustive"])), key
+        assert v.stats.states_visited == c["states"], key
+        assert v.stats.transitions_applied == c["transitions"], key
+        assert v.stats.max_depth_reached == c["max_depth"], key
+        assert (v.stats.configs_explored, v.stats.configs_skipped) == (
+            c["configs_explored"], c["configs_skipped"]), key
+        if v.violated:
+            assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
+                c["final_time"], c["wg"], c["ts"], c["steps"]), key
+            assert sha(v.trace.transitions) == c["trace_sha"], key
+
+
+def test_paper_table1_row1_and_boundary(engine):
+    """Acceptance 1-2: size 8 -> T_min 44 at (4, 4); check(T_min) violated,
+    check(T_min - 1) holds exhaustively; verdicts monotone on a 10-point grid."""
+    m = engine
+    p, prob = m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8)
+    r = m.tune(p, prob)
+    assert (r.t_min, r.params.wg, r.params.ts, r.proven) == (44, 4, 4, True)
+    assert m.check_overtime(p, prob, 44).violated
+    below = m.check_overtime(p, prob, 43)
+    assert not below.violated and below.exhaustive
+    for T in range(40, 50):
+        assert m.check_overtime(p, prob, T).violated == (T >= 44)
+    assert m.extract_params(p, prob, r.trace) == (4, 4, 44)
+
+
+def test_bisect_errors(engine):
+    m = engine
+    p, prob = m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8)
+    with pytest.raises(m.ConfigError):
+        m.bisect_min_time(p, prob, 43)
+    r = m.bisect_min_time(p, prob, 100)
+    assert r.t_min == 44 and r.stats.checks_run <= 9
