@@ -131,7 +131,7 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
  * cap (ExploreLimits::max_states, default 5e6 when <= 0).
  * out = int64[8 * n]: {complete, states_visited, transitions_applied, max_depth_reached,
  *                      min_final_time, max_final_time, terminal_states, deadlocks}
- * info = int64[4]: {levels, total states, packed key words, kernel microseconds} */
+ * info = int64[4]: {table slots, total states, packed key words, kernel microseconds} */
 int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
                  const int32_t* configs, int n_configs, int64_t max_states, int64_t* out,
                  int64_t* info);

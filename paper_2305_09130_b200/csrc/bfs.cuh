@@ -19,7 +19,7 @@ struct BfsStats {
 
 struct BfsResult {
     std::vector<BfsStats> stats;
-    uint64_t levels = 0, states = 0;
+    uint64_t levels = 0, states = 0, capacity = 0;
     int error = 0;
     double ms = 0;
     int words = 0;

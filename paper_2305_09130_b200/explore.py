@@ -30,7 +30,7 @@ class ExploreStats:
 
 @dataclass
 class SweepInfo:
-    levels: int
+    table_slots: int
     states: int
     key_words: int
     kernel_us: int

@@ -13,6 +13,6 @@ for plat, size, kernel, cfgs in cases:
         print(plat, size, 'ERR', e); continue
     el = time.time() - t0
     st = sum(x.states_visited for x in r)
-    print(plat, size, len(cfgs), 'states', st, 'complete', all(x.complete for x in r), 'levels', info[0].levels,
+    print(plat, size, len(cfgs), 'states', st, 'complete', all(x.complete for x in r), 'slots', info[0].table_slots,
           'words', info[0].key_words, 'kernel_ms', info[0].kernel_us/1e3, 'wall', round(el,3),
           'Mstates/s', round(st/(info[0].kernel_us*1e-6)/1e6, 1), flush=True)
