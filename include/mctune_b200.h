@@ -154,6 +154,16 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
               uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
               int64_t* trace_len, double* info);
 
+/* swarm_min_time (search.hpp:373-379) re-designed as rounds of per_round Philox
+ * trajectories over every feasible configuration (max_rounds bounds the rounds).
+ * out = int64[10]: {t_min, wg, ts, t_ini, rounds, transitions_total, first_trail_time,
+ *                   steps, best_trajectory_id, trajectories_run}
+ * trails (optional) = int64[4 * trails_cap] {time, wg, ts, steps} of round 0. */
+int mctb_swarm(const int* plat, int size, int kernel, const int64_t* input, int64_t per_round,
+               int max_rounds, uint64_t seed, int64_t max_steps, int64_t* out, int32_t* trace,
+               int64_t cap, int64_t* trace_len, int64_t* trails, int64_t trails_cap,
+               int64_t* n_trails);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,7 +14,7 @@ from .machine import (FIRST, MT19937, PHILOX, ROUND_ROBIN, SEEDED_RANDOM, Machin
                       Trace, TrajectoryBatch, replay, trace_to_text, trajectories)
 from .explore import ExploreStats, SweepInfo, explore_configs, explore_machine
 from .search import (RankedTrail, SweepRow, TuneResult, Verdict, bisect_min_time, check_overtime,
-                     exhaustive_sweep, extract_params, rank_trails, tune)
+                     exhaustive_sweep, extract_params, rank_trails, swarm_min_time, tune)
 from .space import KEY_INDEX_BITS, KEY_SAT, KEY_TIME_BITS, Space, SpaceResult, space_argmin
 
 __all__ = [
@@ -25,5 +25,5 @@ __all__ = [
     "exhaustive_sweep", "kernel_kind_from_string", "log2_exact", "space_argmin",
     "validate_params", "FIRST", "MT19937", "PHILOX", "ROUND_ROBIN", "SEEDED_RANDOM", "Machine",
     "RunOutcome", "RankedTrail", "TuneResult", "Verdict", "bisect_min_time", "check_overtime",
-    "extract_params", "rank_trails", "tune", "ExploreStats", "SweepInfo", "explore_configs", "explore_machine", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
+    "extract_params", "rank_trails", "swarm_min_time", "tune", "ExploreStats", "SweepInfo", "explore_configs", "explore_machine", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
 ]

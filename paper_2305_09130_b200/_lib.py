@@ -109,3 +109,6 @@ lib.mctb_check_overtime.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int64, C.c
 lib.mctb_tune.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int64, C.c_uint64, C.c_int64, i64p,
                           i32p, C.c_int64, i64p, C.POINTER(C.c_double)]
 EXPORTED += ["mctb_check_overtime", "mctb_tune"]
+lib.mctb_swarm.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int64, C.c_int, C.c_uint64,
+                           C.c_int64, i64p, i32p, C.c_int64, i64p, i64p, C.c_int64, i64p]
+EXPORTED.append("mctb_swarm")

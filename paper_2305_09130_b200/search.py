@@ -168,3 +168,37 @@ def rank_trails(traces) -> list:
     """Stable sort of trail summaries by (time, transitions) (search.hpp:397-398)."""
     out = [RankedTrail(t.final_time, t.params.wg, t.params.ts, t.steps) for t in traces]
     return sorted(out, key=lambda r: (r.time, r.transitions))
+
+
+def swarm_min_time(platform: PlatformConfig, problem: ProblemSpec, workers: int = 4,
+                   seed: int = 1, trajectories_per_worker: int = 4096, max_rounds: int = 64,
+                   max_depth: int = 4_000_000, trails_out: list | None = None) -> TuneResult:
+    """Randomized search for the minimal time (search.hpp:373-379): rounds of
+    counter-based Philox trajectories on the GPU with the reference's stop rule.
+    Heuristic: never a proof (proven = False)."""
+    import time as _time
+    t0 = _time.perf_counter()
+    per_round = max(1, workers) * trajectories_per_worker
+    if workers < 1:
+        from ._lib import ConfigError
+        raise ConfigError("swarm needs at least one worker")
+    out = (C.c_int64 * 10)()
+    buf = (C.c_int32 * (4 * _TRACE_CAP))()
+    n = C.c_int64()
+    tcap = per_round if trails_out is not None else 0
+    trails = (C.c_int64 * (4 * max(tcap, 1)))()
+    nt = C.c_int64()
+    check(lib.mctb_swarm(platform.as_array(), problem.size, problem.kernel, problem.input_array(),
+                         per_round, max_rounds, C.c_uint64(seed), max_depth, out, buf, _TRACE_CAP,
+                         C.byref(n), trails, tcap, C.byref(nt)))
+    if trails_out is not None:
+        for i in range(nt.value):
+            tm, wg, ts, st = trails[4 * i:4 * i + 4]
+            trails_out.append(Trace([], tm, TuningParams(wg, ts), st))
+    trace = _trace_from(buf, n.value, out[0], out[1], out[2])
+    res = TuneResult(out[0], TuningParams(out[1], out[2]), trace, out[3],
+                     TuneStats(out[4] - 1, out[5], _time.perf_counter() - t0), "swarm", False,
+                     out[6])
+    res.best_trajectory = out[8]
+    res.trajectories = out[9]
+    return res

@@ -71,3 +71,32 @@ def test_bisect_errors(engine):
         m.bisect_min_time(p, prob, 43)
     r = m.bisect_min_time(p, prob, 100)
     assert r.t_min == 44 and r.stats.checks_run <= 9
+
+
+def test_swarm_matches_bisection_at_desk_scale(engine, oracle):
+    """Acceptance 4: the swarm optimum equals bisection's (never below it), its
+    trace replays, and the best trajectory replays on the CPU from its id."""
+    m = engine
+    p = m.PlatformConfig(1, 1, 4, 4)
+    for prob in (m.ProblemSpec.abstract(8), m.ProblemSpec.abstract(16), m.ProblemSpec.minimum(16)):
+        b = m.tune(p, prob)
+        s = m.swarm_min_time(p, prob, workers=4, seed=9)
+        assert s.t_min == b.t_min and not s.proven
+        assert (s.params.wg, s.params.ts) == (b.params.wg, b.params.ts)
+        assert m.replay(p, prob, s.trace)[0] == s.t_min
+        o = oracle.simulate((1, 1, 4, 4), prob.size, prob.kernel, s.params.wg, s.params.ts,
+                            policy=3, seed=9, traj=s.best_trajectory, trace=True)
+        assert o["time"] == s.t_min and [tuple(t) for t in o["trace"]] == s.trace.transitions
+    a = m.swarm_min_time(p, m.ProblemSpec.abstract(8), workers=1, seed=11)
+    b2 = m.swarm_min_time(p, m.ProblemSpec.abstract(8), workers=1, seed=11)
+    assert a.trace.transitions == b2.trace.transitions
+    with pytest.raises(m.ConfigError):
+        m.swarm_min_time(p, m.ProblemSpec.abstract(8), workers=0)
+
+
+def test_rank_trails_contract(engine):
+    m = engine
+    mk = lambda t, wg, ts, st: m.Trace([], t, m.TuningParams(wg, ts), st)  # noqa: E731
+    r = m.rank_trails([mk(50, 2, 2, 10), mk(44, 4, 4, 1700), mk(44, 2, 4, 1650)])
+    assert [(x.time, x.transitions) for x in r] == [(44, 1650), (44, 1700), (50, 10)]
+    assert m.rank_trails([]) == []
