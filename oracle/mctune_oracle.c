@@ -1738,3 +1738,103 @@ int mo_trajectories(const int* plat, int size, int kernel, const int64_t* input,
     free(tr);
     return MO_OK;
 }
+
+/* ------------------------------------------------- successor enumeration
+ * For the multi-rank exploration test (tests/test_distributed.py): states are
+ * exchanged in the reference's canonical serialization (machine.cpp:669-706). */
+static uint64_t get_le(const unsigned char** p, int nbytes) {
+    uint64_t v = 0;
+    for (int i = 0; i < nbytes; ++i) v |= (uint64_t)(*p)[i] << (8 * i);
+    *p += nbytes;
+    return v;
+}
+
+static void deserialize(const machine_t* m, const unsigned char* b, state_t* s) {
+    const unsigned char* p = b;
+    s->time = (int64_t)get_le(&p, 8);
+    s->nrp_work = (int32_t)get_le(&p, 4);
+    s->all_nwe = (int32_t)get_le(&p, 4);
+    s->fin = (int32_t)get_le(&p, 1);
+    s->next_wg = (int32_t)get_le(&p, 4);
+    s->host_pc = (int32_t)get_le(&p, 1);
+    s->host_k = (int32_t)get_le(&p, 4);
+    s->clock = (int32_t)get_le(&p, 1);
+    for (int d = 0; d < m->plan.nwd; ++d) {
+        s->dev[d].pc = (int32_t)get_le(&p, 1);
+        s->dev[d].k = (int32_t)get_le(&p, 4);
+        s->dev[d].batch_base = (int32_t)get_le(&p, 4);
+    }
+    for (int g = 0; g < m->n_units; ++g) {
+        unit_t_* u = &s->unit[g];
+        u->pc = (int32_t)get_le(&p, 1);
+        u->k = (int32_t)get_le(&p, 4);
+        u->nwg = (int32_t)get_le(&p, 4);
+        u->sent = (int32_t)get_le(&p, 4);
+        u->got_items = (int32_t)get_le(&p, 4);
+        u->got_ends = (int32_t)get_le(&p, 4);
+    }
+    for (int g = 0; g < m->n_units; ++g) {
+        s->bar[g].pc = (int32_t)get_le(&p, 1);
+        s->bar[g].count = (int32_t)get_le(&p, 4);
+    }
+    for (int q = 0; q < m->n_pex; ++q) {
+        pex_t_* x = &s->pex[q];
+        x->pc = (int32_t)get_le(&p, 1);
+        x->phase = (int32_t)get_le(&p, 1);
+        x->cursor = (int32_t)get_le(&p, 4);
+        x->busy_left = (int32_t)get_le(&p, 4);
+        x->reported = (int32_t)get_le(&p, 1);
+        x->nwg = (int32_t)get_le(&p, 4);
+        x->iter = (int32_t)get_le(&p, 4);
+    }
+    for (int i = 0; i < m->n_glob; ++i) s->glob[i] = (int64_t)get_le(&p, 8);
+    for (int i = 0; i < m->n_loc; ++i) s->loc[i] = (int64_t)get_le(&p, 8);
+}
+
+/* Serialization of the initial state (ser == NULL) or of every successor of the
+ * serialized state `ser`; out receives n records of `*rec_len` bytes and
+ * fps[i] = hash64 (the reference's fingerprint).  Returns the record count. */
+int64_t mo_successors(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                      const unsigned char* ser, unsigned char* out, int64_t cap, uint64_t* fps,
+                      int64_t* rec_len) {
+    const plat_t p = {plat[0], plat[1], plat[2], plat[3]};
+    machine_t m;
+    if (machine_init(&m, &p, size, kernel, input, wg, ts)) return -1;
+    state_t s, t;
+    state_alloc(&m, &s);
+    state_alloc(&m, &t);
+    initial_state(&m, &s);
+    bytes_t b = {0};
+    int64_t n = 0;
+    if (!ser) {
+        serialize(&m, &s, &b);
+        *rec_len = (int64_t)b.n;
+        if (cap >= 1) {
+            memcpy(out, b.b, b.n);
+            fps[0] = hash64(b.b, b.n);
+        }
+        n = 1;
+    } else {
+        deserialize(&m, ser, &s);
+        tvec en = {0};
+        enabled(&m, &s, &en);
+        for (int i = 0; i < en.n; ++i) {
+            state_copy(&m, &t, &s);
+            apply(&m, &t, &en.v[i]);
+            serialize(&m, &t, &b);
+            *rec_len = (int64_t)b.n;
+            if (n < cap) {
+                memcpy(out + n * b.n, b.b, b.n);
+                fps[n] = hash64(b.b, b.n);
+            }
+            ++n;
+        }
+        free(en.v);
+    }
+    free(b.b);
+    state_free(&s);
+    state_free(&t);
+    const int bug = m.bug;
+    machine_free(&m);
+    return bug ? -1 : n;
+}

@@ -90,6 +90,12 @@ int mo_trajectories(const int* plat, int size, int kernel, const int64_t* input,
                     const int32_t* configs, int n_configs, int policy, uint64_t seed,
                     uint64_t traj0, uint64_t n, int64_t* out);
 
+/* Initial state (ser == NULL) or successors of a serialized state, in the reference's
+ * canonical serialization, with the reference's fingerprints (test helper). */
+int64_t mo_successors(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                      const unsigned char* ser, unsigned char* out, int64_t cap, uint64_t* fps,
+                      int64_t* rec_len);
+
 /* Philox4x32-10 (Salmon et al., SC'11), counter (c0..c3), key (k0,k1) -> out[4] */
 void mo_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out);
 

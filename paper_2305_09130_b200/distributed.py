@@ -1,0 +1,104 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed).
+
+* `sharded_space_argmin`: the configuration index space shards across ranks
+  with no data-path collective; the winner is one all-reduce(MIN) of the
+  packed int64 key ((time << 33) | index < 2^63, so signed MIN is exact).
+* `partitioned_explore`: hash-partitioned frontier exploration.  Rank r owns
+  the states whose fingerprint % world == r; each round every rank expands
+  its local frontier, buckets the successors by owner and exchanges them with
+  one all_to_all, then inserts what it owns into its visited set.  The sweep
+  ends when no rank discovered a new state (all-reduce SUM == 0).
+
+The evaluators are injected so the same exchange logic runs over NCCL with
+the GPU kernels and over gloo with CPU checkers in tests/test_distributed.py.
+"""
+from __future__ import annotations
+
+from typing import Callable, Hashable, Iterable, List, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+KEY_INDEX_BITS = 33
+
+
+def shard(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous index range [first, first+count) of `rank` (balanced to +-1)."""
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def sharded_space_argmin(total: int, local_argmin: Callable[[int, int], int],
+                         group=None, device: str = "cpu") -> Tuple[int, int, int]:
+    """Global (key, time, index) of a space of `total` configurations.
+    local_argmin(first, count) -> packed key of the rank's shard (2^63 = none)."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    first, count = shard(total, rank, world)
+    key = local_argmin(first, count) if count else (1 << 62)
+    t = torch.tensor([min(key, (1 << 63) - 1)], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    k = int(t.item())
+    return k, k >> KEY_INDEX_BITS, k & ((1 << KEY_INDEX_BITS) - 1)
+
+
+def owner(fingerprint: int, world: int) -> int:
+    return fingerprint % world
+
+
+def partitioned_explore(initial: Iterable[Tuple[int, Hashable]],
+                        expand: Callable[[Hashable], Sequence[Tuple[int, Hashable]]],
+                        encode: Callable[[Hashable], List[int]],
+                        decode: Callable[[List[int]], Hashable],
+                        width: int, group=None) -> Tuple[int, int]:
+    """Counts the states reachable from `initial` with hash-partitioned ownership.
+
+    initial / expand yield (fingerprint, state); encode/decode map a state to a
+    fixed-width list of ints (the packed words) for the exchange.  Returns
+    (states owned by this rank, global state count)."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    visited = set()
+    frontier = []
+    for fp, s in initial:
+        if owner(fp, world) == rank and s not in visited:
+            visited.add(s)
+            frontier.append(s)
+    while True:
+        buckets: List[List[int]] = [[] for _ in range(world)]
+        for s in frontier:
+            for fp, succ in expand(s):
+                buckets[owner(fp, world)].extend([fp & ((1 << 63) - 1)] + encode(succ))
+        # exchange sizes, then payloads (one all_to_all each)
+        send_counts = torch.tensor([len(b) for b in buckets], dtype=torch.int64)
+        recv_counts = torch.empty(world, dtype=torch.int64)
+        if world > 1:
+            dist.all_to_all_single(recv_counts, send_counts, group=group)
+        else:
+            recv_counts.copy_(send_counts)
+        send = torch.tensor([v for b in buckets for v in b], dtype=torch.int64)
+        recv = torch.empty(int(recv_counts.sum()), dtype=torch.int64)
+        if world > 1:
+            dist.all_to_all_single(recv, send, output_split_sizes=recv_counts.tolist(),
+                                   input_split_sizes=send_counts.tolist(), group=group)
+        else:
+            recv = send
+        vals = recv.tolist()
+        frontier = []
+        rec = 1 + width
+        for i in range(0, len(vals), rec):
+            s = decode(vals[i + 1:i + rec])
+            if s not in visited:
+                visited.add(s)
+                frontier.append(s)
+        new = torch.tensor([len(frontier)], dtype=torch.int64)
+        if world > 1:
+            dist.all_reduce(new, op=dist.ReduceOp.SUM, group=group)
+        if int(new.item()) == 0:
+            break
+    total = torch.tensor([len(visited)], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
+    return len(visited), int(total.item())
