@@ -287,12 +287,16 @@ def run_b200(args):
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_value = world * PER_RANK * args.steps / e2e_tot.item()
 
-    # ---- roofline of the cost-model kernel: integer issue vs the measured INT32 peak
-    peak_ops, _ = C.c_double(), C.c_double()
-    lib.mctb_int32_peak(C.byref(peak_ops), C.byref(_))
+    # ---- roofline of the cost-model kernel: integer issue (thread instructions per
+    # second) against the chip's issue peak, 148 SMs x 4 SMSPs x 32 lanes x SM clock
+    probe_ops, _ = C.c_double(), C.c_double()
+    lib.mctb_int32_peak(C.byref(probe_ops), C.byref(_))
     kern_avg_s = statistics.mean(kern_ms) * 1e-3
     ops_per_cfg = INT_OPS_PER_CONFIG
     achieved = PER_RANK * ops_per_cfg / kern_avg_s
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    clk_mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    peak_issue = sms * 128 * clk_mhz * 1e6
 
     if rank == 0:
         line = {
@@ -309,11 +313,14 @@ def run_b200(args):
                     "d2h_bytes_per_step": 8 + 8 * 8},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "int32", "achieved": achieved / 1e12,
-                         "peak": peak_ops.value / 1e12, "unit": "Tops/s",
-                         "frac": achieved / peak_ops.value, "traffic": None,
+                         "peak": peak_issue / 1e12, "unit": "Tops/s",
+                         "frac": achieved / peak_issue, "traffic": None,
                          "kernel": "space_argmin_kernel<0>", "kernel_ms": statistics.mean(kern_ms),
                          "ops_per_config": ops_per_cfg,
-                         "peak_source": "measured: mctb_int32_peak IMAD+LOP3 probe, same run"},
+                         "peak_source": "nominal INT32 issue rate at the sampled SM clock "
+                                        f"({sms} SMs x 128 lanes x {clk_mhz:.0f} MHz); not in "
+                                        "MEASURED_PEAKS.json",
+                         "probe_peak": probe_ops.value / 1e12},
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -328,10 +335,10 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
-# SASS instructions (thread level) per configuration of the nd-loop body of
-# space_argmin_kernel<0> (cuobjdump: 136 instructions for a 4x-unrolled body),
-# see DESIGN.md §4 and profiles/.
-INT_OPS_PER_CONFIG = 34
+# Thread-level instructions executed per configuration by space_argmin_kernel<0>
+# on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
+# (profiles/r01_argmin_ncu.txt).  Re-measured after every kernel change.
+INT_OPS_PER_CONFIG = 45.3
 
 
 def main():

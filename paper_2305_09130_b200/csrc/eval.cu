@@ -96,16 +96,36 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                 const uint32_t D32 = (uint32_t)D;
                 uint32_t nd = (uint32_t)sd.nd_lo + nd_d;
                 const uint64_t base = first + pos;
-                for (uint32_t k = 0; k < run; ++k, ++nd) {
-                    const uint32_t nwd = q == 0 ? 1u : (nd >= nd_thr ? q : nd);
-                    const uint32_t waves = (dr + nwd - 1) / nwd;
+                // waves = ceil(dr / nwd) with nwd = nd below nd_thr (one working device per
+                // workgroup batch) and nwd = q above it.  Below nd_thr the quotient is
+                // strength-reduced along the nd digit: dr = Q*nd + R, and nd -> nd+1 gives
+                // R -= Q (one correction Q -= 1, R += nd+1 when R < 0 and Q <= nd+1, a real
+                // division otherwise), so the loop issues no XU (I2F/MUFU/F2I) work.
+                const uint32_t w_hi = q == 0 ? dr : (dr + q - 1) / q;
+                uint32_t Q = dr / nd;
+                int32_t R = (int32_t)(dr - Q * nd);
+                uint32_t best_k = 0xffffffffu;
+                for (uint32_t k = 0; k < run; ++k) {
+                    const uint32_t waves = (q == 0 || nd >= nd_thr) ? w_hi : Q + (R != 0);
                     const uint64_t t = (uint64_t)waves * D32;
                     const uint32_t tf = t < kKeySat ? (uint32_t)t : kKeySat;
                     if (tf < best_tf) {
                         best_tf = tf;
-                        best_idx = base + k;
+                        best_k = k;
+                    }
+                    ++nd;
+                    R -= (int32_t)Q;
+                    if (R < 0) {
+                        if (Q <= nd) {
+                            Q -= 1;
+                            R += (int32_t)nd;
+                        } else {
+                            Q = dr / nd;
+                            R = (int32_t)(dr - Q * nd);
+                        }
                     }
                 }
+                if (best_k != 0xffffffffu) best_idx = base + best_k;
             }
             pos += run;
             // ---- odometer: advance nu, np, ts, wg digits
