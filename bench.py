@@ -337,8 +337,8 @@ def run_b200(args):
 
 # Thread-level instructions executed per configuration by space_argmin_kernel<0>
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
-# (profiles/r01_argmin_ncu.txt).  Re-measured after every kernel change.
-INT_OPS_PER_CONFIG = 45.3
+# (profiles/r01_argmin_v2_ncu.txt).  Re-measured after every kernel change.
+INT_OPS_PER_CONFIG = 27.9
 
 
 def main():
