@@ -134,33 +134,40 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     const int lane = threadIdx.x & 31;
     MState s, t;
     Transition en[kMaxEnabled];
-    uint32_t key[kMaxWords];
+    uint32_t key[kMaxWords], cur[kMaxWords];
+    bool local = false;  // the warp continues with a successor it discovered itself
     for (;;) {
-        unsigned long long h = 0;
-        if (lane == 0) h = atomicAdd(a.head, 1ull);
-        h = __shfl_sync(0xffffffffu, h, 0);
-        if (h >= a.queue_cap) return;
-        // wait until entry h is pushed, or the sweep is over
-        uint32_t slot = kEmpty;
-        if (lane == 0) {
-            unsigned ns = 32;
-            for (;;) {
-                slot = ld_acquire32(&a.queue[h]);
-                if (slot != kEmpty) break;
-                if (ld_relaxed_s64(a.outstanding) <= 0 || *(volatile int*)a.error) break;
-                __nanosleep(ns);
-                if (ns < 1024) ns <<= 1;
+        const uint32_t* src;
+        if (local) {
+            src = cur;
+        } else {
+            unsigned long long h = 0;
+            if (lane == 0) h = atomicAdd(a.head, 1ull);
+            h = __shfl_sync(0xffffffffu, h, 0);
+            if (h >= a.queue_cap) return;
+            // wait until entry h is pushed, or the sweep is over
+            uint32_t slot = kEmpty;
+            if (lane == 0) {
+                unsigned ns = 32;
+                for (;;) {
+                    slot = ld_acquire32(&a.queue[h]);
+                    if (slot != kEmpty) break;
+                    if (ld_relaxed_s64(a.outstanding) <= 0 || *(volatile int*)a.error) break;
+                    __nanosleep(ns);
+                    if (ns < 1024) ns <<= 1;
+                }
             }
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (slot == kEmpty) return;
+            // the key is published before its slot index is pushed
+            src = a.keys + (uint64_t)slot * a.words;
         }
-        slot = __shfl_sync(0xffffffffu, slot, 0);
-        if (slot == kEmpty) return;
-        // the key is published before its slot index is pushed
-        const uint32_t* src = a.keys + (uint64_t)slot * a.words;
         const int cfg = peek_cfg(src, a.cfg_bits);
         const BfsDesc& d = a.descs[cfg];
         unpack(d, src, s);
         const int ne = enabled(d.m, s, en);
         BfsStats& st = a.stats[cfg];
+        bool kept = false;
         if (ne == 0) {
             if (lane == 0) {
                 if (is_terminal(d.m, s)) {
@@ -191,11 +198,28 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                         if (ins == -2) atomicExch(a.error, 1);
                     }
                 }
-                push_fresh(a, ins >= 0, ins, st);
+                bool fresh = ins >= 0;
+                if (!kept) {
+                    // keep the first new successor: no queue round trip on the chain
+                    const unsigned m = __ballot_sync(0xffffffffu, fresh);
+                    if (m) {
+                        const int keeper = __ffs(m) - 1;
+                        for (int k = 0; k < a.words; ++k)
+                            cur[k] = __shfl_sync(0xffffffffu, key[k], keeper);
+                        if (lane == keeper) fresh = false;
+                        if (lane == 0) {
+                            atomicAdd((unsigned long long*)a.outstanding, 1ull);
+                            atomicAdd(&st.states, 1ull);
+                        }
+                        kept = true;
+                    }
+                }
+                push_fresh(a, fresh, ins, st);
             }
         }
         __syncwarp();
         if (lane == 0) atomicAdd((unsigned long long*)a.outstanding, ~0ull);  // -1
+        local = kept;
     }
 }
 
