@@ -21,6 +21,7 @@
 // are explored in the same sweep, tagged by a cfg field of the packed state;
 // per-configuration statistics give the reference's ExploreStats.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -48,6 +49,7 @@ struct BfsArgs {
     BfsStats* stats;  // [n_cfg]
     int* error;       // 1 table full, 2 queue full, 3 model bug
     uint64_t cfg_cap; // per-configuration visited cap (ExploreLimits::max_states)
+    int keep;         // continue with the first new successor (no queue round trip)
 };
 
 namespace {
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     }
                 }
                 bool fresh = ins >= 0;
-                if (!kept) {
+                if (!kept && a.keep) {
                     // keep the first new successor: no queue round trip on the chain
                     const unsigned m = __ballot_sync(0xffffffffu, fresh);
                     if (m) {
@@ -297,6 +299,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.cap_mask = cap - 1;
         a.queue_cap = qcap;
         a.cfg_cap = cfg_cap;
+        a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
         const size_t sz_tags = cap * 8, sz_keys = cap * 4 * (size_t)words, sz_q = qcap * 4;
         const size_t sz_misc = 256 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg;
         void* blob = nullptr;
