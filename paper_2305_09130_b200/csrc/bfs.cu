@@ -84,7 +84,9 @@ __device__ long long table_insert(const BfsArgs& a, const uint32_t* key, uint64_
     const unsigned long long tag = (h | 3ull);
     const unsigned long long claim = tag & ~1ull;
     uint64_t i = h & a.cap_mask;
-    for (uint64_t probe = 0; probe <= a.cap_mask; ++probe, i = (i + 1) & a.cap_mask) {
+    // a probe sequence this long only happens in a table that is too full: report it
+    // (the sweep restarts with a larger table) instead of scanning the whole table
+    for (uint64_t probe = 0; probe < 4096; ++probe, i = (i + 1) & a.cap_mask) {
         unsigned long long t = ld_acquire(&a.tags[i]);
         if (t == 0) {
             const unsigned long long prev = atomicCAS(&a.tags[i], 0ull, claim);
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         }
         __syncwarp();
         if (lane == 0) atomicAdd((unsigned long long*)a.outstanding, ~0ull);  // -1
-        local = kept;
+        local = kept && !*(volatile int*)a.error;
     }
 }
 
@@ -345,7 +347,8 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         cudaEventDestroy(e1);
         cudaFreeAsync(blob, st);
         res->ms = ms;
-        res->states = misc_h[1];
+        res->states = 0;
+        for (const auto& x : res->stats) res->states += x.states;
         res->levels = 0;
         res->error = (int)(misc_h[3] & 0xffffffff);
         res->words = words;
