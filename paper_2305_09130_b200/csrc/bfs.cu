@@ -69,6 +69,18 @@ __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -87,7 +99,9 @@ __device__ long long table_insert(const BfsArgs& a, const uint32_t* key, uint64_
     // a probe sequence this long only happens in a table that is too full: report it
     // (the sweep restarts with a larger table) instead of scanning the whole table
     for (uint64_t probe = 0; probe < 4096; ++probe, i = (i + 1) & a.cap_mask) {
-        unsigned long long t = ld_acquire(&a.tags[i]);
+        // relaxed probe (an acquire load invalidates the SM's L1 — CCTL.IVALL — so it
+        // is only issued on a fingerprint match, before the key words are read)
+        unsigned long long t = ld_relaxed64(&a.tags[i]);
         if (t == 0) {
             const unsigned long long prev = atomicCAS(&a.tags[i], 0ull, claim);
             if (prev == 0) {
@@ -103,7 +117,11 @@ __device__ long long table_insert(const BfsArgs& a, const uint32_t* key, uint64_
             t = prev;
         }
         if ((t | 1ull) != tag) continue;  // different fingerprint
-        while (!(t & 1ull)) t = ld_acquire(&a.tags[i]);  // claimed, key not yet published
+        t = ld_acquire(&a.tags[i]);
+        while (!(t & 1ull)) {  // claimed, key not yet published
+            __nanosleep(32);
+            t = ld_acquire(&a.tags[i]);
+        }
         const uint32_t* src = a.keys + i * (uint64_t)a.words;
         bool eq = true;
         for (int k = 0; k < a.words && eq; ++k) eq = src[k] == key[k];
@@ -152,13 +170,17 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             // wait until entry h is pushed, or the sweep is over
             uint32_t slot = kEmpty;
             if (lane == 0) {
-                unsigned ns = 32;
+                unsigned ns = 64;
                 for (;;) {
-                    slot = ld_acquire32(&a.queue[h]);
-                    if (slot != kEmpty) break;
-                    if (ld_relaxed_s64(a.outstanding) <= 0 || *(volatile int*)a.error) break;
+                    slot = ld_relaxed32(&a.queue[h]);  // relaxed poll: no L1 invalidation
+                    if (slot != kEmpty) {
+                        slot = ld_acquire32(&a.queue[h]);
+                        break;
+                    }
+                    if (ld_relaxed_s64(a.outstanding) <= 0 || ld_relaxed32((const uint32_t*)a.error))
+                        break;
                     __nanosleep(ns);
-                    if (ns < 1024) ns <<= 1;
+                    if (ns < 4096) ns <<= 1;
                 }
             }
             slot = __shfl_sync(0xffffffffu, slot, 0);
