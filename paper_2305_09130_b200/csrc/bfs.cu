@@ -153,9 +153,15 @@ __device__ __forceinline__ void push_fresh(const BfsArgs& a, bool fresh, long lo
 }
 
 __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
-    const int lane = threadIdx.x & 31;
-    MState s, t;
-    Transition en[kMaxEnabled];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    // the parent state and its enabled list live once per warp in shared memory;
+    // each lane keeps only its own successor in (L1-resident) local memory
+    __shared__ MState parent[kBfsThreads / 32];
+    __shared__ Transition enabled_s[kBfsThreads / 32][kMaxEnabled];
+    __shared__ int n_enabled[kBfsThreads / 32];
+    MState& s = parent[wib];
+    Transition* en = enabled_s[wib];
+    MState t;
     uint32_t key[kMaxWords], cur[kMaxWords];
     bool local = false;  // the warp continues with a successor it discovered itself
     for (;;) {
@@ -190,8 +196,12 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         }
         const int cfg = peek_cfg(src, a.cfg_bits);
         const BfsDesc& d = a.descs[cfg];
-        unpack(d, src, s);
-        const int ne = enabled(d.m, s, en);
+        if (lane == 0) {
+            unpack(d, src, s);
+            n_enabled[wib] = enabled(d.m, s, en);
+        }
+        __syncwarp();
+        const int ne = n_enabled[wib];
         BfsStats& st = a.stats[cfg];
         bool kept = false;
         if (ne == 0) {
@@ -302,6 +312,9 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     MCTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, explore_kernel, kBfsThreads, 0));
     if (per_sm < 1) per_sm = 1;
+    // local-memory working set: keep the resident warps' successor states L1-sized
+    if (const char* e = getenv("MCTB_BFS_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(e));
+    else per_sm = std::min(per_sm, 2);
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double slot_bytes = 8 + 4.0 * words + 2.0;  // tag + key + queue (half the slots)

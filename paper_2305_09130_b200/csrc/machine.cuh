@@ -63,7 +63,27 @@ struct Transition {
 struct DevS { int32_t pc, k, batch_base; };
 struct UnitS { int32_t pc, k, nwg, sent, got_items, got_ends; };
 struct BarS { int32_t pc, count; };
-struct PexS { int32_t pc, phase, cursor, busy_left, reported, nwg, iter; };
+// Per-element record, 16 bytes: the element fields are the bulk of a state and
+// the exploration keeps one state per lane, so they are narrow (build_desc
+// rejects configurations whose cursor, busy ticks or rounds exceed 16 bits).
+struct PexS {
+    int16_t pc, phase;
+    uint16_t cursor, busy_left;
+    int16_t reported;
+    uint16_t iter;
+    int32_t nwg;
+};
+__host__ __device__ inline PexS pex_init(int32_t nwg, int iter) {
+    PexS p;
+    p.pc = 0;
+    p.phase = 0;
+    p.cursor = 0;
+    p.busy_left = 0;
+    p.reported = 0;
+    p.iter = (uint16_t)iter;
+    p.nwg = nwg;
+    return p;
+}
 
 struct MState {
     int64_t time;
@@ -179,7 +199,7 @@ __host__ __device__ inline void initial_state(const MachDesc& m, MState& s) {
         s.unit[g] = UnitS{0, 0, 0, 0, 0, 0};
         s.bar[g] = BarS{0, 0};
     }
-    for (int p = 0; p < m.n_pex; ++p) s.pex[p] = PexS{0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < m.n_pex; ++p) s.pex[p] = pex_init(0, 0);
     if (m.kernel == 1)
         for (int i = 0; i < m.n_units * m.np; ++i) s.loc[i] = m.max_id;
 }
@@ -211,7 +231,7 @@ __host__ __device__ inline void place_pex(const MachDesc& m, PexS& px) {
     switch (in.kind) {
         case IK_BUSY:
             px.pc = P_RUN;
-            px.busy_left = in.ticks;
+            px.busy_left = (uint16_t)in.ticks;
             px.reported = 0;
             break;
         case IK_EFFECT:
@@ -450,7 +470,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             PexS& px = s.pex[pord];
             const int iter = un.sent / m.nwe;
             if (px.pc != P_WAITGO || t.arg != iter) return false;
-            px = PexS{0, 0, 0, 0, 0, un.nwg, iter};  // start_activation, machine.cpp:164-172
+            px = pex_init(un.nwg, iter);  // start_activation, machine.cpp:164-172
             place_pex(m, px);
             un.sent += 1;
             if (un.pc == U_ACTIVATEPEX) {
@@ -587,7 +607,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             UnitS& un = s.unit[ord / m.nwe];
             if (un.pc != U_SERVE) return false;
             un.got_items += 1;
-            px = PexS{0, 0, 0, 0, 0, 0, 0};
+            px = pex_init(0, 0);
             if (un.sent < m.wg) un.pc = U_REACTPEX;
             else if (m.kernel == 0 && un.got_items == m.wg) un.pc = U_SENDUNITDONE;
             return true;
@@ -600,7 +620,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (un.pc != U_SERVE) return false;
             un.got_ends += 1;
             if (ord % m.nwe == 0) s.all_nwe -= 1;
-            px = PexS{0, 0, 0, 0, 0, 0, 0};
+            px = pex_init(0, 0);
             if (un.got_ends == m.nwe) un.pc = U_SENDUNITDONE;
             return true;
         }

@@ -206,6 +206,12 @@ int build_desc(const int* plat, int size, int kernel, const int64_t* input, int 
         m.act_len = 2 * ts + 1;
         m.epi_len = 2 * (m.nwe - 1) + 3;
     }
+    const int64_t max_ticks = kernel == 0 ? (int64_t)m.gmt * ts : (int64_t)m.gmt;
+    if (m.act_len >= 65535 || m.epi_len >= 65535 || max_ticks >= 65535 || m.rounds >= 65535) {
+        set_error("configuration exceeds the GPU machine's 16-bit element fields (program "
+                  "length, busy ticks or rounds >= 65535)");
+        return MCTB_LIMIT;
+    }
     if (m.nwd > kMaxDev || m.n_units > kMaxUnit || m.n_pex > kMaxPex ||
         (kernel == 1 && m.n_units * m.np > kMaxLoc)) {
         set_error("configuration exceeds the GPU machine capacity (devices <= 8, units <= 16, "
