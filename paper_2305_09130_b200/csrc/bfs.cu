@@ -177,16 +177,19 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             uint32_t slot = kEmpty;
             if (lane == 0) {
                 unsigned ns = 64;
-                for (;;) {
+                for (unsigned it = 0;; ++it) {
                     slot = ld_relaxed32(&a.queue[h]);  // relaxed poll: no L1 invalidation
                     if (slot != kEmpty) {
                         slot = ld_acquire32(&a.queue[h]);
                         break;
                     }
-                    if (ld_relaxed_s64(a.outstanding) <= 0 || ld_relaxed32((const uint32_t*)a.error))
+                    // the shared counters are read rarely: they are the working warps'
+                    // atomics' cache line
+                    if ((it & 7) == 7 && (ld_relaxed_s64(a.outstanding) <= 0 ||
+                                          ld_relaxed32((const uint32_t*)a.error)))
                         break;
                     __nanosleep(ns);
-                    if (ns < 4096) ns <<= 1;
+                    if (ns < 8192) ns <<= 1;
                 }
             }
             slot = __shfl_sync(0xffffffffu, slot, 0);
@@ -314,7 +317,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     if (per_sm < 1) per_sm = 1;
     // local-memory working set: keep the resident warps' successor states L1-sized
     if (const char* e = getenv("MCTB_BFS_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(e));
-    else per_sm = std::min(per_sm, 2);
+    else per_sm = std::min(per_sm, 4);
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double slot_bytes = 8 + 4.0 * words + 2.0;  // tag + key + queue (half the slots)
