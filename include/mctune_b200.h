@@ -149,7 +149,7 @@ int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* in
  * out = int64[10]: {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total,
  *                   first_trail_time, steps, trace_exact}
  * info = double[5] (optional): {ms cost model, ms first paths, ms exploration,
- *                               explored states, BFS levels} */
+ *                               explored states, ms exploration kernel} */
 int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64_t t_hi,
               uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
               int64_t* trace_len, double* info);

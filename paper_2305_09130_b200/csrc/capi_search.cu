@@ -366,7 +366,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         info[1] = c.ms_first;
         info[2] = c.ms_bfs;
         info[3] = (double)c.bfs.states;
-        info[4] = (double)c.bfs.levels;
+        info[4] = c.bfs.ms;  // exploration kernel time (CUDA events)
     }
     return emit_trace(c, best, trace, cap, trace_len);
 }

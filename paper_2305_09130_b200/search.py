@@ -137,7 +137,7 @@ def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: in
                       TuneStats(out[5], out[6], wall), "bisect", bool(out[4]), out[7],
                       bool(out[9]), {"cost_model": info[0], "first_paths": info[1],
                                      "exploration": info[2], "explored_states": info[3],
-                                     "bfs_levels": info[4]})
+                                     "exploration_kernel": info[4]})
 
 
 def bisect_min_time(platform: PlatformConfig, problem: ProblemSpec, t_hi: int,
