@@ -117,53 +117,59 @@ int prepare(Ctx& c, int64_t max_states) {
             cudaStreamDestroy(st);
             return rc;
         }
-    // first DFS paths of every configuration: one GPU trajectory each
+    // first DFS paths of every configuration (one GPU trajectory each, stream st)
+    // overlapped with the exploration of every interleaving (stream sx)
     t0 = now_ms();
-    {
-        int32_t* d_ids = nullptr;
-        if ((rc = upload_desc(c.hs[0], st, &d_ids))) return rc;
-        std::vector<MachDesc> descs(nc);
-        for (int k = 0; k < nc; ++k) {
-            c.hs[k].d.input_id = d_ids;
-            descs[k] = c.hs[k].d;
-        }
-        MachDesc* d_desc = nullptr;
-        TrajOut* d_out = nullptr;
-        MCTB_CUDA(cudaMallocAsync(&d_desc, nc * sizeof(MachDesc), st));
-        MCTB_CUDA(cudaMallocAsync(&d_out, nc * sizeof(TrajOut), st));
-        MCTB_CUDA(cudaMemcpyAsync(d_desc, descs.data(), nc * sizeof(MachDesc),
-                                  cudaMemcpyHostToDevice, st));
-        rc = launch_trajectories(d_desc, nc, MCTB_POLICY_FIRST, 0, 0, nc, 200000000LL, d_out,
-                                 nullptr, 0, st);
-        std::vector<TrajOut> o(nc);
-        if (!rc)
-            rc = cuda_check(cudaMemcpyAsync(o.data(), d_out, nc * sizeof(TrajOut),
-                                            cudaMemcpyDeviceToHost, st), "copy");
-        cudaFreeAsync(d_desc, st);
-        cudaFreeAsync(d_out, st);
-        cudaFreeAsync(d_ids, st);
-        if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "sync");
-        if (rc) {
-            cudaStreamDestroy(st);
-            return rc;
-        }
-        for (int k = 0; k < nc; ++k) {
-            if (o[k].status != MCTB_OK) {
-                cudaStreamDestroy(st);
-                set_error("model bug: deadlock on the first path");
-                return MCTB_MODEL_BUG;
-            }
-            c.first_time.push_back(o[k].time);
-            c.first_steps.push_back(o[k].steps);
-        }
+    int32_t* d_ids = nullptr;
+    if ((rc = upload_desc(c.hs[0], st, &d_ids))) return rc;
+    std::vector<MachDesc> descs(nc);
+    for (int k = 0; k < nc; ++k) {
+        c.hs[k].d.input_id = d_ids;
+        descs[k] = c.hs[k].d;
     }
+    MachDesc* d_desc = nullptr;
+    TrajOut* d_out = nullptr;
+    TrajOut* h_out = nullptr;
+    MCTB_CUDA(cudaMallocHost(&h_out, nc * sizeof(TrajOut)));
+    MCTB_CUDA(cudaMallocAsync(&d_desc, nc * sizeof(MachDesc), st));
+    MCTB_CUDA(cudaMallocAsync(&d_out, nc * sizeof(TrajOut), st));
+    MCTB_CUDA(cudaMemcpyAsync(d_desc, descs.data(), nc * sizeof(MachDesc), cudaMemcpyHostToDevice,
+                              st));
+    rc = launch_trajectories(d_desc, nc, MCTB_POLICY_FIRST, 0, 0, nc, 200000000LL, d_out, nullptr,
+                             0, st);
+    if (!rc)
+        rc = cuda_check(cudaMemcpyAsync(h_out, d_out, nc * sizeof(TrajOut), cudaMemcpyDeviceToHost,
+                                        st), "copy");
+    cudaEvent_t first_done;
+    cudaEventCreateWithFlags(&first_done, cudaEventDisableTiming);
+    cudaEventRecord(first_done, st);
+    cudaStream_t sx;
+    MCTB_CUDA(cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking));
+    const double t1 = now_ms();
+    if (!rc) rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, sx);
+    c.ms_bfs = now_ms() - t1;
+    cudaStreamDestroy(sx);
+    cudaEventSynchronize(first_done);
+    cudaEventDestroy(first_done);
     c.ms_first = now_ms() - t0;
-    // every interleaving of every configuration, one sweep
-    t0 = now_ms();
-    rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st);
+    cudaFreeAsync(d_desc, st);
+    cudaFreeAsync(d_out, st);
+    cudaFreeAsync(d_ids, st);
+    const int rc2 = cuda_check(cudaStreamSynchronize(st), "sync");
     cudaStreamDestroy(st);
+    if (!rc) rc = rc2;
+    if (!rc)
+        for (int k = 0; k < nc; ++k) {
+            if (h_out[k].status != MCTB_OK) {
+                set_error("model bug: deadlock on the first path");
+                rc = MCTB_MODEL_BUG;
+                break;
+            }
+            c.first_time.push_back(h_out[k].time);
+            c.first_steps.push_back(h_out[k].steps);
+        }
+    cudaFreeHost(h_out);
     if (rc) return rc;
-    c.ms_bfs = now_ms() - t0;
     if (c.bfs.error == 3) {
         set_error("model bug: deadlock or inapplicable transition during exploration");
         return MCTB_MODEL_BUG;

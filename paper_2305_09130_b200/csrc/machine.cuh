@@ -261,12 +261,15 @@ __host__ __device__ inline bool is_terminal(const MachDesc& m, const MState& s) 
 // Machine::enabled, machine.cpp:174-336: every enabled transition, ascending
 // actor pid (the reference's stable sort by actor), emitted per process.
 // Returns the count; `out` may be null (count only).
-__host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Transition* out) {
+// max_out stops the enumeration early (the first path needs en[0] only).
+__host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Transition* out,
+                                      int max_out = 1 << 30) {
     int n = 0;
-    auto push = [&](int actor, int peer, int op, int arg) {
-        if (out) out[n] = Transition{(uint16_t)actor, (uint16_t)peer, op, arg};
-        ++n;
-    };
+#define push(A, P, O, G)                                                          \
+    do {                                                                          \
+        if (out) out[n] = Transition{(uint16_t)(A), (uint16_t)(P), (O), (G)};     \
+        if (++n >= max_out) return n;                                             \
+    } while (0)
     switch (s.host_pc) {
         case H_SENDGO:
         case H_REACTGO:
@@ -354,6 +357,7 @@ __host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Trans
     }
     return n;
 }
+#undef push
 
 // Machine::apply, machine.cpp:361-649, in place.  Returns false when the
 // transition is not enabled (replay divergence) or a model bug is hit.

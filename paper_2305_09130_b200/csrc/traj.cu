@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(128) traj_kernel(const MachDesc* __restrict__ 
     uint64_t h = 0xcbf29ce484222325ull;
     int status = MCTB_OK;
     for (;;) {
-        const int n = enabled(m, s, en);
+        const int n = enabled(m, s, en, POLICY == MCTB_POLICY_FIRST ? 1 : (1 << 30));
         if (n == 0) {
             if (!is_terminal(m, s)) status = MCTB_MODEL_BUG;  // deadlock
             break;

@@ -51,6 +51,15 @@ from .machine import Trace  # noqa: E402
 from .model import TuningParams  # noqa: E402
 
 _TRACE_CAP = 1 << 22
+_TRACE_BUF = None
+
+
+def _trace_buffer():
+    """One reusable host buffer for counterexample traces (allocated once)."""
+    global _TRACE_BUF
+    if _TRACE_BUF is None:
+        _TRACE_BUF = (C.c_int32 * (4 * _TRACE_CAP))()
+    return _TRACE_BUF
 
 
 @dataclass
@@ -108,7 +117,7 @@ def check_overtime(platform: PlatformConfig, problem: ProblemSpec, T: int,
     """Exhaustive check of "every terminating run takes more than T ticks" over all
     configurations and interleavings (explore.hpp:279-284)."""
     out = (C.c_int64 * 12)()
-    buf = (C.c_int32 * (4 * _TRACE_CAP))()
+    buf = _trace_buffer()
     n = C.c_int64()
     check(lib.mctb_check_overtime(platform.as_array(), problem.size, problem.kernel,
                                   problem.input_array(), T, max_states, out, buf, _TRACE_CAP,
@@ -125,7 +134,7 @@ def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: in
     import time as _time
     t0 = _time.perf_counter()
     out = (C.c_int64 * 10)()
-    buf = (C.c_int32 * (4 * _TRACE_CAP))()
+    buf = _trace_buffer()
     n = C.c_int64()
     info = (C.c_double * 5)()
     check(lib.mctb_tune(platform.as_array(), problem.size, problem.kernel, problem.input_array(),
@@ -183,7 +192,7 @@ def swarm_min_time(platform: PlatformConfig, problem: ProblemSpec, workers: int 
         from ._lib import ConfigError
         raise ConfigError("swarm needs at least one worker")
     out = (C.c_int64 * 10)()
-    buf = (C.c_int32 * (4 * _TRACE_CAP))()
+    buf = _trace_buffer()
     n = C.c_int64()
     tcap = per_round if trails_out is not None else 0
     trails = (C.c_int64 * (4 * max(tcap, 1)))()
