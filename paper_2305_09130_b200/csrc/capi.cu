@@ -48,6 +48,18 @@ int require_device() {
         set_error("mctune_b200 is built for sm_100a (B200) only");
         return MCTB_NO_DEVICE;
     }
+    // keep freed stream-ordered allocations (visited tables, queues) in the pool
+    // instead of returning them to the driver at every synchronisation
+    static bool pool_set[64] = {};
+    if (!pool_set[dev & 63]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+        pool_set[dev & 63] = true;
+    }
     return MCTB_OK;
 }
 
