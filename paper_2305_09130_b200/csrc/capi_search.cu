@@ -117,59 +117,15 @@ int prepare(Ctx& c, int64_t max_states) {
             cudaStreamDestroy(st);
             return rc;
         }
-    // first DFS paths of every configuration (one GPU trajectory each, stream st)
-    // overlapped with the exploration of every interleaving (stream sx)
-    t0 = now_ms();
-    int32_t* d_ids = nullptr;
-    if ((rc = upload_desc(c.hs[0], st, &d_ids))) return rc;
-    std::vector<MachDesc> descs(nc);
-    for (int k = 0; k < nc; ++k) {
-        c.hs[k].d.input_id = d_ids;
-        descs[k] = c.hs[k].d;
-    }
-    MachDesc* d_desc = nullptr;
-    TrajOut* d_out = nullptr;
-    TrajOut* h_out = nullptr;
-    MCTB_CUDA(cudaMallocHost(&h_out, nc * sizeof(TrajOut)));
-    MCTB_CUDA(cudaMallocAsync(&d_desc, nc * sizeof(MachDesc), st));
-    MCTB_CUDA(cudaMallocAsync(&d_out, nc * sizeof(TrajOut), st));
-    MCTB_CUDA(cudaMemcpyAsync(d_desc, descs.data(), nc * sizeof(MachDesc), cudaMemcpyHostToDevice,
-                              st));
-    rc = launch_trajectories(d_desc, nc, MCTB_POLICY_FIRST, 0, 0, nc, 200000000LL, d_out, nullptr,
-                             0, st);
-    if (!rc)
-        rc = cuda_check(cudaMemcpyAsync(h_out, d_out, nc * sizeof(TrajOut), cudaMemcpyDeviceToHost,
-                                        st), "copy");
-    cudaEvent_t first_done;
-    cudaEventCreateWithFlags(&first_done, cudaEventDisableTiming);
-    cudaEventRecord(first_done, st);
-    cudaStream_t sx;
-    MCTB_CUDA(cudaStreamCreateWithFlags(&sx, cudaStreamNonBlocking));
+    // every interleaving of every configuration, one sweep.  The first DFS paths
+    // (needed only for the configurations a probe finds violating) run lazily.
     const double t1 = now_ms();
-    if (!rc) rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, sx);
+    rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st);
     c.ms_bfs = now_ms() - t1;
-    cudaStreamDestroy(sx);
-    cudaEventSynchronize(first_done);
-    cudaEventDestroy(first_done);
-    c.ms_first = now_ms() - t0;
-    cudaFreeAsync(d_desc, st);
-    cudaFreeAsync(d_out, st);
-    cudaFreeAsync(d_ids, st);
-    const int rc2 = cuda_check(cudaStreamSynchronize(st), "sync");
     cudaStreamDestroy(st);
-    if (!rc) rc = rc2;
-    if (!rc)
-        for (int k = 0; k < nc; ++k) {
-            if (h_out[k].status != MCTB_OK) {
-                set_error("model bug: deadlock on the first path");
-                rc = MCTB_MODEL_BUG;
-                break;
-            }
-            c.first_time.push_back(h_out[k].time);
-            c.first_steps.push_back(h_out[k].steps);
-        }
-    cudaFreeHost(h_out);
     if (rc) return rc;
+    c.first_time.assign(nc, -1);
+    c.first_steps.assign(nc, -1);
     if (c.bfs.error == 3) {
         set_error("model bug: deadlock or inapplicable transition during exploration");
         return MCTB_MODEL_BUG;
@@ -189,8 +145,25 @@ int prepare(Ctx& c, int64_t max_states) {
     return MCTB_OK;
 }
 
+// The first path of explore_machine's DFS for configuration k (GPU run, en[0] policy).
+int ensure_first(Ctx& c, int k) {
+    if (c.first_time[k] >= 0) return MCTB_OK;
+    const double t0 = now_ms();
+    TrajOut o;
+    int rc = gpu_run(c.hs[k], MCTB_POLICY_FIRST, 0, 0, 200000000LL, &o, nullptr, 0);
+    c.ms_first += now_ms() - t0;
+    if (rc) return rc;
+    if (o.status != MCTB_OK) {
+        set_error("model bug: deadlock on the first path");
+        return MCTB_MODEL_BUG;
+    }
+    c.first_time[k] = o.time;
+    c.first_steps[k] = o.steps;
+    return MCTB_OK;
+}
+
 // The reference's verdict for bound T (explore.cpp:167-205) from the tables.
-VerdictOut verdict(const Ctx& c, int64_t T) {
+VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
     VerdictOut v;
     const int nc = (int)c.wg.size();
     bool limit = false;
@@ -202,6 +175,7 @@ VerdictOut verdict(const Ctx& c, int64_t T) {
         if (tmin <= T) {
             v.violated = true;
             v.cfg = k;
+            if ((*rc_out = ensure_first(c, k))) return v;
             if (c.first_time[k] <= T) {
                 // DFS reaches a satisfying terminal on its first path
                 v.final_time = c.first_time[k];
@@ -271,7 +245,8 @@ int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* in
     c.input = input;
     int rc = prepare(c, max_states);
     if (rc) return rc;
-    const VerdictOut v = verdict(c, T);
+    const VerdictOut v = verdict(c, T, &rc);
+    if (rc) return rc;
     const int64_t o[12] = {v.violated, v.exhaustive, v.states, v.max_depth, v.transitions,
                            v.explored, c.skipped, v.final_time, v.cfg >= 0 ? c.wg[v.cfg] : 0,
                            v.cfg >= 0 ? c.ts[v.cfg] : 0, v.violated ? v.steps : 0, v.trace_exact};
@@ -326,7 +301,8 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     int checks = 0;
     int64_t states_total = 0;
     bool proven = true;
-    VerdictOut v = verdict(c, t_hi);
+    VerdictOut v = verdict(c, t_hi, &rc);
+    if (rc) return rc;
     ++checks;
     states_total += v.states;
     if (!v.violated) {
@@ -339,7 +315,8 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     bool lo_checked = false;
     while (hi - lo > 1) {
         const int64_t mid = lo + (hi - lo) / 2;
-        const VerdictOut vm = verdict(c, mid);
+        const VerdictOut vm = verdict(c, mid, &rc);
+        if (rc) return rc;
         ++checks;
         states_total += vm.states;
         if (vm.violated) {
@@ -352,7 +329,8 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         }
     }
     if (!lo_checked && lo == 0 && hi == 1) {
-        const VerdictOut vz = verdict(c, 0);
+        const VerdictOut vz = verdict(c, 0, &rc);
+        if (rc) return rc;
         ++checks;
         if (vz.violated) {
             set_error("a run finished in zero ticks");
