@@ -152,22 +152,53 @@ __device__ __forceinline__ void push_fresh(const BfsArgs& a, bool fresh, long lo
     }
 }
 
+// In-place successor for the transitions behind the combinatorial state
+// explosion (an element reporting a busy tick, an element arriving at its
+// barrier): two field writes on the parent's packed words.  Everything else
+// goes through the generic unpacked apply() (machine.cuh).
+__device__ __forceinline__ bool fast_successor(const BfsDesc& d, const MState& s,
+                                               const Transition& tr, uint32_t* row) {
+    const Layout& l = d.l;
+    if (tr.op == OP_PEXREPORT) {
+        int role, p;
+        role_of(d.m, tr.actor, role, p);
+        set_bits(row, l.off_pex + p * l.pex_bits + l.poff_reported, 1, 1u);
+        set_bits(row, l.off_nrp, l.nrp, (uint32_t)(s.nrp_work + 1));
+        return true;
+    }
+    if (tr.op == OP_PEXARRIVE) {
+        int role, p;
+        role_of(d.m, tr.actor, role, p);
+        const int g = p / d.m.nwe;
+        const int pc = s.pex[p].pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
+        set_bits(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)pc);
+        set_bits(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount,
+                 (uint32_t)(s.bar[g].count + 1));
+        return true;
+    }
+    return false;
+}
+
 __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    // the parent state and its enabled list live once per warp in shared memory;
-    // each lane keeps only its own successor in (L1-resident) local memory
+    // per warp in shared memory: the parent (unpacked and packed) and its enabled
+    // list; per lane: one packed successor row.  Only the generic transitions
+    // materialise an unpacked successor in (L1-resident) local memory.
     __shared__ MState parent[kBfsThreads / 32];
     __shared__ Transition enabled_s[kBfsThreads / 32][kMaxEnabled];
     __shared__ int n_enabled[kBfsThreads / 32];
+    extern __shared__ uint32_t dyn[];
+    uint32_t* pwords = dyn + wib * (34 * a.words);  // parent words
+    uint32_t* kwords = pwords + a.words;             // the successor the warp keeps
+    uint32_t* row = pwords + (2 + lane) * a.words;   // this lane's successor
     MState& s = parent[wib];
     Transition* en = enabled_s[wib];
     MState t;
-    uint32_t key[kMaxWords], cur[kMaxWords];
     bool local = false;  // the warp continues with a successor it discovered itself
     for (;;) {
         const uint32_t* src;
         if (local) {
-            src = cur;
+            src = pwords;  // already holds the kept successor
         } else {
             unsigned long long h = 0;
             if (lane == 0) h = atomicAdd(a.head, 1ull);
@@ -196,6 +227,9 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             if (slot == kEmpty) return;
             // the key is published before its slot index is pushed
             src = a.keys + (uint64_t)slot * a.words;
+            for (int k = lane; k < a.words; k += 32) pwords[k] = src[k];
+            __syncwarp();
+            src = pwords;
         }
         const int cfg = peek_cfg(src, a.cfg_bits);
         const BfsDesc& d = a.descs[cfg];
@@ -227,24 +261,26 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                 const int e = base + lane;
                 long long ins = -1;
                 if (e < ne) {
-                    copy_state(d.m, t, s);
-                    if (!apply(d.m, t, en[e])) {
-                        atomicExch(a.error, 3);
-                    } else {
-                        pack(d, cfg, t, key);
-                        for (int k = d.l.words; k < a.words; ++k) key[k] = 0;
-                        ins = table_insert(a, key, hash_words(key, a.words));
+                    for (int k = 0; k < a.words; ++k) row[k] = pwords[k];
+                    bool ok = true;
+                    if (!fast_successor(d, s, en[e], row)) {
+                        copy_state(d.m, t, s);
+                        ok = apply(d.m, t, en[e]);
+                        if (ok) pack(d, cfg, t, row);
+                        else atomicExch(a.error, 3);
+                    }
+                    if (ok) {
+                        ins = table_insert(a, row, hash_words(row, a.words));
                         if (ins == -2) atomicExch(a.error, 1);
                     }
                 }
                 bool fresh = ins >= 0;
+                int keeper = -1;
                 if (!kept && a.keep) {
                     // keep the first new successor: no queue round trip on the chain
                     const unsigned m = __ballot_sync(0xffffffffu, fresh);
                     if (m) {
-                        const int keeper = __ffs(m) - 1;
-                        for (int k = 0; k < a.words; ++k)
-                            cur[k] = __shfl_sync(0xffffffffu, key[k], keeper);
+                        keeper = __ffs(m) - 1;
                         if (lane == keeper) fresh = false;
                         if (lane == 0) {
                             atomicAdd((unsigned long long*)a.outstanding, 1ull);
@@ -254,11 +290,21 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     }
                 }
                 push_fresh(a, fresh, ins, st);
+                if (keeper >= 0) {
+                    __syncwarp();
+                    const uint32_t* kr = pwords + (2 + keeper) * a.words;
+                    for (int k = lane; k < a.words; k += 32) kwords[k] = kr[k];
+                    __syncwarp();
+                }
             }
         }
         __syncwarp();
         if (lane == 0) atomicAdd((unsigned long long*)a.outstanding, ~0ull);  // -1
         local = kept && !*(volatile int*)a.error;
+        if (local) {
+            for (int k = lane; k < a.words; k += 32) pwords[k] = kwords[k];
+            __syncwarp();
+        }
     }
 }
 
@@ -313,7 +359,12 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     int dev = 0, sms = 0, per_sm = 0;
     MCTB_CUDA(cudaGetDevice(&dev));
     MCTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, explore_kernel, kBfsThreads, 0));
+    const size_t dyn_smem = (size_t)(kBfsThreads / 32) * 34 * words * sizeof(uint32_t);
+    if (dyn_smem > 48 * 1024)
+        MCTB_CUDA(cudaFuncSetAttribute(explore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn_smem));
+    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, explore_kernel, kBfsThreads,
+                                                            dyn_smem));
     if (per_sm < 1) per_sm = 1;
     // local-memory working set: keep the resident warps' successor states L1-sized
     if (const char* e = getenv("MCTB_BFS_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(e));
@@ -370,7 +421,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
-        explore_kernel<<<sms * per_sm, kBfsThreads, 0, st>>>(a);
+        explore_kernel<<<sms * per_sm, kBfsThreads, dyn_smem, st>>>(a);
         cudaEventRecord(e1, st);
         MCTB_CUDA(cudaGetLastError());
         res->stats.resize(n_cfg);

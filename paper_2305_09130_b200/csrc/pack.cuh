@@ -29,6 +29,8 @@ struct Layout {
     uint8_t cfg;                                      // configuration id (multi-config search)
     int32_t words;                                    // packed size in 32-bit words
     int32_t bits;
+    // bit offsets for in-place successor writes (explore fast paths)
+    int32_t off_nrp, off_units, unit_bits, uoff_bcount, off_pex, pex_bits, poff_reported;
 };
 
 struct BfsDesc {
@@ -75,6 +77,14 @@ __host__ inline Layout make_layout(const MachDesc& m, int n_cfg, int64_t max_tim
     bits += m.n_pex * (4 + 1 + l.cursor + l.busy + 1 + l.pnwg + l.iter);
     if (m.kernel == 1) bits += m.n_units * m.np * l.loc;
     l.bits = bits;
+    l.off_nrp = l.cfg + l.time;
+    l.off_units = l.cfg + l.time + l.nrp + l.allnwe + 1 + l.nextwg + 3 + l.hostk + 1 + l.glob0 +
+                  m.nwd * (3 + l.dk + l.bb);
+    l.uoff_bcount = 3 + l.uk + l.nwg + l.sent + l.items + l.ends + 1;
+    l.unit_bits = l.uoff_bcount + l.bcount;
+    l.off_pex = l.off_units + m.n_units * l.unit_bits;
+    l.pex_bits = 4 + 1 + l.cursor + l.busy + 1 + l.pnwg + l.iter;
+    l.poff_reported = 4 + 1 + l.cursor + l.busy;
     l.words = (bits + 31) / 32;
     return l;
 }
@@ -210,6 +220,19 @@ __host__ __device__ inline void unpack(const BfsDesc& d, const uint32_t* in, MSt
     }
     if (m.kernel == 1)
         for (int i = 0; i < m.n_units * m.np; ++i) s.loc[i] = (int32_t)r.get(l.loc);
+}
+
+// Overwrites `width` bits at bit offset `off` of a packed state (LSB-first, the
+// BitWriter order).
+__host__ __device__ inline void set_bits(uint32_t* w, int off, int width, uint32_t v) {
+    if (!width) return;
+    const int i = off >> 5, sh = off & 31;
+    const uint64_t mask = ((1ull << width) - 1) << sh;
+    const bool two = sh + width > 32;
+    uint64_t cur = (uint64_t)w[i] | (two ? (uint64_t)w[i + 1] << 32 : 0ull);
+    cur = (cur & ~mask) | (((uint64_t)v << sh) & mask);
+    w[i] = (uint32_t)cur;
+    if (two) w[i + 1] = (uint32_t)(cur >> 32);
 }
 
 // 64-bit hash of a packed state (splitmix64-style mixing of the words).
