@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample-secs", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     return ap.parse_args()
 
 
@@ -323,6 +324,8 @@ def run_b200(args):
                          "probe_peak": probe_ops.value / 1e12},
             "clocks": clk,
         }
+        if world == 1 and not args.no_secondary:
+            line["secondary"] = secondary_metrics(m, with_reference=not args.no_cpu_baseline)
         if world == 1 and not args.no_cpu_baseline:
             v, kind, thr, n, st, el = reference_sample(args.cpu_sample_secs)
             line["cpu_baseline"] = {
@@ -333,6 +336,77 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def secondary_metrics(m, with_reference=True):
+    """The other north-star paths, one measurement each (reported, not the headline):
+    time-to-optimum of `tune` (BASELINE configs[0..1] scale), the interleaving
+    exploration (configs[3]) and the swarm trajectories (configs[2])."""
+    import hashlib
+    import struct
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import checkers
+    ref = checkers.Ref() if with_reference and os.path.exists(checkers.REF_SO) else None
+    out = {}
+    # (1) tune: paper use case, abstract kernel, size 64 on (1,1,4,4)
+    plat, prob = m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(64)
+    m.tune(plat, prob)  # warm
+    t0 = time.perf_counter()
+    r = m.tune(plat, prob, seed=1)
+    gpu_s = time.perf_counter() - t0
+    tune = {"workload": "tune (estimate_initial_time + bisect_min_time), abstract kernel, size 64, "
+                        "platform (1,1,4,4), seed 1",
+            "gpu_seconds": gpu_s, "t_min": r.t_min, "wg": r.params.wg, "ts": r.params.ts,
+            "proven": r.proven, "states_visited_total": r.stats.states_visited_total,
+            "explored_states": r.timings_ms["explored_states"]}
+    if ref is not None:
+        t0 = time.perf_counter()
+        rr = ref.tune((1, 1, 4, 4), 64, 0, seed=1)
+        tune["reference_seconds"] = time.perf_counter() - t0
+        tune["reference_cores"] = 1
+        sha = lambda tr: hashlib.sha256(b"".join(struct.pack("<4i", *x) for x in tr)).hexdigest()  # noqa: E731
+        tune["identical"] = ((rr["t_min"], rr["wg"], rr["ts"], rr["t_ini"], bool(rr["proven"]),
+                              rr["checks_run"], rr["states_visited_total"], rr["steps"])
+                             == (r.t_min, r.params.wg, r.params.ts, r.t_ini, r.proven,
+                                 r.stats.checks_run, r.stats.states_visited_total, r.trace.steps)
+                             and sha(rr["trace"]) == sha(r.trace.transitions))
+    out["tune"] = tune
+    # (2) exploration of one configuration's full interleaving space (5.6e7 states)
+    info = []
+    plat16 = m.PlatformConfig(1, 1, 16, 4)
+    x = m.explore_configs(plat16, m.ProblemSpec.abstract(32), [m.TuningParams(16, 2)],
+                          max_states=400_000_000, info=info)[0]
+    words = info[0].key_words
+    ex = {"workload": "explore_machine, abstract kernel, size 32, platform (1,1,16,4), "
+                      "(wg,ts)=(16,2): every interleaving",
+          "states": x.states_visited, "transitions": x.transitions_applied,
+          "complete": x.complete, "kernel_ms": info[0].kernel_us / 1e3,
+          "states_per_s": x.states_visited / (info[0].kernel_us * 1e-6),
+          "key_words": words,
+          "algorithmic_bytes_per_state": 8 + 8 * words + 8 + 8 * (
+              x.transitions_applied / max(1, x.states_visited))}
+    ex["achieved_GBps"] = ex["algorithmic_bytes_per_state"] * ex["states_per_s"] / 1e9
+    if ref is not None:
+        t0 = time.perf_counter()
+        rx = ref.explore((1, 1, 8, 4), 32, 0, 8, 2)
+        el = time.perf_counter() - t0
+        ex["reference_states_per_s"] = rx["states"] / el
+        ex["reference_sample"] = ("explore_machine (1,1,8,4) size 32 (8,2): "
+                                  f"{rx['states']} states in {el:.2f} s, 1 core")
+    out["explore"] = ex
+    # (3) swarm trajectories: 10^6 Philox schedules over every configuration, size 16
+    plat = m.PlatformConfig(1, 1, 4, 4)
+    prob = m.ProblemSpec.abstract(16)
+    cfgs = m.enumerate_configs(16)
+    m.trajectories(plat, prob, cfgs, m.PHILOX, 1, 0, 4096)
+    t0 = time.perf_counter()
+    b = m.trajectories(plat, prob, cfgs, m.PHILOX, 1, 0, 1_000_000)
+    el = time.perf_counter() - t0
+    out["swarm"] = {"workload": "1e6 Philox4x32-10 schedule trajectories, abstract kernel, size 16, "
+                                "(1,1,4,4), all 9 configurations (host API, incl. copies)",
+                    "seconds": el, "trajectories_per_s": 1e6 / el,
+                    "transitions_per_s": sum(b.steps) / el, "min_time": min(b.time)}
+    return out
 
 
 # Thread-level instructions executed per configuration by space_argmin_kernel<0>
