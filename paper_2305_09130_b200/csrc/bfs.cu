@@ -186,7 +186,6 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     // materialise an unpacked successor in (L1-resident) local memory.
     __shared__ MState parent[kBfsThreads / 32];
     __shared__ Transition enabled_s[kBfsThreads / 32][kMaxEnabled];
-    __shared__ int n_enabled[kBfsThreads / 32];
     extern __shared__ uint32_t dyn[];
     uint32_t* pwords = dyn + wib * (34 * a.words);  // parent words
     uint32_t* kwords = pwords + a.words;             // the successor the warp keeps
@@ -233,12 +232,24 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         }
         const int cfg = peek_cfg(src, a.cfg_bits);
         const BfsDesc& d = a.descs[cfg];
-        if (lane == 0) {
-            unpack(d, src, s);
-            n_enabled[wib] = enabled(d.m, s, en);
-        }
+        // warp-parallel unpack and enumeration: lane i reads the records of process
+        // slots i, i+32, ... and applies their rules (machine.cuh); a warp prefix sum
+        // places every lane's transitions in the shared enabled list
+        unpack_lanes(d, src, s, lane);
         __syncwarp();
-        const int ne = n_enabled[wib];
+        const int nsl = n_slots(d.m);
+        int cnt = 0;
+        for (int k = lane; k < nsl; k += 32) cnt = slot_rules(d.m, s, k, nullptr, cnt);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int ne = __shfl_sync(0xffffffffu, incl, 31);
+        int pos = incl - cnt;
+        for (int k = lane; k < nsl; k += 32) pos = slot_rules(d.m, s, k, en, pos);
+        __syncwarp();
         BfsStats& st = a.stats[cfg];
         bool kept = false;
         if (ne == 0) {

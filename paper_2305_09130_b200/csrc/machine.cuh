@@ -258,18 +258,19 @@ __host__ __device__ inline bool is_terminal(const MachDesc& m, const MState& s) 
     return true;
 }
 
-// Machine::enabled, machine.cpp:174-336: every enabled transition, ascending
-// actor pid (the reference's stable sort by actor), emitted per process.
-// Returns the count; `out` may be null (count only).
-// max_out stops the enumeration early (the first path needs en[0] only).
-__host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Transition* out,
-                                      int max_out = 1 << 30) {
-    int n = 0;
-#define push(A, P, O, G)                                                          \
-    do {                                                                          \
-        if (out) out[n] = Transition{(uint16_t)(A), (uint16_t)(P), (O), (G)};     \
-        if (++n >= max_out) return n;                                             \
+// Machine::enabled, machine.cpp:174-336, split per process: each rule appends
+// the transitions whose ACTOR is that process (to out + n, when out != null)
+// and returns the new count.  The serial enumeration below visits the
+// processes in ascending pid — the reference's stable sort by actor — and the
+// exploration visits them warp-parallel (bfs.cu).
+#define MCTB_PUSH(A, P, O, G)                                                   \
+    do {                                                                        \
+        if (out) out[n] = Transition{(uint16_t)(A), (uint16_t)(P), (O), (G)};   \
+        ++n;                                                                    \
     } while (0)
+
+__host__ __device__ inline int host_rules(const MachDesc& m, const MState& s, Transition* out,
+                                          int n) {
     switch (s.host_pc) {
         case H_SENDGO:
         case H_REACTGO:
@@ -278,86 +279,151 @@ __host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Trans
                            : s.host_pc == H_REACTGO ? OP_HOSTREACTGO
                                                     : OP_HOSTSTOP;
             for (int d = 0; d < m.nwd; ++d)
-                if (s.dev[d].pc == D_WAITGO) push(1, device_pid(m, d), op, s.host_k);
+                if (s.dev[d].pc == D_WAITGO) MCTB_PUSH(1, device_pid(m, d), op, s.host_k);
             break;
         }
-        case H_SETFIN: push(1, kNoPeer, OP_HOSTSETFIN, 0); break;
+        case H_SETFIN: MCTB_PUSH(1, kNoPeer, OP_HOSTSETFIN, 0); break;
         default: break;
     }
+    return n;
+}
+
+__host__ __device__ inline int clock_rules(const MachDesc&, const MState& s, Transition* out,
+                                           int n) {
     if (s.clock == 0) {
-        if (s.fin) push(2, kNoPeer, OP_CLOCKHALT, 0);
-        if (s.all_nwe != 0 && s.nrp_work == s.all_nwe) push(2, kNoPeer, OP_CLOCKTICK, 0);
+        if (s.fin) MCTB_PUSH(2, kNoPeer, OP_CLOCKHALT, 0);
+        if (s.all_nwe != 0 && s.nrp_work == s.all_nwe) MCTB_PUSH(2, kNoPeer, OP_CLOCKTICK, 0);
     }
+    return n;
+}
+
+__host__ __device__ inline int device_rules(const MachDesc& m, const MState& s, int d,
+                                            Transition* out, int n) {
+    const DevS& dv = s.dev[d];
+    const int dpid = device_pid(m, d);
+    if (dv.pc == D_SENDUNITGO || dv.pc == D_STOPUNITS) {
+        const int op = dv.pc == D_SENDUNITGO ? OP_DEVICEUNITGO : OP_DEVICEUNITSTOP;
+        const int arg = dv.pc == D_SENDUNITGO ? dv.batch_base + dv.k : 0;
+        for (int u = 0; u < m.nwu; ++u)
+            if (s.unit[d * m.nwu + u].pc == U_WAITGO) MCTB_PUSH(dpid, unit_pid(m, d * m.nwu + u), op, arg);
+    } else if (dv.pc == D_SENDDONE) {
+        if (s.host_pc == H_WAITDONEREACT || s.host_pc == H_WAITDONESTOP)
+            MCTB_PUSH(dpid, 1, OP_DEVICEDONE, 0);
+    }
+    return n;
+}
+
+__host__ __device__ inline int unit_rules(const MachDesc& m, const MState& s, int g,
+                                          Transition* out, int n) {
+    const UnitS& un = s.unit[g];
+    const int upid = unit_pid(m, g);
+    switch (un.pc) {
+        case U_ACTIVATEPEX:
+        case U_REACTPEX:
+        case U_STOPPEXES: {
+            const int op = un.pc == U_STOPPEXES ? OP_UNITPEXSTOP : OP_UNITPEXGO;
+            const int arg = un.pc == U_STOPPEXES ? 0 : un.sent / m.nwe;
+            for (int e = 0; e < m.nwe; ++e)
+                if (s.pex[g * m.nwe + e].pc == P_WAITGO) MCTB_PUSH(upid, upid + 2 + e, op, arg);
+            break;
+        }
+        case U_SENDUNITDONE:
+            if (s.dev[g / m.nwu].pc == D_WAITUNITDONE)
+                MCTB_PUSH(upid, device_pid(m, g / m.nwu), OP_UNITDONE, un.nwg);
+            break;
+        case U_STOPBARRIER:
+            if (s.bar[g].pc == B_COUNTING && s.bar[g].count == 0)
+                MCTB_PUSH(upid, upid + 1, OP_UNITBARRIERSTOP, 0);
+            break;
+        default: break;
+    }
+    return n;
+}
+
+__host__ __device__ inline int barrier_rules(const MachDesc& m, const MState& s, int g,
+                                             Transition* out, int n) {
+    const BarS& b = s.bar[g];
+    if (b.pc == B_COUNTING && b.count == m.nwe) MCTB_PUSH(barrier_pid(m, g), kNoPeer, OP_BARRIERRELEASE, 0);
+    return n;
+}
+
+__host__ __device__ inline int pex_rules(const MachDesc& m, const MState& s, int p,
+                                         Transition* out, int n) {
+    const int g = p / m.nwe;
+    const PexS& px = s.pex[p];
+    const int upid = unit_pid(m, g);
+    const int ppid = upid + 2 + (p - g * m.nwe);
+    switch (px.pc) {
+        case P_RUN: {
+            const Instr in = instr_at(m, px.phase, px.cursor);
+            if (in.kind == IK_BUSY) {
+                if (px.busy_left > 0 && !px.reported) MCTB_PUSH(ppid, kNoPeer, OP_PEXREPORT, 0);
+            } else if (in.kind == IK_EFFECT) {
+                MCTB_PUSH(ppid, kNoPeer, OP_PEXEFFECT, px.cursor);
+            }
+            break;
+        }
+        case P_ARRIVEBARRIER:
+        case P_ARRIVEGROUPEND:
+            if (s.bar[g].pc == B_COUNTING && s.bar[g].count < m.nwe)
+                MCTB_PUSH(ppid, upid + 1, OP_PEXARRIVE, 0);
+            break;
+        case P_SENDITEMDONE:
+            if (s.unit[g].pc == U_SERVE) MCTB_PUSH(ppid, upid, OP_PEXITEMDONE, px.iter);
+            break;
+        case P_SENDENDDONE:
+            if (s.unit[g].pc == U_SERVE) MCTB_PUSH(ppid, upid, OP_PEXENDDONE, 0);
+            break;
+        default: break;
+    }
+    return n;
+}
+#undef MCTB_PUSH
+
+// Process slot k of the warp-parallel enumeration: host, clock, devices,
+// units, barriers, elements (any order gives the same successor set).
+__host__ __device__ inline int slot_rules(const MachDesc& m, const MState& s, int k,
+                                          Transition* out, int n) {
+    if (k == 0) return host_rules(m, s, out, n);
+    if (k == 1) return clock_rules(m, s, out, n);
+    k -= 2;
+    if (k < m.nwd) return device_rules(m, s, k, out, n);
+    k -= m.nwd;
+    if (k < m.n_units) return unit_rules(m, s, k, out, n);
+    k -= m.n_units;
+    if (k < m.n_units) return barrier_rules(m, s, k, out, n);
+    k -= m.n_units;
+    return pex_rules(m, s, k, out, n);
+}
+
+__host__ __device__ inline int n_slots(const MachDesc& m) {
+    return 2 + m.nwd + 2 * m.n_units + m.n_pex;
+}
+
+// Every enabled transition in ascending actor pid (max_out stops early: the
+// first path needs en[0] only).
+__host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Transition* out,
+                                      int max_out = 1 << 30) {
+    int n = host_rules(m, s, out, 0);
+    if (n >= max_out) return n;
+    n = clock_rules(m, s, out, n);
+    if (n >= max_out) return n;
     int g = 0;
     for (int d = 0; d < m.nwd; ++d) {
-        const DevS& dv = s.dev[d];
-        const int dpid = device_pid(m, d);
-        if (dv.pc == D_SENDUNITGO || dv.pc == D_STOPUNITS) {
-            const int op = dv.pc == D_SENDUNITGO ? OP_DEVICEUNITGO : OP_DEVICEUNITSTOP;
-            const int arg = dv.pc == D_SENDUNITGO ? dv.batch_base + dv.k : 0;
-            for (int u = 0; u < m.nwu; ++u)
-                if (s.unit[d * m.nwu + u].pc == U_WAITGO)
-                    push(dpid, unit_pid(m, d * m.nwu + u), op, arg);
-        } else if (dv.pc == D_SENDDONE) {
-            if (s.host_pc == H_WAITDONEREACT || s.host_pc == H_WAITDONESTOP)
-                push(dpid, 1, OP_DEVICEDONE, 0);
-        }
+        n = device_rules(m, s, d, out, n);
+        if (n >= max_out) return n;
         for (int u = 0; u < m.nwu; ++u, ++g) {
-            const UnitS& un = s.unit[g];
-            const int upid = unit_pid(m, g);
-            switch (un.pc) {
-                case U_ACTIVATEPEX:
-                case U_REACTPEX:
-                case U_STOPPEXES: {
-                    const int op = un.pc == U_STOPPEXES ? OP_UNITPEXSTOP : OP_UNITPEXGO;
-                    const int arg = un.pc == U_STOPPEXES ? 0 : un.sent / m.nwe;
-                    for (int e = 0; e < m.nwe; ++e)
-                        if (s.pex[g * m.nwe + e].pc == P_WAITGO) push(upid, upid + 2 + e, op, arg);
-                    break;
-                }
-                case U_SENDUNITDONE:
-                    if (dv.pc == D_WAITUNITDONE) push(upid, dpid, OP_UNITDONE, un.nwg);
-                    break;
-                case U_STOPBARRIER:
-                    if (s.bar[g].pc == B_COUNTING && s.bar[g].count == 0)
-                        push(upid, upid + 1, OP_UNITBARRIERSTOP, 0);
-                    break;
-                default: break;
-            }
-            const BarS& b = s.bar[g];
-            if (b.pc == B_COUNTING && b.count == m.nwe) push(upid + 1, kNoPeer, OP_BARRIERRELEASE, 0);
+            n = unit_rules(m, s, g, out, n);
+            n = barrier_rules(m, s, g, out, n);
+            if (n >= max_out) return n;
             for (int e = 0; e < m.nwe; ++e) {
-                const PexS& px = s.pex[g * m.nwe + e];
-                const int ppid = upid + 2 + e;
-                switch (px.pc) {
-                    case P_RUN: {
-                        const Instr in = instr_at(m, px.phase, px.cursor);
-                        if (in.kind == IK_BUSY) {
-                            if (px.busy_left > 0 && !px.reported) push(ppid, kNoPeer, OP_PEXREPORT, 0);
-                        } else if (in.kind == IK_EFFECT) {
-                            push(ppid, kNoPeer, OP_PEXEFFECT, px.cursor);
-                        }
-                        break;
-                    }
-                    case P_ARRIVEBARRIER:
-                    case P_ARRIVEGROUPEND:
-                        if (b.pc == B_COUNTING && b.count < m.nwe)
-                            push(ppid, upid + 1, OP_PEXARRIVE, 0);
-                        break;
-                    case P_SENDITEMDONE:
-                        if (un.pc == U_SERVE) push(ppid, upid, OP_PEXITEMDONE, px.iter);
-                        break;
-                    case P_SENDENDDONE:
-                        if (un.pc == U_SERVE) push(ppid, upid, OP_PEXENDDONE, 0);
-                        break;
-                    default: break;
-                }
+                n = pex_rules(m, s, g * m.nwe + e, out, n);
+                if (n >= max_out) return n;
             }
         }
     }
     return n;
 }
-#undef push
 
 // Machine::apply, machine.cpp:361-649, in place.  Returns false when the
 // transition is not enabled (replay divergence) or a model bug is hit.

@@ -31,6 +31,7 @@ struct Layout {
     int32_t bits;
     // bit offsets for in-place successor writes (explore fast paths)
     int32_t off_nrp, off_units, unit_bits, uoff_bcount, off_pex, pex_bits, poff_reported;
+    int32_t off_dev, dev_bits, off_loc;
 };
 
 struct BfsDesc {
@@ -85,6 +86,9 @@ __host__ inline Layout make_layout(const MachDesc& m, int n_cfg, int64_t max_tim
     l.off_pex = l.off_units + m.n_units * l.unit_bits;
     l.pex_bits = 4 + 1 + l.cursor + l.busy + 1 + l.pnwg + l.iter;
     l.poff_reported = 4 + 1 + l.cursor + l.busy;
+    l.dev_bits = 3 + l.dk + l.bb;
+    l.off_dev = l.off_units - m.nwd * l.dev_bits;
+    l.off_loc = l.off_pex + m.n_pex * l.pex_bits;
     l.words = (bits + 31) / 32;
     return l;
 }
@@ -115,6 +119,14 @@ struct BitReader {
     uint64_t acc = 0;
     int n = 0, idx = 0;
     __host__ __device__ explicit BitReader(const uint32_t* in) : w(in) {}
+    // positioned at bit `off`
+    __host__ __device__ BitReader(const uint32_t* in, int off) : w(in), idx(off >> 5) {
+        const int sh = off & 31;
+        if (sh) {
+            acc = (uint64_t)w[idx++] >> sh;
+            n = 32 - sh;
+        }
+    }
     __host__ __device__ inline uint32_t get(int bits) {
         if (!bits) return 0;
         if (n < bits) {
@@ -233,6 +245,60 @@ __host__ __device__ inline void set_bits(uint32_t* w, int off, int width, uint32
     cur = (cur & ~mask) | (((uint64_t)v << sh) & mask);
     w[i] = (uint32_t)cur;
     if (two) w[i + 1] = (uint32_t)(cur >> 32);
+}
+
+// Warp-parallel unpack (exploration): lane 0 reads the header, lane i the
+// records of device/unit/element i (+32k); the caller syncs the warp after.
+__device__ inline void unpack_lanes(const BfsDesc& d, const uint32_t* in, MState& s, int lane) {
+    const MachDesc& m = d.m;
+    const Layout& l = d.l;
+    if (lane == 0) {
+        BitReader r(in);
+        r.get(l.cfg);
+        s.time = r.get(l.time);
+        s.nrp_work = (int32_t)r.get(l.nrp);
+        s.all_nwe = (int32_t)r.get(l.allnwe);
+        s.fin = (int32_t)r.get(1);
+        s.next_wg = (int32_t)r.get(l.nextwg);
+        s.host_pc = (int32_t)r.get(3);
+        s.host_k = (int32_t)r.get(l.hostk);
+        s.clock = (int32_t)r.get(1);
+        s.glob0 = (int32_t)r.get(l.glob0);
+    }
+    for (int i = lane; i < m.nwd; i += 32) {
+        BitReader r(in, l.off_dev + i * l.dev_bits);
+        s.dev[i].pc = (int32_t)r.get(3);
+        s.dev[i].k = (int32_t)r.get(l.dk);
+        s.dev[i].batch_base = (int32_t)r.get(l.bb);
+    }
+    for (int g = lane; g < m.n_units; g += 32) {
+        BitReader r(in, l.off_units + g * l.unit_bits);
+        UnitS& u = s.unit[g];
+        u.pc = (int32_t)r.get(3);
+        u.k = (int32_t)r.get(l.uk);
+        u.nwg = (int32_t)r.get(l.nwg);
+        u.sent = (int32_t)r.get(l.sent);
+        u.got_items = (int32_t)r.get(l.items);
+        u.got_ends = (int32_t)r.get(l.ends);
+        s.bar[g].pc = (int32_t)r.get(1);
+        s.bar[g].count = (int32_t)r.get(l.bcount);
+    }
+    for (int p = lane; p < m.n_pex; p += 32) {
+        BitReader r(in, l.off_pex + p * l.pex_bits);
+        PexS& x = s.pex[p];
+        x.pc = (int16_t)r.get(4);
+        x.phase = (int16_t)r.get(1);
+        x.cursor = (uint16_t)r.get(l.cursor);
+        x.busy_left = (uint16_t)r.get(l.busy);
+        x.reported = (int16_t)r.get(1);
+        x.nwg = (int32_t)r.get(l.pnwg);
+        x.iter = (uint16_t)r.get(l.iter);
+    }
+    if (m.kernel == 1)
+        for (int i = lane; i < m.n_units * m.np; i += 32) {
+            BitReader r(in, l.off_loc + i * l.loc);
+            s.loc[i] = (int32_t)r.get(l.loc);
+        }
 }
 
 // 64-bit hash of a packed state (splitmix64-style mixing of the words).
