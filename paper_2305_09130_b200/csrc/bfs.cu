@@ -21,6 +21,7 @@
 // are explored in the same sweep, tagged by a cfg field of the packed state;
 // per-configuration statistics give the reference's ExploreStats.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -50,6 +51,7 @@ struct BfsArgs {
     int* error;       // 1 table full, 2 queue full, 3 model bug
     uint64_t cfg_cap; // per-configuration visited cap (ExploreLimits::max_states)
     int keep;         // continue with the first new successor (no queue round trip)
+    unsigned long long* op_hist;  // generic successors per op (diagnostics)
 };
 
 namespace {
@@ -156,27 +158,111 @@ __device__ __forceinline__ void push_fresh(const BfsArgs& a, bool fresh, long lo
 // explosion (an element reporting a busy tick, an element arriving at its
 // barrier): two field writes on the parent's packed words.  Everything else
 // goes through the generic unpacked apply() (machine.cuh).
+// Record writers for the in-place successors (field order of pack()).
+__device__ __forceinline__ void write_pex(uint32_t* row, const Layout& l, int p, const PexS& x) {
+    const int o = l.off_pex + p * l.pex_bits;
+    set_bits(row, o, 4, (uint32_t)x.pc);
+    set_bits(row, o + 4, 1, (uint32_t)x.phase);
+    set_bits(row, o + 5, l.cursor, x.cursor);
+    set_bits(row, o + 5 + l.cursor, l.busy, x.busy_left);
+    set_bits(row, o + 5 + l.cursor + l.busy, 1, (uint32_t)x.reported);
+    set_bits(row, o + 6 + l.cursor + l.busy, l.pnwg, (uint32_t)x.nwg);
+    set_bits(row, o + 6 + l.cursor + l.busy + l.pnwg, l.iter, x.iter);
+}
+
+__device__ __forceinline__ void write_unit(uint32_t* row, const Layout& l, int g, const UnitS& u) {
+    const int o = l.off_units + g * l.unit_bits;
+    set_bits(row, o, 3, (uint32_t)u.pc);
+    set_bits(row, o + 3, l.uk, (uint32_t)u.k);
+    set_bits(row, o + 3 + l.uk, l.nwg, (uint32_t)u.nwg);
+    set_bits(row, o + 3 + l.uk + l.nwg, l.sent, (uint32_t)u.sent);
+    set_bits(row, o + 3 + l.uk + l.nwg + l.sent, l.items, (uint32_t)u.got_items);
+    set_bits(row, o + 3 + l.uk + l.nwg + l.sent + l.items, l.ends, (uint32_t)u.got_ends);
+}
+
+// In-place successors for the transitions behind the combinatorial state
+// explosion: an element reporting a busy tick or arriving at its barrier, and
+// the unit <-> element handshakes (activation, item done, group done, stop).
+// They touch one element record, its unit record and at most one header field;
+// the new values follow Machine::apply (machine.cpp:479-500, 518-530, 541-551,
+// 569-580, 618-646) and are written over the parent's packed words.  Every
+// other transition goes through the generic unpacked apply() (machine.cuh).
 __device__ __forceinline__ bool fast_successor(const BfsDesc& d, const MState& s,
                                                const Transition& tr, uint32_t* row) {
     const Layout& l = d.l;
-    if (tr.op == OP_PEXREPORT) {
-        int role, p;
-        role_of(d.m, tr.actor, role, p);
-        set_bits(row, l.off_pex + p * l.pex_bits + l.poff_reported, 1, 1u);
-        set_bits(row, l.off_nrp, l.nrp, (uint32_t)(s.nrp_work + 1));
-        return true;
+    const MachDesc& m = d.m;
+    int role, ord;
+    switch (tr.op) {
+        case OP_PEXREPORT: {
+            role_of(m, tr.actor, role, ord);
+            set_bits(row, l.off_pex + ord * l.pex_bits + l.poff_reported, 1, 1u);
+            set_bits(row, l.off_nrp, l.nrp, (uint32_t)(s.nrp_work + 1));
+            return true;
+        }
+        case OP_PEXARRIVE: {
+            role_of(m, tr.actor, role, ord);
+            const int g = ord / m.nwe;
+            const int pc = s.pex[ord].pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
+            set_bits(row, l.off_pex + ord * l.pex_bits, 4, (uint32_t)pc);
+            set_bits(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount,
+                     (uint32_t)(s.bar[g].count + 1));
+            return true;
+        }
+        case OP_UNITPEXGO: {
+            role_of(m, tr.actor, role, ord);
+            int prole, p;
+            role_of(m, tr.peer, prole, p);
+            UnitS un = s.unit[ord];
+            PexS px = pex_init(un.nwg, un.sent / m.nwe);
+            place_pex(m, px);
+            un.sent += 1;
+            if (un.pc == U_ACTIVATEPEX) {
+                if (++un.k == m.nwe) {
+                    un.pc = U_SERVE;
+                    un.k = 0;
+                }
+            } else {
+                un.pc = U_SERVE;
+            }
+            write_pex(row, l, p, px);
+            write_unit(row, l, ord, un);
+            return true;
+        }
+        case OP_UNITPEXSTOP: {
+            role_of(m, tr.actor, role, ord);
+            int prole, p;
+            role_of(m, tr.peer, prole, p);
+            UnitS un = s.unit[ord];
+            if (++un.k == m.nwe) un.pc = U_STOPBARRIER;
+            set_bits(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)P_EXITED);
+            write_unit(row, l, ord, un);
+            return true;
+        }
+        case OP_PEXITEMDONE: {
+            role_of(m, tr.actor, role, ord);
+            const int g = ord / m.nwe;
+            UnitS un = s.unit[g];
+            un.got_items += 1;
+            if (un.sent < m.wg) un.pc = U_REACTPEX;
+            else if (m.kernel == 0 && un.got_items == m.wg) un.pc = U_SENDUNITDONE;
+            write_pex(row, l, ord, pex_init(0, 0));
+            write_unit(row, l, g, un);
+            return true;
+        }
+        case OP_PEXENDDONE: {
+            role_of(m, tr.actor, role, ord);
+            const int g = ord / m.nwe;
+            UnitS un = s.unit[g];
+            un.got_ends += 1;
+            if (un.got_ends == m.nwe) un.pc = U_SENDUNITDONE;
+            if (ord % m.nwe == 0)
+                set_bits(row, l.off_nrp + l.nrp, l.allnwe, (uint32_t)(s.all_nwe - 1));
+            write_pex(row, l, ord, pex_init(0, 0));
+            write_unit(row, l, g, un);
+            return true;
+        }
+        default: return false;
     }
-    if (tr.op == OP_PEXARRIVE) {
-        int role, p;
-        role_of(d.m, tr.actor, role, p);
-        const int g = p / d.m.nwe;
-        const int pc = s.pex[p].pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
-        set_bits(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)pc);
-        set_bits(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount,
-                 (uint32_t)(s.bar[g].count + 1));
-        return true;
-    }
-    return false;
 }
 
 __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
@@ -275,6 +361,8 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     for (int k = 0; k < a.words; ++k) row[k] = pwords[k];
                     bool ok = true;
                     if (!fast_successor(d, s, en[e], row)) {
+                        atomicAdd(&st.generic, 1ull);
+                        atomicAdd(&a.op_hist[en[e].op], 1ull);
                         copy_state(d.m, t, s);
                         ok = apply(d.m, t, en[e]);
                         if (ok) pack(d, cfg, t, row);
@@ -403,7 +491,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
         const size_t sz_tags = cap * 8, sz_keys = cap * 4 * (size_t)words, sz_q = qcap * 4;
-        const size_t sz_misc = 256 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg;
+        const size_t sz_misc = 512 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg;
         void* blob = nullptr;
         MCTB_CUDA(cudaMallocAsync(&blob, sz_tags + sz_keys + sz_q + sz_misc, st));
         char* b = (char*)blob;
@@ -415,13 +503,14 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.tail = (unsigned long long*)(misc + 8);
         a.outstanding = (long long*)(misc + 16);
         a.error = (int*)(misc + 24);
-        a.stats = (BfsStats*)(misc + 256);
-        a.descs = (BfsDesc*)(misc + 256 + sizeof(BfsStats) * n_cfg);
+        a.op_hist = (unsigned long long*)(misc + 32);  // 19 counters, bytes 32..183
+        a.stats = (BfsStats*)(misc + 512);
+        a.descs = (BfsDesc*)(misc + 512 + sizeof(BfsStats) * n_cfg);
         MCTB_CUDA(cudaMemsetAsync(a.tags, 0, sz_tags, st));
         MCTB_CUDA(cudaMemsetAsync(a.queue, 0xff, sz_q, st));
-        MCTB_CUDA(cudaMemsetAsync(misc, 0, 256, st));
+        MCTB_CUDA(cudaMemsetAsync(misc, 0, 512, st));
         std::vector<BfsStats> init(n_cfg);
-        for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0};
+        for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0};
         MCTB_CUDA(cudaMemcpyAsync(a.stats, init.data(), sizeof(BfsStats) * n_cfg,
                                   cudaMemcpyHostToDevice, st));
         MCTB_CUDA(cudaMemcpyAsync((void*)a.descs, descs.data(), sizeof(BfsDesc) * n_cfg,
@@ -436,10 +525,10 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         cudaEventRecord(e1, st);
         MCTB_CUDA(cudaGetLastError());
         res->stats.resize(n_cfg);
-        unsigned long long misc_h[4];
+        unsigned long long misc_h[32];
         MCTB_CUDA(cudaMemcpyAsync(res->stats.data(), a.stats, sizeof(BfsStats) * n_cfg,
                                   cudaMemcpyDeviceToHost, st));
-        MCTB_CUDA(cudaMemcpyAsync(misc_h, misc, 32, cudaMemcpyDeviceToHost, st));
+        MCTB_CUDA(cudaMemcpyAsync(misc_h, misc, 256, cudaMemcpyDeviceToHost, st));
         MCTB_CUDA(cudaStreamSynchronize(st));
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
@@ -451,6 +540,12 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         for (const auto& x : res->stats) res->states += x.states;
         res->levels = 0;
         res->error = (int)(misc_h[3] & 0xffffffff);
+        if (getenv("MCTB_BFS_OPHIST")) {
+            fprintf(stderr, "[explore] generic successors by op:");
+            for (int o = 0; o < 19; ++o)
+                if (misc_h[4 + o]) fprintf(stderr, " op%d=%llu", o, misc_h[4 + o]);
+            fprintf(stderr, "\n");
+        }
         res->words = words;
         res->capacity = cap;
         if ((res->error == 1 || res->error == 2) && cap < cap_limit) {
@@ -525,6 +620,10 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
         o[7] = (int64_t)s.deadlocks;
     }
     if (info) {
+        uint64_t generic = 0;
+        for (const auto& x : r.stats) generic += x.generic;
+        if (getenv("MCTB_BFS_OPHIST"))
+            fprintf(stderr, "[mctb_explore] generic successors: %llu\n", (unsigned long long)generic);
         info[0] = (int64_t)r.capacity;
         info[1] = (int64_t)r.states;
         info[2] = r.words;

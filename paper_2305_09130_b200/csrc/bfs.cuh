@@ -14,7 +14,8 @@ struct BfsStats {
     unsigned long long states, transitions, terminals;
     long long min_time, max_time;
     unsigned long long deadlocks;
-    unsigned long long capped;  // the per-configuration state cap was reached
+    unsigned long long capped;   // the per-configuration state cap was reached
+    unsigned long long generic;  // successors built by the generic unpacked apply()
 };
 
 struct BfsResult {
