@@ -45,8 +45,9 @@ struct BfsArgs {
     uint32_t* queue;           // [queue_cap] slot indices, EMPTY until pushed
     uint64_t queue_cap;
     unsigned long long* head;
-    unsigned long long* tail;
-    long long* outstanding;
+    // tq = (tail << 32) | outstanding: queue reservations and the count of states
+    // discovered but not yet expanded move together in one atomic
+    unsigned long long* tq;
     BfsStats* stats;  // [n_cfg]
     int* error;       // 1 table full, 2 queue full, 3 model bug
     uint64_t cfg_cap; // per-configuration visited cap (ExploreLimits::max_states)
@@ -133,18 +134,16 @@ __device__ long long table_insert(const BfsArgs& a, const uint32_t* key, uint64_
 }
 
 // Pushes the lanes' new slots (fresh lanes) with one queue reservation per warp.
-__device__ __forceinline__ void push_fresh(const BfsArgs& a, bool fresh, long long slot,
-                                           BfsStats& st) {
+// Returns the number pushed (on every lane).
+__device__ __forceinline__ unsigned push_fresh(const BfsArgs& a, bool fresh, long long slot) {
     const int lane = threadIdx.x & 31;
     const unsigned mask = __ballot_sync(0xffffffffu, fresh);
-    if (!mask) return;
+    if (!mask) return 0;
     const int leader = __ffs(mask) - 1;
+    const unsigned cnt = __popc(mask);
     unsigned long long pos0 = 0;
     if (lane == leader) {
-        const unsigned cnt = __popc(mask);
-        atomicAdd((unsigned long long*)a.outstanding, (unsigned long long)cnt);
-        pos0 = atomicAdd(a.tail, (unsigned long long)cnt);
-        atomicAdd(&st.states, (unsigned long long)cnt);
+        pos0 = atomicAdd(a.tq, ((unsigned long long)cnt << 32) | cnt) >> 32;
         if (pos0 + cnt > a.queue_cap) atomicExch(a.error, 2);
     }
     pos0 = __shfl_sync(0xffffffffu, pos0, leader);
@@ -152,12 +151,9 @@ __device__ __forceinline__ void push_fresh(const BfsArgs& a, bool fresh, long lo
         const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1));
         if (pos < a.queue_cap) st_release32(&a.queue[pos], (uint32_t)slot);
     }
+    return cnt;
 }
 
-// In-place successor for the transitions behind the combinatorial state
-// explosion (an element reporting a busy tick, an element arriving at its
-// barrier): two field writes on the parent's packed words.  Everything else
-// goes through the generic unpacked apply() (machine.cuh).
 // Record writers for the in-place successors (field order of pack()).
 __device__ __forceinline__ void write_pex(uint32_t* row, const Layout& l, int p, const PexS& x) {
     const int o = l.off_pex + p * l.pex_bits;
@@ -279,6 +275,16 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     MState& s = parent[wib];
     Transition* en = enabled_s[wib];
     MState t;
+    // warp-local statistics of the current configuration, flushed on change/exit
+    int cur_cfg = -1;
+    unsigned long long n_states = 0, n_trans = 0;
+    auto flush = [&]() {
+        if (lane == 0 && cur_cfg >= 0) {
+            if (n_states) atomicAdd(&a.stats[cur_cfg].states, n_states);
+            if (n_trans) atomicAdd(&a.stats[cur_cfg].transitions, n_trans);
+        }
+        n_states = n_trans = 0;
+    };
     bool local = false;  // the warp continues with a successor it discovered itself
     for (;;) {
         const uint32_t* src;
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             unsigned long long h = 0;
             if (lane == 0) h = atomicAdd(a.head, 1ull);
             h = __shfl_sync(0xffffffffu, h, 0);
-            if (h >= a.queue_cap) return;
+            if (h >= a.queue_cap) break;
             // wait until entry h is pushed, or the sweep is over
             uint32_t slot = kEmpty;
             if (lane == 0) {
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     }
                     // the shared counters are read rarely: they are the working warps'
                     // atomics' cache line
-                    if ((it & 7) == 7 && (ld_relaxed_s64(a.outstanding) <= 0 ||
+                    if ((it & 7) == 7 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
                                           ld_relaxed32((const uint32_t*)a.error)))
                         break;
                     __nanosleep(ns);
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                 }
             }
             slot = __shfl_sync(0xffffffffu, slot, 0);
-            if (slot == kEmpty) return;
+            if (slot == kEmpty) break;
             // the key is published before its slot index is pushed
             src = a.keys + (uint64_t)slot * a.words;
             for (int k = lane; k < a.words; k += 32) pwords[k] = src[k];
@@ -317,6 +323,10 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             src = pwords;
         }
         const int cfg = peek_cfg(src, a.cfg_bits);
+        if (cfg != cur_cfg) {
+            flush();
+            cur_cfg = cfg;
+        }
         const BfsDesc& d = a.descs[cfg];
         // warp-parallel unpack and enumeration: lane i reads the records of process
         // slots i, i+32, ... and applies their rules (machine.cuh); a warp prefix sum
@@ -349,11 +359,11 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     atomicExch(a.error, 3);
                 }
             }
-        } else if (*(volatile unsigned long long*)&st.states >= a.cfg_cap) {
+        } else if (*(volatile unsigned long long*)&st.states + n_states >= a.cfg_cap) {
             // explore.cpp:28: a full visited set inserts nothing more
             if (lane == 0) st.capped = 1;
         } else {
-            if (lane == 0) atomicAdd(&st.transitions, (unsigned long long)ne);
+            n_trans += (unsigned)ne;
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
                 long long ins = -1;
@@ -361,8 +371,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     for (int k = 0; k < a.words; ++k) row[k] = pwords[k];
                     bool ok = true;
                     if (!fast_successor(d, s, en[e], row)) {
-                        atomicAdd(&st.generic, 1ull);
-                        atomicAdd(&a.op_hist[en[e].op], 1ull);
+                        if (a.op_hist) atomicAdd(&a.op_hist[en[e].op], 1ull);
                         copy_state(d.m, t, s);
                         ok = apply(d.m, t, en[e]);
                         if (ok) pack(d, cfg, t, row);
@@ -376,19 +385,17 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                 bool fresh = ins >= 0;
                 int keeper = -1;
                 if (!kept && a.keep) {
-                    // keep the first new successor: no queue round trip on the chain
+                    // keep the first new successor: no queue round trip on the chain; it
+                    // inherits the parent's place in `outstanding`
                     const unsigned m = __ballot_sync(0xffffffffu, fresh);
                     if (m) {
                         keeper = __ffs(m) - 1;
                         if (lane == keeper) fresh = false;
-                        if (lane == 0) {
-                            atomicAdd((unsigned long long*)a.outstanding, 1ull);
-                            atomicAdd(&st.states, 1ull);
-                        }
                         kept = true;
+                        n_states += 1;
                     }
                 }
-                push_fresh(a, fresh, ins, st);
+                n_states += push_fresh(a, fresh, ins);
                 if (keeper >= 0) {
                     __syncwarp();
                     const uint32_t* kr = pwords + (2 + keeper) * a.words;
@@ -398,13 +405,15 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             }
         }
         __syncwarp();
-        if (lane == 0) atomicAdd((unsigned long long*)a.outstanding, ~0ull);  // -1
         local = kept && !*(volatile int*)a.error;
         if (local) {
             for (int k = lane; k < a.words; k += 32) pwords[k] = kwords[k];
             __syncwarp();
+        } else if (lane == 0) {
+            atomicAdd(a.tq, ~0ull);  // this state is expanded: outstanding - 1
         }
     }
+    flush();
 }
 
 __global__ void seed_kernel(BfsArgs a) {
@@ -423,8 +432,7 @@ __global__ void seed_kernel(BfsArgs a) {
         return;
     }
     atomicAdd(&a.stats[c].states, 1ull);
-    atomicAdd((unsigned long long*)a.outstanding, 1ull);
-    const unsigned long long pos = atomicAdd(a.tail, 1ull);
+    const unsigned long long pos = atomicAdd(a.tq, (1ull << 32) | 1ull) >> 32;
     st_release32(&a.queue[pos], (uint32_t)ins);
 }
 
@@ -500,10 +508,9 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.queue = (uint32_t*)(b + sz_tags + sz_keys);
         char* misc = b + sz_tags + sz_keys + sz_q;
         a.head = (unsigned long long*)misc;
-        a.tail = (unsigned long long*)(misc + 8);
-        a.outstanding = (long long*)(misc + 16);
+        a.tq = (unsigned long long*)(misc + 8);
         a.error = (int*)(misc + 24);
-        a.op_hist = (unsigned long long*)(misc + 32);  // 19 counters, bytes 32..183
+        a.op_hist = getenv("MCTB_BFS_OPHIST") ? (unsigned long long*)(misc + 32) : nullptr;
         a.stats = (BfsStats*)(misc + 512);
         a.descs = (BfsDesc*)(misc + 512 + sizeof(BfsStats) * n_cfg);
         MCTB_CUDA(cudaMemsetAsync(a.tags, 0, sz_tags, st));
