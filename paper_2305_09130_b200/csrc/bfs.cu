@@ -111,9 +111,8 @@ __device__ long long table_insert(const BfsArgs& a, const uint32_t* key, uint64_
                 uint32_t* dst = a.keys + i * (uint64_t)a.words;
                 for (int k = 0; k < a.words; ++k) dst[k] = key[k];
                 // release: the key words become visible before the published bit
-                asm volatile("atom.release.gpu.global.or.b64 %0, [%1], 1;"
-                             : "=l"(t)
-                             : "l"(&a.tags[i])
+                // (a reduction: nothing waits for its result)
+                asm volatile("red.release.gpu.global.or.b64 [%0], 1;" ::"l"(&a.tags[i])
                              : "memory");
                 return (long long)i;
             }
@@ -307,11 +306,11 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     }
                     // the shared counters are read rarely: they are the working warps'
                     // atomics' cache line
-                    if ((it & 7) == 7 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
-                                          ld_relaxed32((const uint32_t*)a.error)))
+                    if ((it & 15) == 15 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
+                                            ld_relaxed32((const uint32_t*)a.error)))
                         break;
                     __nanosleep(ns);
-                    if (ns < 8192) ns <<= 1;
+                    if (ns < 1024) ns <<= 1;
                 }
             }
             slot = __shfl_sync(0xffffffffu, slot, 0);
