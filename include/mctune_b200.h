@@ -128,13 +128,15 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
 
 /* explore_machine (explore.hpp:272-277) over several configurations in one GPU sweep
  * (configs = int32[2 * n] of (wg, ts)); max_states = the reference's per-machine visited
- * cap (ExploreLimits::max_states, default 5e6 when <= 0).
- * out = int64[8 * n]: {complete, states_visited, transitions_applied, max_depth_reached,
- *                      min_final_time, max_final_time, terminal_states, deadlocks}
+ * cap (ExploreLimits::max_states, default 5e6 when <= 0); flags bit 0 = check
+ * Machine::check_invariants (machine.cpp:719-756) and tick gating on every state.
+ * out = int64[9 * n]: {complete, states_visited, transitions_applied, max_depth_reached,
+ *                      min_final_time, max_final_time, terminal_states, deadlocks,
+ *                      invariant_violations}
  * info = int64[4]: {table slots, total states, packed key words, kernel microseconds} */
 int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
-                 const int32_t* configs, int n_configs, int64_t max_states, int64_t* out,
-                 int64_t* info);
+                 const int32_t* configs, int n_configs, int64_t max_states, int flags,
+                 int64_t* out, int64_t* info);
 
 /* check_overtime (explore.hpp:279-284), exact mode.
  * out = int64[12]: {violated, exhaustive, states_visited, max_depth_reached,

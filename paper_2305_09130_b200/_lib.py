@@ -102,7 +102,8 @@ def i64arr(vals):
 def device_count() -> int:
     return lib.mctb_device_count()
 
-lib.mctb_explore.argtypes = [i32p, C.c_int, C.c_int, i64p, i32p, C.c_int, C.c_int64, i64p, i64p]
+lib.mctb_explore.argtypes = [i32p, C.c_int, C.c_int, i64p, i32p, C.c_int, C.c_int64, C.c_int,
+                             i64p, i64p]
 EXPORTED.append("mctb_explore")
 lib.mctb_check_overtime.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int64, C.c_int64, i64p,
                                     i32p, C.c_int64, i64p]

@@ -53,6 +53,7 @@ struct BfsArgs {
     uint64_t cfg_cap; // per-configuration visited cap (ExploreLimits::max_states)
     int keep;         // continue with the first new successor (no queue round trip)
     unsigned long long* op_hist;  // generic successors per op (diagnostics)
+    int check_inv;                // check Machine::check_invariants on every state
 };
 
 namespace {
@@ -346,6 +347,13 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         for (int k = lane; k < nsl; k += 32) pos = slot_rules(d.m, s, k, en, pos);
         __syncwarp();
         BfsStats& st = a.stats[cfg];
+        if (a.check_inv && lane == 0) {
+            // machine.cpp:719-756, plus tick gating (acceptance criterion 7)
+            bool bad = check_invariants(d.m, s) != 0;
+            for (int e = 0; e < ne; ++e)
+                bad |= en[e].op == OP_CLOCKTICK && (s.nrp_work != s.all_nwe || s.all_nwe == 0);
+            if (bad) atomicAdd(&st.violations, 1ull);
+        }
         bool kept = false;
         if (ne == 0) {
             if (lane == 0) {
@@ -439,7 +447,7 @@ __global__ void seed_kernel(BfsArgs a) {
 
 // ------------------------------------------------------------------ host
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
-            cudaStream_t st) {
+            cudaStream_t st, bool check_invariants) {
     const int n_cfg = (int)hs.size();
     std::vector<BfsDesc> descs(n_cfg);
     int32_t* d_ids = nullptr;
@@ -497,6 +505,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.queue_cap = qcap;
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
+        a.check_inv = check_invariants ? 1 : 0;
         const size_t sz_tags = cap * 8, sz_keys = cap * 4 * (size_t)words, sz_q = qcap * 4;
         const size_t sz_misc = 512 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg;
         void* blob = nullptr;
@@ -516,7 +525,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         MCTB_CUDA(cudaMemsetAsync(a.queue, 0xff, sz_q, st));
         MCTB_CUDA(cudaMemsetAsync(misc, 0, 512, st));
         std::vector<BfsStats> init(n_cfg);
-        for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0};
+        for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0, 0};
         MCTB_CUDA(cudaMemcpyAsync(a.stats, init.data(), sizeof(BfsStats) * n_cfg,
                                   cudaMemcpyHostToDevice, st));
         MCTB_CUDA(cudaMemcpyAsync((void*)a.descs, descs.data(), sizeof(BfsDesc) * n_cfg,
@@ -576,8 +585,8 @@ int check_machine(const int* plat, int size, int kernel, int wg, int ts);
 extern "C" {
 
 int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
-                 const int32_t* configs, int n_configs, int64_t max_states, int64_t* out,
-                 int64_t* info) {
+                 const int32_t* configs, int n_configs, int64_t max_states, int flags,
+                 int64_t* out, int64_t* info) {
     int rc;
     if (n_configs < 1) {
         set_error("no configurations");
@@ -594,7 +603,7 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     BfsResult r;
     const uint64_t cap = max_states > 0 ? (uint64_t)max_states : 5000000ull;
-    rc = run_bfs(hs, cap * (uint64_t)n_configs, cap, &r, st);
+    rc = run_bfs(hs, cap * (uint64_t)n_configs, cap, &r, st, (flags & 1) != 0);
     cudaStreamDestroy(st);
     if (rc) return rc;
     if (r.error == 3) {
@@ -607,7 +616,8 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     }
     for (int c = 0; c < n_configs; ++c) {
         const BfsStats& s = r.stats[c];
-        int64_t* o = out + 8 * c;
+        int64_t* o = out + 9 * c;
+        o[8] = (int64_t)s.violations;
         o[0] = !s.capped;
         o[1] = (int64_t)std::min<uint64_t>(s.states, cap);
         o[2] = (int64_t)s.transitions;

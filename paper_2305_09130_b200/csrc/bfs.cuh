@@ -16,6 +16,7 @@ struct BfsStats {
     unsigned long long deadlocks;
     unsigned long long capped;   // the per-configuration state cap was reached
     unsigned long long generic;  // successors built by the generic unpacked apply()
+    unsigned long long violations;  // states breaking Machine::check_invariants
 };
 
 struct BfsResult {
@@ -30,6 +31,6 @@ struct BfsResult {
 // whole table; cfg_cap is the per-configuration visited cap of the reference
 // (ExploreLimits::max_states, explore.hpp:227-233).
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
-            cudaStream_t st);
+            cudaStream_t st, bool check_invariants = false);
 
 }  // namespace mctb

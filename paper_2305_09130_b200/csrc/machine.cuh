@@ -247,6 +247,45 @@ __host__ __device__ inline void place_pex(const MachDesc& m, PexS& px) {
 }
 
 // Machine::is_terminal, machine.cpp:651-662
+// Machine::check_invariants, machine.cpp:719-756: 0 when every structural
+// invariant holds, else the number of the violated one (1 nrp_work range,
+// 2 all_nwe range, 3 barrier count vs waiting elements, 4 over-counted barrier,
+// 5 elements waiting at different barrier instances, 6 unit serving after fin,
+// 7 element working after fin).
+__host__ __device__ inline int check_invariants(const MachDesc& m, const MState& s) {
+    if (s.nrp_work < 0 || s.nrp_work > s.all_nwe) return 1;
+    if (s.all_nwe < 0 || s.all_nwe > m.all_nwe) return 2;
+    for (int g = 0; g < m.n_units; ++g) {
+        int waiting = 0, cursor = -1, phase = 0;
+        bool mixed = false;
+        for (int e = 0; e < m.nwe; ++e) {
+            const PexS& px = s.pex[g * m.nwe + e];
+            if (px.pc == P_WAITBARRIER || px.pc == P_WAITGROUPEND) {
+                if (waiting == 0) {
+                    cursor = px.cursor;
+                    phase = px.phase;
+                } else if (px.cursor != cursor || px.phase != phase) {
+                    mixed = true;
+                }
+                ++waiting;
+            }
+        }
+        if (s.bar[g].pc == B_COUNTING && s.bar[g].count != waiting) return 3;
+        if (s.bar[g].count > m.nwe) return 4;
+        if (mixed) return 5;
+    }
+    if (s.fin) {
+        for (int g = 0; g < m.n_units; ++g) {
+            const int pc = s.unit[g].pc;
+            if (pc != U_WAITGO && pc != U_STOPPEXES && pc != U_STOPBARRIER && pc != U_EXITED)
+                return 6;
+        }
+        for (int p = 0; p < m.n_pex; ++p)
+            if (s.pex[p].pc != P_WAITGO && s.pex[p].pc != P_EXITED) return 7;
+    }
+    return 0;
+}
+
 __host__ __device__ inline bool is_terminal(const MachDesc& m, const MState& s) {
     if (!s.fin || s.clock != 1 || s.host_pc != H_EXITED) return false;
     for (int d = 0; d < m.nwd; ++d)

@@ -26,6 +26,7 @@ class ExploreStats:
     max_time: int
     terminals: int
     deadlocks: int
+    invariant_violations: int = 0
 
 
 @dataclass
@@ -38,15 +39,16 @@ class SweepInfo:
 
 def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
                     configs: Sequence[TuningParams], max_states: int = 5_000_000,
-                    info: list | None = None) -> List[ExploreStats]:
+                    info: list | None = None, check_invariants: bool = False) -> List[ExploreStats]:
     cfg = i32arr([v for c in configs for v in (c.wg, c.ts)])
-    out = (C.c_int64 * (8 * len(configs)))()
+    out = (C.c_int64 * (9 * len(configs)))()
     inf = (C.c_int64 * 4)()
     check(lib.mctb_explore(platform.as_array(), problem.size, problem.kernel,
-                           problem.input_array(), cfg, len(configs), max_states, out, inf))
+                           problem.input_array(), cfg, len(configs), max_states,
+                           1 if check_invariants else 0, out, inf))
     if info is not None:
         info.append(SweepInfo(*inf))
-    return [ExploreStats(bool(out[8 * i]), *out[8 * i + 1:8 * i + 8]) for i in range(len(configs))]
+    return [ExploreStats(bool(out[9 * i]), *out[9 * i + 1:9 * i + 9]) for i in range(len(configs))]
 
 
 def explore_machine(platform: PlatformConfig, problem: ProblemSpec, params: TuningParams,

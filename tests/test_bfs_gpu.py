@@ -55,3 +55,42 @@ def test_state_limit_is_reported(engine):
     r = m.explore_machine(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(32),
                           m.TuningParams(16, 2), max_states=1000)
     assert not r.complete
+
+
+def test_acceptance_7_interleaving_invariants(engine):
+    """Every reachable state of every size-8 configuration (both kernels) keeps
+    Machine::check_invariants and tick gating; no deadlock; the final time is
+    schedule-independent and equals the deterministic run (acceptance 7, and
+    test_explore.cpp:145-170 for sizes 4-16)."""
+    m = engine
+    p = m.PlatformConfig(1, 1, 4, 4)
+    for prob in (m.ProblemSpec.abstract(4), m.ProblemSpec.abstract(8), m.ProblemSpec.abstract(16),
+                 m.ProblemSpec.minimum(8), m.ProblemSpec.minimum(16)):
+        cfgs = [c for c in m.enumerate_configs(prob.size) if m.config_feasible(prob, c)]
+        got = m.explore_configs(p, prob, cfgs, check_invariants=True)
+        for c, g in zip(cfgs, got):
+            assert g.complete and g.deadlocks == 0 and g.invariant_violations == 0, (prob, c)
+            assert g.min_time == g.max_time == m.Machine(p, prob, c).run().time, (prob, c)
+
+
+def test_multi_device_skew_minimum_is_lockstep_time(engine, oracle):
+    """test_explore.cpp:199-225: with two devices and host re-arming some
+    schedules are slower, but the explored minimum is the lock-step time."""
+    m = engine
+    g = m.explore_machine(m.PlatformConfig(2, 1, 2, 4), m.ProblemSpec.abstract(16),
+                          m.TuningParams(2, 2))
+    want = oracle.cost_model((2, 1, 2, 4), 16, 0, 2, 2)[0]
+    assert g.complete and g.min_time == want and g.max_time > want
+
+
+def test_acceptance_6_minimum_kernel_trend(engine):
+    m = engine
+    p = m.PlatformConfig(1, 1, 4, 4)
+
+    def max_wg_among_best(rows):
+        best = next(r.time for r in rows if r.ok)
+        return max(r.wg for r in rows if r.ok and r.time == best)
+    b16 = max_wg_among_best(m.exhaustive_sweep(p, m.ProblemSpec.minimum(16)))
+    b64 = max_wg_among_best(m.exhaustive_sweep(p, m.ProblemSpec.minimum(64)))
+    tuned = m.tune(p, m.ProblemSpec.minimum(16))
+    assert tuned.params.wg == b16 == 8 and b16 <= b64
