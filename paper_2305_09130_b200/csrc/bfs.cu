@@ -286,17 +286,26 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         n_states = n_trans = 0;
     };
     bool local = false;  // the warp continues with a successor it discovered itself
+    // queue entries are claimed in runs: a warp that finds its entries already
+    // filled doubles its next claim (up to 8), one that has to wait claims one
+    unsigned long long h_next = 0, h_end = 0;
+    unsigned claim = 1;
     for (;;) {
         const uint32_t* src;
         if (local) {
             src = pwords;  // already holds the kept successor
         } else {
-            unsigned long long h = 0;
-            if (lane == 0) h = atomicAdd(a.head, 1ull);
-            h = __shfl_sync(0xffffffffu, h, 0);
+            if (h_next == h_end) {
+                unsigned long long h0 = 0;
+                if (lane == 0) h0 = atomicAdd(a.head, (unsigned long long)claim);
+                h_next = __shfl_sync(0xffffffffu, h0, 0);
+                h_end = h_next + claim;
+            }
+            const unsigned long long h = h_next++;
             if (h >= a.queue_cap) break;
             // wait until entry h is pushed, or the sweep is over
             uint32_t slot = kEmpty;
+            bool waited = false;
             if (lane == 0) {
                 unsigned ns = 64;
                 for (unsigned it = 0;; ++it) {
@@ -305,6 +314,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                         slot = ld_acquire32(&a.queue[h]);
                         break;
                     }
+                    waited = true;
                     // the shared counters are read rarely: they are the working warps'
                     // atomics' cache line
                     if ((it & 15) == 15 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
@@ -315,6 +325,8 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                 }
             }
             slot = __shfl_sync(0xffffffffu, slot, 0);
+            waited = __shfl_sync(0xffffffffu, waited, 0);
+            claim = waited ? 1u : (claim < 8u ? claim * 2u : 8u);
             if (slot == kEmpty) break;
             // the key is published before its slot index is pushed
             src = a.keys + (uint64_t)slot * a.words;
