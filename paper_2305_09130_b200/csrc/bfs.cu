@@ -435,22 +435,32 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     flush();
 }
 
-__global__ void seed_kernel(BfsArgs a) {
-    // one initial state per configuration (explore.cpp:98-105)
+__global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
+    // one initial state per configuration (explore.cpp:98-105), or the given
+    // packed states of configuration 0 (a multi-source exploration)
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= a.n_cfg) return;
-    const BfsDesc& d = a.descs[c];
-    MState s;
-    initial_state(d.m, s);
     uint32_t key[kMaxWords];
-    pack(d, c, s, key);
-    for (int k = d.l.words; k < a.words; ++k) key[k] = 0;
+    int cfg = c;
+    if (seeds) {
+        if (c >= n_seeds) return;
+        cfg = 0;
+        for (int k = 0; k < a.words; ++k) key[k] = seeds[(size_t)c * a.words + k];
+    } else {
+        if (c >= a.n_cfg) return;
+        const BfsDesc& d = a.descs[c];
+        MState s;
+        initial_state(d.m, s);
+        pack(d, c, s, key);
+        for (int k = d.l.words; k < a.words; ++k) key[k] = 0;
+    }
     const long long ins = table_insert(a, key, hash_words(key, a.words));
+    if (ins == -1) return;  // a repeated seed
     if (ins < 0) {
         atomicExch(a.error, 1);
         return;
     }
-    atomicAdd(&a.stats[c].states, 1ull);
+    const int c_ = cfg;
+    atomicAdd(&a.stats[c_].states, 1ull);
     const unsigned long long pos = atomicAdd(a.tq, (1ull << 32) | 1ull) >> 32;
     st_release32(&a.queue[pos], (uint32_t)ins);
 }
@@ -458,8 +468,16 @@ __global__ void seed_kernel(BfsArgs a) {
 }  // namespace
 
 // ------------------------------------------------------------------ host
+Layout bfs_layout(const MachDesc& m, int n_cfg) {
+    // time bound: every tick consumes >= 1 busy tick of some element
+    const int64_t groups = (int64_t)m.device_rounds * m.nwu;
+    const int64_t per_item = m.kernel == 0 ? (int64_t)m.reps * (m.gmt * m.ts + m.ts) + m.gmt
+                                           : (int64_t)m.ts * m.gmt + m.nwe + m.gmt;
+    return make_layout(m, n_cfg, groups * m.wg * per_item + 1);
+}
+
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
-            cudaStream_t st, bool check_invariants) {
+            cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds) {
     const int n_cfg = (int)hs.size();
     std::vector<BfsDesc> descs(n_cfg);
     int32_t* d_ids = nullptr;
@@ -470,11 +488,8 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         MachDesc m = hs[c].d;
         m.input_id = d_ids;
         // time bound: every tick consumes >= 1 busy tick of some element
-        const int64_t groups = (int64_t)m.device_rounds * m.nwu;
-        const int64_t per_item = m.kernel == 0 ? (int64_t)m.reps * (m.gmt * m.ts + m.ts) + m.gmt
-                                               : (int64_t)m.ts * m.gmt + m.nwe + m.gmt;
         descs[c].m = m;
-        descs[c].l = make_layout(m, n_cfg, groups * m.wg * per_item + 1);
+        descs[c].l = bfs_layout(m, n_cfg);
         if (descs[c].l.time > 32 || descs[c].l.words > kMaxWords) {
             set_error("state does not fit the GPU packing (time > 2^32 or > 24 words)");
             cudaFreeAsync(d_ids, st);
@@ -542,7 +557,17 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
                                   cudaMemcpyHostToDevice, st));
         MCTB_CUDA(cudaMemcpyAsync((void*)a.descs, descs.data(), sizeof(BfsDesc) * n_cfg,
                                   cudaMemcpyHostToDevice, st));
-        seed_kernel<<<(n_cfg + 127) / 128, 128, 0, st>>>(a);
+        uint32_t* d_seeds = nullptr;
+        int n_seeds = 0;
+        if (seeds && !seeds->empty()) {
+            n_seeds = (int)(seeds->size() / words);
+            MCTB_CUDA(cudaMallocAsync(&d_seeds, seeds->size() * 4, st));
+            MCTB_CUDA(cudaMemcpyAsync(d_seeds, seeds->data(), seeds->size() * 4,
+                                      cudaMemcpyHostToDevice, st));
+        }
+        const int n_first = seeds ? n_seeds : n_cfg;
+        seed_kernel<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds);
+        if (d_seeds) cudaFreeAsync(d_seeds, st);
         MCTB_CUDA(cudaGetLastError());
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);

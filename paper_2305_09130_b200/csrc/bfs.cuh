@@ -6,6 +6,7 @@
 
 #include <vector>
 
+#include "pack.cuh"
 #include "traj.cuh"
 
 namespace mctb {
@@ -30,7 +31,18 @@ struct BfsResult {
 // Explores every configuration in `hs` in one sweep.  max_states bounds the
 // whole table; cfg_cap is the per-configuration visited cap of the reference
 // (ExploreLimits::max_states, explore.hpp:227-233).
+// seeds (optional): packed states of configuration 0 (layout bfs_layout(hs[0].d, 1))
+// to start from instead of the initial states — a multi-source exploration.
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
-            cudaStream_t st, bool check_invariants = false);
+            cudaStream_t st, bool check_invariants = false,
+            const std::vector<uint32_t>* seeds = nullptr);
+
+// The packed layout the exploration uses for a configuration among n_cfg.
+Layout bfs_layout(const MachDesc& m, int n_cfg);
+
+// The reference DFS's counterexample for bound T (lexfirst.cu).
+int lexfirst_path(MachHost& h, int64_t T, int64_t max_len, const Layout& layout,
+                  std::vector<int32_t>* path, int64_t* final_time, int64_t* sibling_applies,
+                  std::vector<uint32_t>* siblings, int* n_siblings);
 
 }  // namespace mctb

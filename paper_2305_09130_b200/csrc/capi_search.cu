@@ -38,6 +38,16 @@ int gpu_run(MachHost& h, int policy, uint64_t seed, uint64_t traj, int64_t max_s
 
 namespace {
 
+// The DFS's counterexample and search effort for a schedule-dependent
+// configuration at bound T (lexfirst.cu + a multi-source exploration of the
+// siblings the DFS abandons).
+struct Walk {
+    int k = -1;
+    int64_t T = -1;
+    std::vector<int32_t> path;
+    int64_t final_time = -1, applies = 0, sib_states = 0, sib_transitions = 0;
+};
+
 struct Ctx {
     int plat[4];
     int size = 0, kernel = 0;
@@ -49,14 +59,51 @@ struct Ctx {
     std::vector<MachHost> hs;
     BfsResult bfs;
     std::vector<int64_t> first_time, first_steps;
+    std::vector<Walk> walks;
     double ms_cost = 0, ms_bfs = 0, ms_first = 0;
 };
+
+int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
+    for (const Walk& w : c.walks)
+        if (w.k == k && w.T == T) {
+            *out = &w;
+            return MCTB_OK;
+        }
+    Walk w;
+    w.k = k;
+    w.T = T;
+    std::vector<uint32_t> sib;
+    int n_sib = 0;
+    const Layout lay = bfs_layout(c.hs[k].d, 1);
+    int rc = lexfirst_path(c.hs[k], T, 4 * c.cm_steps[k] + 4096, lay, &w.path, &w.final_time,
+                           &w.applies, &sib, &n_sib);
+    if (rc) return rc;
+    if (n_sib > 0) {
+        std::vector<MachHost> one(1, c.hs[k]);
+        BfsResult r;
+        cudaStream_t st;
+        MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib);
+        cudaStreamDestroy(st);
+        if (rc) return rc;
+        if (r.error) {
+            set_error("model bug or capacity limit in the sibling exploration");
+            return r.error == 3 ? MCTB_MODEL_BUG : MCTB_LIMIT;
+        }
+        w.sib_states = (int64_t)std::min<uint64_t>(r.stats[0].states, c.cap);
+        w.sib_transitions = (int64_t)r.stats[0].transitions;
+    }
+    c.walks.push_back(std::move(w));
+    *out = &c.walks.back();
+    return MCTB_OK;
+}
 
 struct VerdictOut {
     bool violated = false, exhaustive = false, trace_exact = true;
     int64_t states = 0, transitions = 0, max_depth = 0, explored = 0;
     int cfg = -1;  // index of the violating configuration
     int64_t final_time = -1, steps = 0;
+    const std::vector<int32_t>* path = nullptr;  // guided-walk counterexample, if any
 };
 
 double now_ms() {
@@ -184,14 +231,17 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
                 v.transitions += v.steps;
                 v.max_depth = std::max(v.max_depth, v.steps);
             } else {
-                // schedule-dependent configuration: a lock-step counterexample is
-                // emitted instead of the DFS's lexicographically first one
-                v.trace_exact = false;
-                v.final_time = tmin;
-                v.steps = c.cm_steps[k];
-                v.states += v.steps + 1;
-                v.transitions += v.steps;
-                v.max_depth = std::max(v.max_depth, v.steps);
+                // schedule-dependent configuration: the DFS backtracks into later
+                // branches; its first satisfying path comes from the guided walk and
+                // its effort from the abandoned siblings' exploration
+                const Walk* w = nullptr;
+                if ((*rc_out = ensure_walk(c, k, T, &w))) return v;
+                v.path = &w->path;
+                v.final_time = w->final_time;
+                v.steps = (int64_t)(w->path.size() / 4);
+                v.states += 1 + v.steps + w->sib_states;
+                v.transitions += w->applies + w->sib_transitions;
+                v.max_depth = std::max(v.max_depth, v.steps);  // DFS depth of the path
             }
             v.exhaustive = false;
             return v;
@@ -210,6 +260,11 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
 int emit_trace(Ctx& c, const VerdictOut& v, int32_t* trace, int64_t cap, int64_t* trace_len) {
     if (trace_len) *trace_len = v.steps;
     if (!trace || cap <= 0 || v.cfg < 0) return MCTB_OK;
+    if (v.path) {
+        const size_t n = std::min<size_t>(v.path->size(), (size_t)cap * 4);
+        std::memcpy(trace, v.path->data(), n * sizeof(int32_t));
+        return MCTB_OK;
+    }
     TrajOut o;
     const int policy = v.trace_exact ? MCTB_POLICY_FIRST : MCTB_POLICY_TICK_LAST;
     int rc = gpu_run(c.hs[v.cfg], policy, 0, 0, 200000000LL, &o, trace, cap);

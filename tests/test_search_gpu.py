@@ -100,3 +100,41 @@ def test_rank_trails_contract(engine):
     r = m.rank_trails([mk(50, 2, 2, 10), mk(44, 4, 4, 1700), mk(44, 2, 4, 1650)])
     assert [(x.time, x.transitions) for x in r] == [(44, 1650), (44, 1700), (50, 10)]
     assert m.rank_trails([]) == []
+
+
+def _tune_matches(m, c):
+    r = m.tune(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]), seed=c["seed"])
+    key = (c["plat"], c["size"], c["kernel"], c["seed"])
+    assert (r.t_min, r.params.wg, r.params.ts) == (c["t_min"], c["wg"], c["ts"]), key
+    assert (r.t_ini, r.first_trail_time, r.proven) == (
+        c["t_ini"], c["first_trail_time"], bool(c["proven"])), key
+    assert (r.stats.checks_run, r.stats.states_visited_total) == (
+        c["checks_run"], c["states_visited_total"]), key
+    assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
+
+
+def test_tune_bit_exact_on_multi_device_platforms(engine, gold):
+    """96 platforms with nd in {2,3}, nu in {1,2}: host re-arming makes some
+    schedules slower than the lock-step time."""
+    for c in gold("tune_multidevice.json"):
+        _tune_matches(engine, c)
+
+
+def test_schedule_dependent_counterexamples(engine, gold):
+    """Bounds where the violating configuration's first DFS path is too slow:
+    the reference's DFS backtracks; the GPU reproduces its counterexample
+    (guided walk) and its search effort (sibling exploration)."""
+    m = engine
+    g = gold("skew.json")
+    for c in g["checks"]:
+        v = m.check_overtime(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]),
+                             c["T"])
+        key = (c["plat"], c["size"], c["T"])
+        assert v.violated and v.trace_exact, key
+        assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
+            c["final_time"], c["wg"], c["ts"], c["steps"]), key
+        assert sha(v.trace.transitions) == c["trace_sha"], key
+        assert (v.stats.states_visited, v.stats.transitions_applied) == (
+            c["states"], c["transitions"]), key
+    for c in g["tunes"]:
+        _tune_matches(m, c)
