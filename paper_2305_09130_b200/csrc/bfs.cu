@@ -592,6 +592,11 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         for (const auto& x : res->stats) res->states += x.states;
         res->levels = 0;
         res->error = (int)(misc_h[3] & 0xffffffff);
+        // explore.cpp:28-31: a visited set holding max_states refuses every later
+        // insert, so reaching the cap ends the exhaustive claim (statistics are
+        // flushed per warp, so the final count decides)
+        for (auto& x : res->stats)
+            if (x.states >= cfg_cap) x.capped = 1;
         if (getenv("MCTB_BFS_OPHIST")) {
             fprintf(stderr, "[explore] generic successors by op:");
             for (int o = 0; o < 19; ++o)
