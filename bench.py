@@ -406,6 +406,22 @@ def secondary_metrics(m, with_reference=True):
                                 "(1,1,4,4), all 9 configurations (host API, incl. copies)",
                     "seconds": el, "trajectories_per_s": 1e6 / el,
                     "transitions_per_s": sum(b.steps) / el, "min_time": min(b.time)}
+    if with_reference:
+        # the same trajectories replayed by the CPU port (oracle, all host cores)
+        from concurrent.futures import ThreadPoolExecutor
+        orc = checkers.Oracle()
+        threads = os.cpu_count() or 1
+        per = 2000
+        cfg = [(c.wg, c.ts) for c in cfgs]
+
+        def work(w):
+            orc.trajectories((1, 1, 4, 4), 16, 0, cfg, 3, 1, w * per, per)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(work, range(threads)))
+        cel = time.perf_counter() - t0
+        out["swarm"]["cpu_port_trajectories_per_s"] = threads * per / cel
+        out["swarm"]["cpu_port_cores"] = threads
     return out
 
 
