@@ -395,17 +395,28 @@ def secondary_metrics(m, with_reference=True):
                                   f"{rx['states']} states in {el:.2f} s, 1 core")
     out["explore"] = ex
     # (3) swarm trajectories: 10^6 Philox schedules over every configuration, size 16
+    import ctypes as C
+    from paper_2305_09130_b200._lib import i32arr, lib
     plat = m.PlatformConfig(1, 1, 4, 4)
     prob = m.ProblemSpec.abstract(16)
     cfgs = m.enumerate_configs(16)
-    m.trajectories(plat, prob, cfgs, m.PHILOX, 1, 0, 4096)
+    ntr = 1_000_000
+    carr = i32arr([v for c in cfgs for v in (c.wg, c.ts)])
+    outb = (C.c_int64 * (6 * ntr))()
+    lib.mctb_trajectories(plat.as_array(), 16, 0, None, carr, len(cfgs), 3, C.c_uint64(1),
+                          C.c_uint64(0), C.c_uint64(4096), C.c_int64(200_000_000), outb)
     t0 = time.perf_counter()
-    b = m.trajectories(plat, prob, cfgs, m.PHILOX, 1, 0, 1_000_000)
+    rc = lib.mctb_trajectories(plat.as_array(), 16, 0, None, carr, len(cfgs), 3, C.c_uint64(1),
+                               C.c_uint64(0), C.c_uint64(ntr), C.c_int64(200_000_000), outb)
     el = time.perf_counter() - t0
+    assert rc == 0
+    steps = sum(outb[1::6][:ntr])
     out["swarm"] = {"workload": "1e6 Philox4x32-10 schedule trajectories, abstract kernel, size 16, "
-                                "(1,1,4,4), all 9 configurations (host API, incl. copies)",
-                    "seconds": el, "trajectories_per_s": 1e6 / el,
-                    "transitions_per_s": sum(b.steps) / el, "min_time": min(b.time)}
+                                "(1,1,4,4), all 9 configurations, through mctb_trajectories "
+                                "(host buffers: per-trajectory time, transitions, result, status, "
+                                "trace hash copied back)",
+                    "seconds": el, "trajectories_per_s": ntr / el,
+                    "transitions_per_s": steps / el, "min_time": min(outb[0::6][:ntr])}
     if with_reference:
         # the same trajectories replayed by the CPU port (oracle, all host cores)
         from concurrent.futures import ThreadPoolExecutor
