@@ -514,8 +514,10 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double slot_bytes = 8 + 4.0 * words + 2.0;  // tag + key + queue (half the slots)
     // capacity grows 8x on overflow; the sweep restarts (all counts are rebuilt)
+    // first capacity: enough for the bound up to 2^28 slots (a restart loses the
+    // work done, so large sweeps start large); then 8x per overflow
     uint64_t cap = 1ull << 20;
-    while (cap < 2 * std::min<uint64_t>(max_states, 1ull << 22)) cap <<= 1;
+    while (cap < 2 * std::min<uint64_t>(max_states, 1ull << 27)) cap <<= 1;
     const uint64_t cap_limit = [&] {
         uint64_t c = 1024;
         while ((double)(c * 2) * slot_bytes < 0.8 * (double)free_b) c <<= 1;

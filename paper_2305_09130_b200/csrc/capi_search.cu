@@ -195,6 +195,15 @@ int prepare(Ctx& c, int64_t max_states) {
 // The first path of explore_machine's DFS for configuration k (GPU run, en[0] policy).
 int ensure_first(Ctx& c, int k) {
     if (c.first_time[k] >= 0) return MCTB_OK;
+    const BfsStats& b = c.bfs.stats[k];
+    if (!b.capped && b.terminals > 0 && b.min_time == b.max_time) {
+        // every run of this configuration was explored and ends at one time, so
+        // every run has the same length (protocol transitions + time): the first
+        // path is known without stepping it
+        c.first_time[k] = b.min_time;
+        c.first_steps[k] = c.cm_steps[k] - c.cm_time[k] + b.min_time;
+        return MCTB_OK;
+    }
     const double t0 = now_ms();
     TrajOut o;
     int rc = gpu_run(c.hs[k], MCTB_POLICY_FIRST, 0, 0, 200000000LL, &o, nullptr, 0);
