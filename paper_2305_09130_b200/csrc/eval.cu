@@ -102,29 +102,27 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                 // R -= Q (one correction Q -= 1, R += nd+1 when R < 0 and Q <= nd+1, a real
                 // division otherwise), so the loop issues no XU (I2F/MUFU/F2I) work.
                 const uint32_t w_hi = q == 0 ? dr : (dr + q - 1) / q;
-                // t = waves * D saturates at kKeySat: compare waves against the largest
-                // non-saturating count once instead of a 64-bit product per configuration
-                const uint32_t w_max = kKeySat / D32;  // D32 >= 1, D < kKeySat
                 uint32_t Q = dr / nd;
                 int32_t R = (int32_t)(dr - Q * nd);
                 uint32_t best_k = 0xffffffffu;
                 for (uint32_t k = 0; k < run; ++k) {
                     const uint32_t waves = (q == 0 || nd >= nd_thr) ? w_hi : Q + (R != 0);
-                    const uint32_t tf = waves <= w_max ? waves * D32 : kKeySat;
+                    const uint64_t t = (uint64_t)waves * D32;
+                    const uint32_t tf = t < kKeySat ? (uint32_t)t : kKeySat;
                     if (tf < best_tf) {
                         best_tf = tf;
                         best_k = k;
                     }
                     ++nd;
                     R -= (int32_t)Q;
-                    // one correction step (Q <= nd) is branch-free; a real division is
-                    // only needed while nd is below sqrt(dr)
-                    const bool fix = R < 0 && Q <= nd;
-                    Q -= fix ? 1u : 0u;
-                    R += fix ? (int32_t)nd : 0;
-                    if (__builtin_expect(R < 0, 0)) {
-                        Q = dr / nd;
-                        R = (int32_t)(dr - Q * nd);
+                    if (R < 0) {
+                        if (Q <= nd) {
+                            Q -= 1;
+                            R += (int32_t)nd;
+                        } else {
+                            Q = dr / nd;
+                            R = (int32_t)(dr - Q * nd);
+                        }
                     }
                 }
                 if (best_k != 0xffffffffu) best_idx = base + best_k;
