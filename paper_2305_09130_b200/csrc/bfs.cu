@@ -9,10 +9,13 @@
 //   * one warp per state, one lane per enabled transition (machine.cuh):
 //     unpack the parent, apply the lane's transition, pack the successor
 //     (pack.cuh) and insert it into the visited table;
-//   * visited table in HBM, lock-free open addressing:
-//       tag[slot]  64-bit = fingerprint | 2 (claimed) | 1 (key published)
-//       keys[slot] the packed state, written once by the claiming lane
-//     exact: a fingerprint match is confirmed on the full packed key;
+//   * visited table in HBM, lock-free open addressing over 64- or 128-byte
+//     slots: {key words, guard-filled padding, 64-bit tag}.  A probe is one
+//     line read (tag and key in the same round trip); an empty tag is claimed
+//     with a CAS and the claimer writes the key after it.  Key words carry a
+//     guard bit (pack.cuh), so a reader that races the writer sees a word
+//     without it and reads again — no release/acquire pair on the table;
+//     exact: a tag match is confirmed on the full packed key;
 //   * work queue = the slot indices of new states in discovery order
 //     (pre-filled with EMPTY); producers bump `tail` (one atomic per warp via
 //     ballot), consumers bump `head`; `outstanding` counts states pushed but
@@ -29,6 +32,7 @@
 #include "bfs.cuh"
 #include "common.cuh"
 #include "cost_model.cuh"
+#include "bfs_rules.cuh"
 #include "pack.cuh"
 #include "traj.cuh"
 
@@ -40,14 +44,15 @@ struct BfsArgs {
     int words;                 // key words per slot (max over configurations)
     int cfg_bits;
     uint64_t cap_mask;         // table capacity - 1 (power of two)
-    unsigned long long* tags;  // [cap]
-    uint32_t* keys;            // [cap * words]
+    uint32_t* table;           // [cap * SW]: slot = {key, padding, tag}
     uint32_t* queue;           // [queue_cap] slot indices, EMPTY until pushed
     uint64_t queue_cap;
     unsigned long long* head;
     // tq = (tail << 32) | outstanding: queue reservations and the count of states
     // discovered but not yet expanded move together in one atomic
     unsigned long long* tq;
+    const uint32_t* ftab;  // [n_cfg * kMaxFields] field tables (bfs_rules.cuh)
+    const int* nfields;    // [n_cfg]
     BfsStats* stats;  // [n_cfg]
     int* error;       // 1 table full, 2 queue full, 3 model bug
     uint64_t cfg_cap; // per-configuration visited cap (ExploreLimits::max_states)
@@ -61,18 +66,6 @@ namespace {
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kBfsThreads = 256;
 
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 __device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -85,50 +78,81 @@ __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long l
     return v;
 }
 
-__device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void ld_relaxed_v4(const uint32_t* p, uint32_t* v) {
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "l"(p)
+                 : "memory");
 }
 
-__device__ __forceinline__ long long ld_relaxed_s64(const long long* p) {
-    long long v;
-    asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
+// One slot line (SW words: key + padding + tag) from L2, 16 bytes per load.
+template <int SW>
+__device__ __forceinline__ void ld_line(const uint32_t* p, uint32_t (&v)[SW]) {
+#pragma unroll
+    for (int c = 0; c < SW / 4; ++c) ld_relaxed_v4(p + 4 * c, v + 4 * c);
+}
+
+// The SW-2 key/padding words of a slot (the tag is not touched).
+template <int SW>
+__device__ __forceinline__ void st_key(uint32_t* p, const uint32_t* row) {
+#pragma unroll
+    for (int c = 0; c < (SW - 2) / 4; ++c)
+        *reinterpret_cast<uint4*>(p + 4 * c) = *reinterpret_cast<const uint4*>(row + 4 * c);
+    *reinterpret_cast<uint2*>(p + SW - 4) = *reinterpret_cast<const uint2*>(row + SW - 4);
+}
+
+template <int SW>
+__device__ __forceinline__ void copy_key(uint32_t* dst, const uint32_t* src) {
+#pragma unroll
+    for (int c = 0; c < (SW - 2) / 4; ++c)
+        *reinterpret_cast<uint4*>(dst + 4 * c) = *reinterpret_cast<const uint4*>(src + 4 * c);
+    *reinterpret_cast<uint2*>(dst + SW - 4) = *reinterpret_cast<const uint2*>(src + SW - 4);
 }
 
 // Returns the slot of a newly inserted key, -1 if already present, -2 if full.
-__device__ long long table_insert(const BfsArgs& a, const uint32_t* key, uint64_t h) {
-    const unsigned long long tag = (h | 3ull);
-    const unsigned long long claim = tag & ~1ull;
+// `row` holds the key padded with guard words to SW-2 words.
+template <int SW>
+__device__ long long table_insert(const BfsArgs& a, const uint32_t* row, uint64_t h) {
+    const unsigned long long fp = h | 1ull;  // nonzero: 0 marks an empty slot
     uint64_t i = h & a.cap_mask;
     // a probe sequence this long only happens in a table that is too full: report it
     // (the sweep restarts with a larger table) instead of scanning the whole table
     for (uint64_t probe = 0; probe < 4096; ++probe, i = (i + 1) & a.cap_mask) {
-        // relaxed probe (an acquire load invalidates the SM's L1 — CCTL.IVALL — so it
-        // is only issued on a fingerprint match, before the key words are read)
-        unsigned long long t = ld_relaxed64(&a.tags[i]);
+        uint32_t* sl = a.table + i * SW;
+        uint32_t v[SW];
+        ld_line<SW>(sl, v);
+        unsigned long long t = (unsigned long long)v[SW - 2] | ((unsigned long long)v[SW - 1] << 32);
         if (t == 0) {
-            const unsigned long long prev = atomicCAS(&a.tags[i], 0ull, claim);
-            if (prev == 0) {
-                uint32_t* dst = a.keys + i * (uint64_t)a.words;
-                for (int k = 0; k < a.words; ++k) dst[k] = key[k];
-                // release: the key words become visible before the published bit
-                // (a reduction: nothing waits for its result)
-                asm volatile("red.release.gpu.global.or.b64 [%0], 1;" ::"l"(&a.tags[i])
-                             : "memory");
+            t = atomicCAS(reinterpret_cast<unsigned long long*>(sl + SW - 2), 0ull, fp);
+            if (t == 0) {
+                st_key<SW>(sl, row);
                 return (long long)i;
             }
-            t = prev;
+            // claimed meanwhile: its key is read below if the fingerprint matches
+#pragma unroll
+            for (int k = 0; k < SW - 2; ++k) v[k] = 0;
         }
-        if ((t | 1ull) != tag) continue;  // different fingerprint
-        t = ld_acquire(&a.tags[i]);
-        while (!(t & 1ull)) {  // claimed, key not yet published
-            __nanosleep(32);
-            t = ld_acquire(&a.tags[i]);
+        if (t != fp) continue;  // different fingerprint
+        for (unsigned ns = 32, spins = 0;; ++spins) {
+            bool eq = true, torn = false;
+#pragma unroll
+            for (int k = 0; k < SW - 2; ++k) {
+                eq &= v[k] == row[k];
+                torn |= !(v[k] & kGuard);
+            }
+            if (!torn) {
+                if (eq) return -1;
+                break;
+            }
+            // the claimer is still writing the key
+            if (spins > (1u << 21)) {  // watchdog: a key that never completes
+                atomicExch(a.error, 5);
+                return -3;
+            }
+            __nanosleep(ns);
+            if (ns < 512) ns <<= 1;
+            ld_line<SW>(sl, v);
         }
-        const uint32_t* src = a.keys + i * (uint64_t)a.words;
-        bool eq = true;
-        for (int k = 0; k < a.words && eq; ++k) eq = src[k] == key[k];
-        if (eq) return -1;
     }
     return -2;
 }
@@ -149,31 +173,36 @@ __device__ __forceinline__ unsigned push_fresh(const BfsArgs& a, bool fresh, lon
     pos0 = __shfl_sync(0xffffffffu, pos0, leader);
     if (fresh) {
         const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1));
-        if (pos < a.queue_cap) st_release32(&a.queue[pos], (uint32_t)slot);
+        // relaxed: the consumer re-reads the slot until every guard bit is set
+        if (pos < a.queue_cap) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&a.queue[pos]),
+                                            "r"((uint32_t)slot) : "memory");
     }
     return cnt;
 }
 
-// Record writers for the in-place successors (field order of pack()).
-__device__ __forceinline__ void write_pex(uint32_t* row, const Layout& l, int p, const PexS& x) {
+// Record writers for the in-place successors (field order of pack()); every
+// rewritten word also updates the state hash H.
+__device__ __forceinline__ void write_pex(uint32_t* row, const Layout& l, int p, const PexS& x,
+                                          const uint64_t* hk, uint64_t& H) {
     const int o = l.off_pex + p * l.pex_bits;
-    set_bits(row, o, 4, (uint32_t)x.pc);
-    set_bits(row, o + 4, 1, (uint32_t)x.phase);
-    set_bits(row, o + 5, l.cursor, x.cursor);
-    set_bits(row, o + 5 + l.cursor, l.busy, x.busy_left);
-    set_bits(row, o + 5 + l.cursor + l.busy, 1, (uint32_t)x.reported);
-    set_bits(row, o + 6 + l.cursor + l.busy, l.pnwg, (uint32_t)x.nwg);
-    set_bits(row, o + 6 + l.cursor + l.busy + l.pnwg, l.iter, x.iter);
+    set_bits_h(row, o, 4, (uint32_t)x.pc, hk, H);
+    set_bits_h(row, o + 4, 1, (uint32_t)x.phase, hk, H);
+    set_bits_h(row, o + 5, l.cursor, x.cursor, hk, H);
+    set_bits_h(row, o + 5 + l.cursor, l.busy, x.busy_left, hk, H);
+    set_bits_h(row, o + 5 + l.cursor + l.busy, 1, (uint32_t)x.reported, hk, H);
+    set_bits_h(row, o + 6 + l.cursor + l.busy, l.pnwg, (uint32_t)x.nwg, hk, H);
+    set_bits_h(row, o + 6 + l.cursor + l.busy + l.pnwg, l.iter, x.iter, hk, H);
 }
 
-__device__ __forceinline__ void write_unit(uint32_t* row, const Layout& l, int g, const UnitS& u) {
+__device__ __forceinline__ void write_unit(uint32_t* row, const Layout& l, int g, const UnitS& u,
+                                           const uint64_t* hk, uint64_t& H) {
     const int o = l.off_units + g * l.unit_bits;
-    set_bits(row, o, 3, (uint32_t)u.pc);
-    set_bits(row, o + 3, l.uk, (uint32_t)u.k);
-    set_bits(row, o + 3 + l.uk, l.nwg, (uint32_t)u.nwg);
-    set_bits(row, o + 3 + l.uk + l.nwg, l.sent, (uint32_t)u.sent);
-    set_bits(row, o + 3 + l.uk + l.nwg + l.sent, l.items, (uint32_t)u.got_items);
-    set_bits(row, o + 3 + l.uk + l.nwg + l.sent + l.items, l.ends, (uint32_t)u.got_ends);
+    set_bits_h(row, o, 3, (uint32_t)u.pc, hk, H);
+    set_bits_h(row, o + 3, l.uk, (uint32_t)u.k, hk, H);
+    set_bits_h(row, o + 3 + l.uk, l.nwg, (uint32_t)u.nwg, hk, H);
+    set_bits_h(row, o + 3 + l.uk + l.nwg, l.sent, (uint32_t)u.sent, hk, H);
+    set_bits_h(row, o + 3 + l.uk + l.nwg + l.sent, l.items, (uint32_t)u.got_items, hk, H);
+    set_bits_h(row, o + 3 + l.uk + l.nwg + l.sent + l.items, l.ends, (uint32_t)u.got_ends, hk, H);
 }
 
 // In-place successors for the transitions behind the combinatorial state
@@ -181,35 +210,36 @@ __device__ __forceinline__ void write_unit(uint32_t* row, const Layout& l, int g
 // the unit <-> element handshakes (activation, item done, group done, stop).
 // They touch one element record, its unit record and at most one header field;
 // the new values follow Machine::apply (machine.cpp:479-500, 518-530, 541-551,
-// 569-580, 618-646) and are written over the parent's packed words.  Every
-// other transition goes through the generic unpacked apply() (machine.cuh).
+// 569-580, 618-646) and are written over the parent's packed words.  `tr` is in
+// the ordinal form of bfs_rules.cuh.  Every other transition goes through the
+// generic unpacked apply() (machine.cuh).
 __device__ __forceinline__ bool fast_successor(const BfsDesc& d, const MState& s,
-                                               const Transition& tr, uint32_t* row) {
+                                               const Transition& tr, uint32_t* row,
+                                               const uint64_t* hk, uint64_t& H) {
     const Layout& l = d.l;
     const MachDesc& m = d.m;
-    int role, ord;
     switch (tr.op) {
         case OP_PEXREPORT: {
-            role_of(m, tr.actor, role, ord);
-            set_bits(row, l.off_pex + ord * l.pex_bits + l.poff_reported, 1, 1u);
-            set_bits(row, l.off_nrp, l.nrp, (uint32_t)(s.nrp_work + 1));
+            const int off = l.off_pex + tr.actor * l.pex_bits + l.poff_reported;
+            const int i = div31(off);
+            const uint32_t bit = 1u << (off - i * kWordBits);  // reported was 0
+            row[i] |= bit;
+            H += (uint64_t)bit * hk[i];
+            set_bits_h(row, l.off_nrp, l.nrp, (uint32_t)(s.nrp_work + 1), hk, H);
             return true;
         }
         case OP_PEXARRIVE: {
-            role_of(m, tr.actor, role, ord);
-            const int g = ord / m.nwe;
-            const int pc = s.pex[ord].pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
-            set_bits(row, l.off_pex + ord * l.pex_bits, 4, (uint32_t)pc);
-            set_bits(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount,
-                     (uint32_t)(s.bar[g].count + 1));
+            const int p = tr.actor, g = tr.peer;
+            const int pc = s.pex[p].pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
+            set_bits_h(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)pc, hk, H);
+            set_bits_h(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount,
+                       (uint32_t)(s.bar[g].count + 1), hk, H);
             return true;
         }
         case OP_UNITPEXGO: {
-            role_of(m, tr.actor, role, ord);
-            int prole, p;
-            role_of(m, tr.peer, prole, p);
-            UnitS un = s.unit[ord];
-            PexS px = pex_init(un.nwg, un.sent / m.nwe);
+            const int g = tr.actor, p = tr.peer;
+            UnitS un = s.unit[g];
+            PexS px = pex_init(un.nwg, tr.arg);  // arg = sent / nwe
             place_pex(m, px);
             un.sent += 1;
             if (un.pc == U_ACTIVATEPEX) {
@@ -220,47 +250,51 @@ __device__ __forceinline__ bool fast_successor(const BfsDesc& d, const MState& s
             } else {
                 un.pc = U_SERVE;
             }
-            write_pex(row, l, p, px);
-            write_unit(row, l, ord, un);
+            write_pex(row, l, p, px, hk, H);
+            write_unit(row, l, g, un, hk, H);
             return true;
         }
         case OP_UNITPEXSTOP: {
-            role_of(m, tr.actor, role, ord);
-            int prole, p;
-            role_of(m, tr.peer, prole, p);
-            UnitS un = s.unit[ord];
+            const int g = tr.actor, p = tr.peer;
+            UnitS un = s.unit[g];
             if (++un.k == m.nwe) un.pc = U_STOPBARRIER;
-            set_bits(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)P_EXITED);
-            write_unit(row, l, ord, un);
+            set_bits_h(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)P_EXITED, hk, H);
+            write_unit(row, l, g, un, hk, H);
             return true;
         }
         case OP_PEXITEMDONE: {
-            role_of(m, tr.actor, role, ord);
-            const int g = ord / m.nwe;
+            const int p = tr.actor, g = tr.peer;
             UnitS un = s.unit[g];
             un.got_items += 1;
             if (un.sent < m.wg) un.pc = U_REACTPEX;
             else if (m.kernel == 0 && un.got_items == m.wg) un.pc = U_SENDUNITDONE;
-            write_pex(row, l, ord, pex_init(0, 0));
-            write_unit(row, l, g, un);
+            write_pex(row, l, p, pex_init(0, 0), hk, H);
+            write_unit(row, l, g, un, hk, H);
             return true;
         }
         case OP_PEXENDDONE: {
-            role_of(m, tr.actor, role, ord);
-            const int g = ord / m.nwe;
+            const int p = tr.actor, g = tr.peer;
             UnitS un = s.unit[g];
             un.got_ends += 1;
             if (un.got_ends == m.nwe) un.pc = U_SENDUNITDONE;
-            if (ord % m.nwe == 0)
-                set_bits(row, l.off_nrp + l.nrp, l.allnwe, (uint32_t)(s.all_nwe - 1));
-            write_pex(row, l, ord, pex_init(0, 0));
-            write_unit(row, l, g, un);
+            if ((p & (m.nwe - 1)) == 0)
+                set_bits_h(row, l.off_nrp + l.nrp, l.allnwe, (uint32_t)(s.all_nwe - 1), hk, H);
+            write_pex(row, l, p, pex_init(0, 0), hk, H);
+            write_unit(row, l, g, un, hk, H);
             return true;
         }
         default: return false;
     }
 }
 
+// 64-bit warp sum (every lane gets it)
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int SW>
 __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     // per warp in shared memory: the parent (unpacked and packed) and its enabled
@@ -268,10 +302,14 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     // materialise an unpacked successor in (L1-resident) local memory.
     __shared__ MState parent[kBfsThreads / 32];
     __shared__ Transition enabled_s[kBfsThreads / 32][kMaxEnabled];
+    __shared__ uint64_t hk[32];  // hash coefficients K_i
     extern __shared__ uint32_t dyn[];
-    uint32_t* pwords = dyn + wib * (34 * a.words);  // parent words
-    uint32_t* kwords = pwords + a.words;             // the successor the warp keeps
-    uint32_t* row = pwords + (2 + lane) * a.words;   // this lane's successor
+    if (threadIdx.x < 32) hk[threadIdx.x] = hash_coef(threadIdx.x);
+    __syncthreads();
+    // rows are SW words apart (16-byte aligned); words [words, SW-2) are guard padding
+    uint32_t* pwords = dyn + wib * (34 * SW);  // parent words
+    uint32_t* kwords = pwords + SW;            // the successor the warp keeps
+    uint32_t* row = pwords + (2 + lane) * SW;  // this lane's successor
     MState& s = parent[wib];
     Transition* en = enabled_s[wib];
     MState t;
@@ -286,15 +324,13 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         n_states = n_trans = 0;
     };
     bool local = false;  // the warp continues with a successor it discovered itself
+    uint64_t H = 0;      // hash of the parent (known for a kept successor)
     // queue entries are claimed in runs: a warp that finds its entries already
     // filled doubles its next claim (up to 8), one that has to wait claims one
     unsigned long long h_next = 0, h_end = 0;
     unsigned claim = 1;
     for (;;) {
-        const uint32_t* src;
-        if (local) {
-            src = pwords;  // already holds the kept successor
-        } else {
+        if (!local) {
             if (h_next == h_end) {
                 unsigned long long h0 = 0;
                 if (lane == 0) h0 = atomicAdd(a.head, (unsigned long long)claim);
@@ -310,16 +346,17 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                 unsigned ns = 64;
                 for (unsigned it = 0;; ++it) {
                     slot = ld_relaxed32(&a.queue[h]);  // relaxed poll: no L1 invalidation
-                    if (slot != kEmpty) {
-                        slot = ld_acquire32(&a.queue[h]);
-                        break;
-                    }
+                    if (slot != kEmpty) break;
                     waited = true;
                     // the shared counters are read rarely: they are the working warps'
                     // atomics' cache line
                     if ((it & 15) == 15 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
                                             ld_relaxed32((const uint32_t*)a.error)))
                         break;
+                    if (it > (1u << 23)) {  // watchdog: outstanding states never arrive
+                        atomicExch(a.error, 7);
+                        break;
+                    }
                     __nanosleep(ns);
                     if (ns < 1024) ns <<= 1;
                 }
@@ -328,35 +365,50 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             waited = __shfl_sync(0xffffffffu, waited, 0);
             claim = waited ? 1u : (claim < 8u ? claim * 2u : 8u);
             if (slot == kEmpty) break;
-            // the key is published before its slot index is pushed
-            src = a.keys + (uint64_t)slot * a.words;
-            for (int k = lane; k < a.words; k += 32) pwords[k] = src[k];
+            // one coalesced line read; a word without its guard bit is still being
+            // written by the slot's claimer: read again
+            const uint32_t* src = a.table + (uint64_t)slot * SW;
+            uint32_t w;
+            for (unsigned spins = 0;; ++spins) {
+                w = lane < SW - 2 ? ld_relaxed32(src + lane) : kGuard;
+                if (__all_sync(0xffffffffu, w & kGuard)) break;
+                if (spins > (1u << 22)) {  // watchdog: a pushed key that never completes
+                    if (lane == 0) atomicExch(a.error, 6);
+                    break;
+                }
+                __nanosleep(64);
+            }
+            if (lane < SW - 2) pwords[lane] = w;
+            H = warp_sum64(lane < a.words ? (uint64_t)w * hk[lane] : 0ull);
             __syncwarp();
-            src = pwords;
         }
-        const int cfg = peek_cfg(src, a.cfg_bits);
+        const int cfg = peek_cfg(pwords, a.cfg_bits);
         if (cfg != cur_cfg) {
             flush();
             cur_cfg = cfg;
         }
         const BfsDesc& d = a.descs[cfg];
-        // warp-parallel unpack and enumeration: lane i reads the records of process
-        // slots i, i+32, ... and applies their rules (machine.cuh); a warp prefix sum
-        // places every lane's transitions in the shared enabled list
-        unpack_lanes(d, src, s, lane);
+        const int lognwe = __ffs(d.m.nwe) - 1;
+        // table-driven warp-parallel unpack, then one pass of the per-process rules
+        // (bfs_rules.cuh) with a warp prefix sum placing every lane's transitions
+        unpack_fields(a.ftab + (size_t)cfg * kMaxFields, a.nfields[cfg], pwords, s, lane);
         __syncwarp();
         const int nsl = n_slots(d.m);
-        int cnt = 0;
-        for (int k = lane; k < nsl; k += 32) cnt = slot_rules(d.m, s, k, nullptr, cnt);
-        int incl = cnt;
+        int ne = 0;
+        for (int k0 = 0; k0 < nsl; k0 += 32) {
+            Transition mine[2];
+            const int cnt = k0 + lane < nsl ? bfs_slot_rules(d.m, s, k0 + lane, lognwe, mine) : 0;
+            int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int pos = ne + incl - cnt;
+            if (cnt > 0) en[pos] = mine[0];
+            if (cnt > 1) en[pos + 1] = mine[1];
+            ne += __shfl_sync(0xffffffffu, incl, 31);
         }
-        const int ne = __shfl_sync(0xffffffffu, incl, 31);
-        int pos = incl - cnt;
-        for (int k = lane; k < nsl; k += 32) pos = slot_rules(d.m, s, k, en, pos);
         __syncwarp();
         BfsStats& st = a.stats[cfg];
         if (a.check_inv && lane == 0) {
@@ -367,6 +419,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             if (bad) atomicAdd(&st.violations, 1ull);
         }
         bool kept = false;
+        uint64_t H_kept = 0;
         if (ne == 0) {
             if (lane == 0) {
                 if (is_terminal(d.m, s)) {
@@ -386,18 +439,24 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
                 long long ins = -1;
+                uint64_t Hc = H;
                 if (e < ne) {
-                    for (int k = 0; k < a.words; ++k) row[k] = pwords[k];
+                    copy_key<SW>(row, pwords);
                     bool ok = true;
-                    if (!fast_successor(d, s, en[e], row)) {
+                    if (!fast_successor(d, s, en[e], row, hk, Hc)) {
                         if (a.op_hist) atomicAdd(&a.op_hist[en[e].op], 1ull);
                         copy_state(d.m, t, s);
-                        ok = apply(d.m, t, en[e]);
-                        if (ok) pack(d, cfg, t, row);
-                        else atomicExch(a.error, 3);
+                        ok = apply(d.m, t, to_pid(d.m, en[e]));
+                        if (ok) {
+                            pack(d, cfg, t, row);
+                            Hc = 0;
+                            for (int k = 0; k < a.words; ++k) Hc += (uint64_t)row[k] * hk[k];
+                        } else {
+                            atomicExch(a.error, 3);
+                        }
                     }
                     if (ok) {
-                        ins = table_insert(a, row, hash_words(row, a.words));
+                        ins = table_insert<SW>(a, row, fmix64(Hc));
                         if (ins == -2) atomicExch(a.error, 1);
                     }
                 }
@@ -412,13 +471,14 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                         if (lane == keeper) fresh = false;
                         kept = true;
                         n_states += 1;
+                        H_kept = __shfl_sync(0xffffffffu, Hc, keeper);
                     }
                 }
                 n_states += push_fresh(a, fresh, ins);
                 if (keeper >= 0) {
                     __syncwarp();
-                    const uint32_t* kr = pwords + (2 + keeper) * a.words;
-                    for (int k = lane; k < a.words; k += 32) kwords[k] = kr[k];
+                    const uint32_t* kr = pwords + (2 + keeper) * SW;
+                    if (lane < SW - 2) kwords[lane] = kr[lane];
                     __syncwarp();
                 }
             }
@@ -426,7 +486,8 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         __syncwarp();
         local = kept && !*(volatile int*)a.error;
         if (local) {
-            for (int k = lane; k < a.words; k += 32) pwords[k] = kwords[k];
+            if (lane < SW - 2) pwords[lane] = kwords[lane];
+            H = H_kept;
             __syncwarp();
         } else if (lane == 0) {
             atomicAdd(a.tq, ~0ull);  // this state is expanded: outstanding - 1
@@ -435,11 +496,13 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     flush();
 }
 
+template <int SW>
 __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
     // one initial state per configuration (explore.cpp:98-105), or the given
     // packed states of configuration 0 (a multi-source exploration)
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t key[kMaxWords];
+    uint32_t key[SW];
+    for (int k = 0; k < SW; ++k) key[k] = kGuard;
     int cfg = c;
     if (seeds) {
         if (c >= n_seeds) return;
@@ -451,9 +514,8 @@ __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
         MState s;
         initial_state(d.m, s);
         pack(d, c, s, key);
-        for (int k = d.l.words; k < a.words; ++k) key[k] = 0;
     }
-    const long long ins = table_insert(a, key, hash_words(key, a.words));
+    const long long ins = table_insert<SW>(a, key, fmix64(hash_full(key, a.words)));
     if (ins == -1) return;  // a repeated seed
     if (ins < 0) {
         atomicExch(a.error, 1);
@@ -462,7 +524,8 @@ __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
     const int c_ = cfg;
     atomicAdd(&a.stats[c_].states, 1ull);
     const unsigned long long pos = atomicAdd(a.tq, (1ull << 32) | 1ull) >> 32;
-    st_release32(&a.queue[pos], (uint32_t)ins);
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&a.queue[pos]), "r"((uint32_t)ins)
+                 : "memory");
 }
 
 }  // namespace
@@ -497,14 +560,23 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         }
         words = std::max(words, descs[c].l.words);
     }
+    // field tables of the table-driven unpack
+    std::vector<uint32_t> ftab((size_t)n_cfg * kMaxFields);
+    std::vector<int> nfields(n_cfg);
+    for (int c = 0; c < n_cfg; ++c)
+        nfields[c] = build_field_table(descs[c].m, descs[c].l, ftab.data() + (size_t)c * kMaxFields);
+    // slot stride: key words + guard padding + 8-byte tag in one 64- or 128-byte line
+    const int sw = words <= 14 ? 16 : 32;
+    void (*kern)(BfsArgs) = sw == 16 ? explore_kernel<16> : explore_kernel<32>;
+    void (*seed)(BfsArgs, const uint32_t*, int) = sw == 16 ? seed_kernel<16> : seed_kernel<32>;
     int dev = 0, sms = 0, per_sm = 0;
     MCTB_CUDA(cudaGetDevice(&dev));
     MCTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t dyn_smem = (size_t)(kBfsThreads / 32) * 34 * words * sizeof(uint32_t);
-    if (dyn_smem > 48 * 1024)
-        MCTB_CUDA(cudaFuncSetAttribute(explore_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)dyn_smem));
-    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, explore_kernel, kBfsThreads,
+    const size_t dyn_smem = (size_t)(kBfsThreads / 32) * 34 * sw * sizeof(uint32_t);
+    // static (parent states, enabled lists) + dynamic (rows) may exceed the 48 KB default
+    MCTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)dyn_smem));
+    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBfsThreads,
                                                             dyn_smem));
     if (per_sm < 1) per_sm = 1;
     // local-memory working set: keep the resident warps' successor states L1-sized
@@ -512,7 +584,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     else per_sm = std::min(per_sm, 4);
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const double slot_bytes = 8 + 4.0 * words + 2.0;  // tag + key + queue (half the slots)
+    const double slot_bytes = 4.0 * sw + 2.0;  // slot line + queue (half the slots)
     // capacity grows 8x on overflow; the sweep restarts (all counts are rebuilt)
     // first capacity: enough for the bound up to 2^28 slots (a restart loses the
     // work done, so large sweeps start large); then 8x per overflow
@@ -535,22 +607,28 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
         a.check_inv = check_invariants ? 1 : 0;
-        const size_t sz_tags = cap * 8, sz_keys = cap * 4 * (size_t)words, sz_q = qcap * 4;
-        const size_t sz_misc = 512 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg;
+        const size_t sz_table = cap * 4 * (size_t)sw, sz_q = qcap * 4;
+        const size_t sz_ftab = ftab.size() * 4 + nfields.size() * 4;
+        const size_t sz_misc = 512 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg + sz_ftab;
         void* blob = nullptr;
-        MCTB_CUDA(cudaMallocAsync(&blob, sz_tags + sz_keys + sz_q + sz_misc, st));
+        MCTB_CUDA(cudaMallocAsync(&blob, sz_table + sz_q + sz_misc, st));
         char* b = (char*)blob;
-        a.tags = (unsigned long long*)b;
-        a.keys = (uint32_t*)(b + sz_tags);
-        a.queue = (uint32_t*)(b + sz_tags + sz_keys);
-        char* misc = b + sz_tags + sz_keys + sz_q;
+        a.table = (uint32_t*)b;
+        a.queue = (uint32_t*)(b + sz_table);
+        char* misc = b + sz_table + sz_q;
         a.head = (unsigned long long*)misc;
         a.tq = (unsigned long long*)(misc + 8);
         a.error = (int*)(misc + 24);
         a.op_hist = getenv("MCTB_BFS_OPHIST") ? (unsigned long long*)(misc + 32) : nullptr;
         a.stats = (BfsStats*)(misc + 512);
         a.descs = (BfsDesc*)(misc + 512 + sizeof(BfsStats) * n_cfg);
-        MCTB_CUDA(cudaMemsetAsync(a.tags, 0, sz_tags, st));
+        uint32_t* d_ftab = (uint32_t*)(misc + 512 + (sizeof(BfsStats) + sizeof(BfsDesc)) * n_cfg);
+        a.ftab = d_ftab;
+        a.nfields = (const int*)(d_ftab + ftab.size());
+        MCTB_CUDA(cudaMemcpyAsync(d_ftab, ftab.data(), ftab.size() * 4, cudaMemcpyHostToDevice, st));
+        MCTB_CUDA(cudaMemcpyAsync(d_ftab + ftab.size(), nfields.data(), nfields.size() * 4,
+                                  cudaMemcpyHostToDevice, st));
+        MCTB_CUDA(cudaMemsetAsync(a.table, 0, sz_table, st));
         MCTB_CUDA(cudaMemsetAsync(a.queue, 0xff, sz_q, st));
         MCTB_CUDA(cudaMemsetAsync(misc, 0, 512, st));
         std::vector<BfsStats> init(n_cfg);
@@ -568,14 +646,18 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
                                       cudaMemcpyHostToDevice, st));
         }
         const int n_first = seeds ? n_seeds : n_cfg;
-        seed_kernel<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds);
+        seed<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds);
         if (d_seeds) cudaFreeAsync(d_seeds, st);
         MCTB_CUDA(cudaGetLastError());
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
-        explore_kernel<<<sms * per_sm, kBfsThreads, dyn_smem, st>>>(a);
+        const bool trace = getenv("MCTB_BFS_TRACE") != nullptr;
+        if (trace)
+            fprintf(stderr, "[bfs] launch cfgs=%d words=%d sw=%d cap=%llu grid=%d smem=%zu\n", n_cfg,
+                    words, sw, (unsigned long long)cap, sms * per_sm, dyn_smem);
+        kern<<<sms * per_sm, kBfsThreads, dyn_smem, st>>>(a);
         cudaEventRecord(e1, st);
         MCTB_CUDA(cudaGetLastError());
         res->stats.resize(n_cfg);
@@ -594,6 +676,21 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         for (const auto& x : res->stats) res->states += x.states;
         res->levels = 0;
         res->error = (int)(misc_h[3] & 0xffffffff);
+        if (trace)
+            fprintf(stderr, "[bfs] done %.3f ms error=%d head=%llu tail=%llu outstanding=%llu\n", ms,
+                    res->error, misc_h[0], misc_h[1] >> 32, misc_h[1] & 0xffffffffull);
+        if (res->error >= 5) {
+            // a watchdog fired (bfs.cu spin loops): report instead of hanging
+            char msg[256];
+            snprintf(msg, sizeof msg,
+                     "exploration stalled (watchdog %d: head %llu, tail %llu, outstanding %llu)",
+                     res->error, misc_h[0], misc_h[1] >> 32, misc_h[1] & 0xffffffffull);
+            fprintf(stderr, "[mctb] %s\n", msg);
+            set_error(msg);
+            cudaFreeAsync(d_ids, st);
+            cudaStreamSynchronize(st);
+            return MCTB_MODEL_BUG;
+        }
         // explore.cpp:28-31: a visited set holding max_states refuses every later
         // insert, so reaching the cap ends the exhaustive claim (statistics are
         // flushed per warp, so the final count decides)

@@ -1,0 +1,302 @@
+// Exploration-side views of the transition system (bfs.cu): a table-driven
+// warp-parallel unpack, a per-process enumeration of the enabled set in which
+// every lane emits at most two transitions, and the linear state hash that
+// in-place successors update word by word.
+//
+// The enumeration yields exactly the set of Machine::enabled
+// (machine.cpp:174-336, machine.cuh host/clock/device/unit/barrier/pex_rules)
+// but in a different order: a handshake is emitted by the process it is
+// offered TO (host -> device, device -> unit, unit -> element), so no lane loops
+// over its peers.  The exploration's counts do not depend on the order
+// (states, transitions, terminal times are set properties); the paths that do
+// (first DFS path, lexfirst walk, trajectories) keep using enabled().
+//
+// Transitions in the exploration's enabled list name processes by ORDINAL
+// within their role (to_pid() gives the pid form that apply() takes):
+//   clock ops (0, -)        host ops (0, device d)     DEVICEDONE (d, 0)
+//   DEVICEUNIT* (d, unit g) UNITDONE (g, d)            UNITBARRIERSTOP (g, g)
+//   BARRIERRELEASE (g, -)   UNITPEX* (g, element p)    PEXREPORT/EFFECT (p, -)
+//   PEXARRIVE (p, g)        PEXITEMDONE/ENDDONE (p, g)
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "machine.cuh"
+#include "pack.cuh"
+
+namespace mctb {
+
+// one entry per packed field: word i (5 bits) | shift (5) | width (6) |
+// byte offset in MState (13) | store size (2: 0 = 16-bit, 1 = 32-bit, 2 = 64-bit)
+constexpr int kMaxFields = 10 + 3 * kMaxDev + 8 * kMaxUnit + 7 * kMaxPex + kMaxLoc;
+
+__host__ __device__ inline uint32_t field_entry(int off, int width, size_t dst, int sz) {
+    const int i = off / kWordBits, sh = off % kWordBits;
+    return (uint32_t)i | ((uint32_t)sh << 5) | ((uint32_t)width << 10) | ((uint32_t)dst << 16) |
+           ((uint32_t)sz << 29);
+}
+
+// The field table of a layout, in pack() order (pack.cuh).  Returns the count.
+__host__ inline int build_field_table(const MachDesc& m, const Layout& l, uint32_t* out) {
+    int n = 0, off = l.cfg;
+    auto add = [&](int width, size_t dst, int sz) {
+        out[n++] = field_entry(off, width, dst, sz);
+        off += width;
+    };
+    add(l.time, offsetof(MState, time), 2);
+    add(l.nrp, offsetof(MState, nrp_work), 1);
+    add(l.allnwe, offsetof(MState, all_nwe), 1);
+    add(1, offsetof(MState, fin), 1);
+    add(l.nextwg, offsetof(MState, next_wg), 1);
+    add(3, offsetof(MState, host_pc), 1);
+    add(l.hostk, offsetof(MState, host_k), 1);
+    add(1, offsetof(MState, clock), 1);
+    add(l.glob0, offsetof(MState, glob0), 1);
+    for (int i = 0; i < m.nwd; ++i) {
+        const size_t b = offsetof(MState, dev) + i * sizeof(DevS);
+        add(3, b + offsetof(DevS, pc), 1);
+        add(l.dk, b + offsetof(DevS, k), 1);
+        add(l.bb, b + offsetof(DevS, batch_base), 1);
+    }
+    for (int g = 0; g < m.n_units; ++g) {
+        const size_t b = offsetof(MState, unit) + g * sizeof(UnitS);
+        const size_t bb = offsetof(MState, bar) + g * sizeof(BarS);
+        add(3, b + offsetof(UnitS, pc), 1);
+        add(l.uk, b + offsetof(UnitS, k), 1);
+        add(l.nwg, b + offsetof(UnitS, nwg), 1);
+        add(l.sent, b + offsetof(UnitS, sent), 1);
+        add(l.items, b + offsetof(UnitS, got_items), 1);
+        add(l.ends, b + offsetof(UnitS, got_ends), 1);
+        add(1, bb + offsetof(BarS, pc), 1);
+        add(l.bcount, bb + offsetof(BarS, count), 1);
+    }
+    for (int p = 0; p < m.n_pex; ++p) {
+        const size_t b = offsetof(MState, pex) + p * sizeof(PexS);
+        add(4, b + offsetof(PexS, pc), 0);
+        add(1, b + offsetof(PexS, phase), 0);
+        add(l.cursor, b + offsetof(PexS, cursor), 0);
+        add(l.busy, b + offsetof(PexS, busy_left), 0);
+        add(1, b + offsetof(PexS, reported), 0);
+        add(l.pnwg, b + offsetof(PexS, nwg), 1);
+        add(l.iter, b + offsetof(PexS, iter), 0);
+    }
+    if (m.kernel == 1)
+        for (int i = 0; i < m.n_units * m.np; ++i) add(l.loc, offsetof(MState, loc) + 4 * i, 1);
+    return n;
+}
+
+// Warp-parallel unpack: lane f extracts fields f, f+32, ... into the shared
+// MState (the caller syncs the warp).  `in` holds >= words+1 readable words.
+__device__ __forceinline__ void unpack_fields(const uint32_t* __restrict__ ftab, int nf,
+                                              const uint32_t* in, MState& s, int lane) {
+    char* base = reinterpret_cast<char*>(&s);
+    for (int f = lane; f < nf; f += 32) {
+        const uint32_t e = __ldg(ftab + f);
+        const int i = e & 31, sh = (e >> 5) & 31, w = (e >> 10) & 63;
+        const uint32_t dst = (e >> 16) & 0x1fff, sz = e >> 29;
+        const uint64_t x = (uint64_t)(in[i] & kData) | ((uint64_t)(in[i + 1] & kData) << kWordBits);
+        const uint32_t v = (uint32_t)(x >> sh) & (uint32_t)((1ull << w) - 1);
+        if (sz == 0) *reinterpret_cast<uint16_t*>(base + dst) = (uint16_t)v;
+        else if (sz == 1) *reinterpret_cast<uint32_t*>(base + dst) = v;
+        else *reinterpret_cast<int64_t*>(base + dst) = (int64_t)v;
+    }
+}
+
+// Process slot k (host, clock, devices, units, barriers, elements): its own
+// transitions plus the handshake offered to it.  Writes <= 2 to o.
+__device__ __forceinline__ int bfs_slot_rules(const MachDesc& m, const MState& s, int k,
+                                              int lognwe, Transition* o) {
+    int n = 0;
+    if (k == 0) {
+        if (s.host_pc == H_SETFIN) o[n++] = Transition{0, kNoPeer, OP_HOSTSETFIN, 0};
+        return n;
+    }
+    if (k == 1) {
+        if (s.clock == 0) {
+            if (s.fin) o[n++] = Transition{0, kNoPeer, OP_CLOCKHALT, 0};
+            if (s.all_nwe != 0 && s.nrp_work == s.all_nwe)
+                o[n++] = Transition{0, kNoPeer, OP_CLOCKTICK, 0};
+        }
+        return n;
+    }
+    k -= 2;
+    if (k < m.nwd) {
+        const int d = k;
+        const DevS& dv = s.dev[d];
+        // host_rules: offered by the host to every waiting device
+        if (dv.pc == D_WAITGO &&
+            (s.host_pc == H_SENDGO || s.host_pc == H_REACTGO || s.host_pc == H_SENDSTOP)) {
+            const int op = s.host_pc == H_SENDGO ? OP_HOSTGO
+                           : s.host_pc == H_REACTGO ? OP_HOSTREACTGO
+                                                    : OP_HOSTSTOP;
+            o[n++] = Transition{0, (uint16_t)d, op, s.host_k};
+        }
+        if (dv.pc == D_SENDDONE && (s.host_pc == H_WAITDONEREACT || s.host_pc == H_WAITDONESTOP))
+            o[n++] = Transition{(uint16_t)d, 0, OP_DEVICEDONE, 0};
+        return n;
+    }
+    k -= m.nwd;
+    if (k < m.n_units) {
+        const int g = k, d = g / m.nwu;
+        const UnitS& un = s.unit[g];
+        const DevS& dv = s.dev[d];
+        // device_rules: offered by the unit's device
+        if (un.pc == U_WAITGO && (dv.pc == D_SENDUNITGO || dv.pc == D_STOPUNITS)) {
+            const bool go = dv.pc == D_SENDUNITGO;
+            o[n++] = Transition{(uint16_t)d, (uint16_t)g, go ? OP_DEVICEUNITGO : OP_DEVICEUNITSTOP,
+                                go ? dv.batch_base + dv.k : 0};
+        }
+        if (un.pc == U_SENDUNITDONE) {
+            if (dv.pc == D_WAITUNITDONE)
+                o[n++] = Transition{(uint16_t)g, (uint16_t)d, OP_UNITDONE, un.nwg};
+        } else if (un.pc == U_STOPBARRIER) {
+            if (s.bar[g].pc == B_COUNTING && s.bar[g].count == 0)
+                o[n++] = Transition{(uint16_t)g, (uint16_t)g, OP_UNITBARRIERSTOP, 0};
+        }
+        return n;
+    }
+    k -= m.n_units;
+    if (k < m.n_units) {
+        const BarS& b = s.bar[k];
+        if (b.pc == B_COUNTING && b.count == m.nwe)
+            o[n++] = Transition{(uint16_t)k, kNoPeer, OP_BARRIERRELEASE, 0};
+        return n;
+    }
+    k -= m.n_units;
+    const int p = k, g = p >> lognwe;  // nwe = min(wg, np) is a power of two
+    const PexS& px = s.pex[p];
+    const UnitS& un = s.unit[g];
+    // unit_rules: offered by the element's unit
+    if (px.pc == P_WAITGO &&
+        (un.pc == U_ACTIVATEPEX || un.pc == U_REACTPEX || un.pc == U_STOPPEXES)) {
+        const bool stop = un.pc == U_STOPPEXES;
+        o[n++] = Transition{(uint16_t)g, (uint16_t)p, stop ? OP_UNITPEXSTOP : OP_UNITPEXGO,
+                            stop ? 0 : un.sent >> lognwe};
+    }
+    // pex_rules
+    switch (px.pc) {
+        case P_RUN: {
+            const Instr in = instr_at(m, px.phase, px.cursor);
+            if (in.kind == IK_BUSY) {
+                if (px.busy_left > 0 && !px.reported)
+                    o[n++] = Transition{(uint16_t)p, kNoPeer, OP_PEXREPORT, 0};
+            } else if (in.kind == IK_EFFECT) {
+                o[n++] = Transition{(uint16_t)p, kNoPeer, OP_PEXEFFECT, px.cursor};
+            }
+            break;
+        }
+        case P_ARRIVEBARRIER:
+        case P_ARRIVEGROUPEND:
+            if (s.bar[g].pc == B_COUNTING && s.bar[g].count < m.nwe)
+                o[n++] = Transition{(uint16_t)p, (uint16_t)g, OP_PEXARRIVE, 0};
+            break;
+        case P_SENDITEMDONE:
+            if (un.pc == U_SERVE) o[n++] = Transition{(uint16_t)p, (uint16_t)g, OP_PEXITEMDONE, px.iter};
+            break;
+        case P_SENDENDDONE:
+            if (un.pc == U_SERVE) o[n++] = Transition{(uint16_t)p, (uint16_t)g, OP_PEXENDDONE, 0};
+            break;
+        default: break;
+    }
+    return n;
+}
+
+// Ordinal form -> the pid form of machine.hpp:78-88 (what apply() takes).
+__host__ __device__ inline Transition to_pid(const MachDesc& m, const Transition& t) {
+    Transition r{0, kNoPeer, t.op, t.arg};
+    const int a = t.actor, p = t.peer;
+    switch (t.op) {
+        case OP_CLOCKTICK:
+        case OP_CLOCKHALT: r.actor = 2; break;
+        case OP_HOSTGO:
+        case OP_HOSTREACTGO:
+        case OP_HOSTSTOP:
+            r.actor = 1;
+            r.peer = (uint16_t)device_pid(m, p);
+            break;
+        case OP_HOSTSETFIN: r.actor = 1; break;
+        case OP_DEVICEDONE:
+            r.actor = (uint16_t)device_pid(m, a);
+            r.peer = 1;
+            break;
+        case OP_DEVICEUNITGO:
+        case OP_DEVICEUNITSTOP:
+            r.actor = (uint16_t)device_pid(m, a);
+            r.peer = (uint16_t)unit_pid(m, p);
+            break;
+        case OP_UNITDONE:
+            r.actor = (uint16_t)unit_pid(m, a);
+            r.peer = (uint16_t)device_pid(m, p);
+            break;
+        case OP_UNITBARRIERSTOP:
+            r.actor = (uint16_t)unit_pid(m, a);
+            r.peer = (uint16_t)barrier_pid(m, p);
+            break;
+        case OP_UNITPEXGO:
+        case OP_UNITPEXSTOP:
+            r.actor = (uint16_t)unit_pid(m, a);
+            r.peer = (uint16_t)pex_pid(m, p);
+            break;
+        case OP_BARRIERRELEASE: r.actor = (uint16_t)barrier_pid(m, a); break;
+        case OP_PEXREPORT:
+        case OP_PEXEFFECT: r.actor = (uint16_t)pex_pid(m, a); break;
+        case OP_PEXARRIVE:
+            r.actor = (uint16_t)pex_pid(m, a);
+            r.peer = (uint16_t)barrier_pid(m, p);
+            break;
+        case OP_PEXITEMDONE:
+        case OP_PEXENDDONE:
+            r.actor = (uint16_t)pex_pid(m, a);
+            r.peer = (uint16_t)unit_pid(m, p);
+            break;
+        default: break;
+    }
+    return r;
+}
+
+// ------------------------------------------------------------------ hashing
+// H(key) = sum_i w_i * K_i (mod 2^64) over the key words, K_i odd and random;
+// an in-place successor updates H by (new - old) * K_i for each word it
+// rewrites.  The table slot and fingerprint come from fmix64(H).  (Equal H for
+// different keys only costs a probe: the table compares full keys.)
+__host__ __device__ inline uint64_t fmix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xFF51AFD7ED558CCDull;
+    x ^= x >> 33;
+    x *= 0xC4CEB9FE1A85EC53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__host__ __device__ inline uint64_t hash_coef(int i) {
+    return fmix64(0x9E3779B97F4A7C15ull * (uint64_t)(i + 1)) | 1ull;
+}
+
+__host__ __device__ inline uint64_t hash_full(const uint32_t* w, int n) {
+    uint64_t h = 0;
+    for (int i = 0; i < n; ++i) h += (uint64_t)w[i] * hash_coef(i);
+    return h;
+}
+
+// set_bits (pack.cuh) that also updates the linear hash H (coefficients k).
+__device__ __forceinline__ void set_bits_h(uint32_t* w, int off, int width, uint32_t v,
+                                           const uint64_t* k, uint64_t& H) {
+    if (!width) return;
+    const int i = div31(off), sh = off - i * kWordBits;
+    const uint64_t mask = ((1ull << width) - 1) << sh;
+    const bool two = sh + width > kWordBits;
+    const uint32_t o0 = w[i], o1 = two ? w[i + 1] : 0u;
+    uint64_t cur = (uint64_t)(o0 & kData) | ((uint64_t)(o1 & kData) << kWordBits);
+    cur = (cur & ~mask) | (((uint64_t)v << sh) & mask);
+    const uint32_t n0 = ((uint32_t)cur & kData) | kGuard;
+    w[i] = n0;
+    H += ((uint64_t)n0 - (uint64_t)o0) * k[i];
+    if (two) {
+        const uint32_t n1 = ((uint32_t)(cur >> kWordBits) & kData) | kGuard;
+        w[i + 1] = n1;
+        H += ((uint64_t)n1 - (uint64_t)o1) * k[i + 1];
+    }
+}
+
+}  // namespace mctb

@@ -5,9 +5,14 @@
 // We key ours on an injective bit packing of the same fields: each field gets
 // the width of its reachable range for this configuration (computed on the
 // host from the launch plan), so a state of a desk-scale configuration fits in
-// a handful of 32-bit words and one hash-table probe moves one or two 32-byte
-// sectors.  Two states of one configuration are equal iff their packings are
-// equal, which is what makes the GPU state counts equal the reference's.
+// a handful of 32-bit words and one hash-table probe moves one 64-byte line.
+// Two states of one configuration are equal iff their packings are equal,
+// which is what makes the GPU state counts equal the reference's.
+//
+// Every packed word carries 31 data bits and a guard bit (bit 31) that is
+// always set.  The visited table starts zeroed, so a reader that races the
+// writer of a slot sees a word without its guard bit and reads again: the key
+// words need no release/acquire ordering against the slot's tag (bfs.cu).
 #pragma once
 
 #include <stdint.h>
@@ -17,6 +22,14 @@
 namespace mctb {
 
 constexpr int kMaxWords = 24;
+constexpr int kWordBits = 31;            // data bits per packed word
+constexpr uint32_t kGuard = 0x80000000u;  // set in every written key word
+constexpr uint32_t kData = 0x7fffffffu;
+
+// floor(x / 31) for 0 <= x < 1.5e8 (bit offsets), without a division
+__host__ __device__ inline int div31(int x) {
+    return (int)(((uint64_t)(uint32_t)x * 0x8421085ull) >> 32);
+}
 
 struct Layout {
     // widths in bits
@@ -89,7 +102,7 @@ __host__ inline Layout make_layout(const MachDesc& m, int n_cfg, int64_t max_tim
     l.dev_bits = 3 + l.dk + l.bb;
     l.off_dev = l.off_units - m.nwd * l.dev_bits;
     l.off_loc = l.off_pex + m.n_pex * l.pex_bits;
-    l.words = (bits + 31) / 32;
+    l.words = (bits + kWordBits - 1) / kWordBits;
     return l;
 }
 
@@ -102,15 +115,16 @@ struct BitWriter {
         if (!bits) return;
         acc |= (uint64_t)(v & (uint32_t)((1ull << bits) - 1)) << n;
         n += bits;
-        if (n >= 32) {
-            w[idx++] = (uint32_t)acc;
-            acc >>= 32;
-            n -= 32;
+        while (n >= kWordBits) {
+            w[idx++] = ((uint32_t)acc & kData) | kGuard;
+            acc >>= kWordBits;
+            n -= kWordBits;
         }
     }
+    // pads with guard-only words up to `words`
     __host__ __device__ inline void flush(int words) {
-        if (n > 0) w[idx++] = (uint32_t)acc;
-        while (idx < words) w[idx++] = 0;
+        if (n > 0) w[idx++] = ((uint32_t)acc & kData) | kGuard;
+        while (idx < words) w[idx++] = kGuard;
     }
 };
 
@@ -120,18 +134,19 @@ struct BitReader {
     int n = 0, idx = 0;
     __host__ __device__ explicit BitReader(const uint32_t* in) : w(in) {}
     // positioned at bit `off`
-    __host__ __device__ BitReader(const uint32_t* in, int off) : w(in), idx(off >> 5) {
-        const int sh = off & 31;
+    __host__ __device__ BitReader(const uint32_t* in, int off) : w(in) {
+        idx = div31(off);
+        const int sh = off - idx * kWordBits;
         if (sh) {
-            acc = (uint64_t)w[idx++] >> sh;
-            n = 32 - sh;
+            acc = (uint64_t)(w[idx++] & kData) >> sh;
+            n = kWordBits - sh;
         }
     }
     __host__ __device__ inline uint32_t get(int bits) {
         if (!bits) return 0;
-        if (n < bits) {
-            acc |= (uint64_t)w[idx++] << n;
-            n += 32;
+        while (n < bits) {
+            acc |= (uint64_t)(w[idx++] & kData) << n;
+            n += kWordBits;
         }
         const uint32_t v = (uint32_t)(acc & ((1ull << bits) - 1));
         acc >>= bits;
@@ -187,7 +202,7 @@ __host__ __device__ inline void pack(const BfsDesc& d, int cfg, const MState& s,
 
 // cfg id first (so a reader can select the layout), then the fields in pack order.
 __host__ __device__ inline int peek_cfg(const uint32_t* in, int cfg_bits) {
-    return cfg_bits ? (int)(in[0] & ((1u << cfg_bits) - 1)) : 0;
+    return cfg_bits ? (int)(in[0] & ((1u << cfg_bits) - 1)) : 0;  // cfg_bits < 31
 }
 
 __host__ __device__ inline void unpack(const BfsDesc& d, const uint32_t* in, MState& s) {
@@ -234,17 +249,17 @@ __host__ __device__ inline void unpack(const BfsDesc& d, const uint32_t* in, MSt
         for (int i = 0; i < m.n_units * m.np; ++i) s.loc[i] = (int32_t)r.get(l.loc);
 }
 
-// Overwrites `width` bits at bit offset `off` of a packed state (LSB-first, the
-// BitWriter order).
+// Overwrites `width` (<= 32) bits at data-bit offset `off` of a packed state
+// (the BitWriter order); a field spans at most two words.
 __host__ __device__ inline void set_bits(uint32_t* w, int off, int width, uint32_t v) {
     if (!width) return;
-    const int i = off >> 5, sh = off & 31;
+    const int i = div31(off), sh = off - i * kWordBits;
     const uint64_t mask = ((1ull << width) - 1) << sh;
-    const bool two = sh + width > 32;
-    uint64_t cur = (uint64_t)w[i] | (two ? (uint64_t)w[i + 1] << 32 : 0ull);
+    const bool two = sh + width > kWordBits;
+    uint64_t cur = (uint64_t)(w[i] & kData) | (two ? (uint64_t)(w[i + 1] & kData) << kWordBits : 0ull);
     cur = (cur & ~mask) | (((uint64_t)v << sh) & mask);
-    w[i] = (uint32_t)cur;
-    if (two) w[i + 1] = (uint32_t)(cur >> 32);
+    w[i] = ((uint32_t)cur & kData) | kGuard;
+    if (two) w[i + 1] = ((uint32_t)(cur >> kWordBits) & kData) | kGuard;
 }
 
 // Warp-parallel unpack (exploration): lane 0 reads the header, lane i the
