@@ -180,29 +180,50 @@ __device__ __forceinline__ unsigned push_fresh(const BfsArgs& a, bool fresh, lon
     return cnt;
 }
 
-// Record writers for the in-place successors (field order of pack()); every
-// rewritten word also updates the state hash H.
+// Record writers for the in-place successors (field order of pack()): the
+// record is composed in a register and written with one multi-word set (every
+// rewritten word also updates the state hash H); records wider than 62 bits
+// are written field by field.
 __device__ __forceinline__ void write_pex(uint32_t* row, const Layout& l, int p, const PexS& x,
                                           const uint64_t* hk, uint64_t& H) {
     const int o = l.off_pex + p * l.pex_bits;
+    const int s1 = 5 + l.cursor, s2 = s1 + l.busy, s3 = s2 + 1, s4 = s3 + l.pnwg;
+    if (l.pex_bits <= 62) {
+        const uint64_t v = (uint64_t)x.pc | ((uint64_t)x.phase << 4) | ((uint64_t)x.cursor << 5) |
+                           ((uint64_t)x.busy_left << s1) | ((uint64_t)x.reported << s2) |
+                           ((uint64_t)(uint32_t)x.nwg << s3) | ((uint64_t)x.iter << s4);
+        set_bits_h(row, o, l.pex_bits, v, hk, H);
+        return;
+    }
     set_bits_h(row, o, 4, (uint32_t)x.pc, hk, H);
     set_bits_h(row, o + 4, 1, (uint32_t)x.phase, hk, H);
     set_bits_h(row, o + 5, l.cursor, x.cursor, hk, H);
-    set_bits_h(row, o + 5 + l.cursor, l.busy, x.busy_left, hk, H);
-    set_bits_h(row, o + 5 + l.cursor + l.busy, 1, (uint32_t)x.reported, hk, H);
-    set_bits_h(row, o + 6 + l.cursor + l.busy, l.pnwg, (uint32_t)x.nwg, hk, H);
-    set_bits_h(row, o + 6 + l.cursor + l.busy + l.pnwg, l.iter, x.iter, hk, H);
+    set_bits_h(row, o + s1, l.busy, x.busy_left, hk, H);
+    set_bits_h(row, o + s2, 1, (uint32_t)x.reported, hk, H);
+    set_bits_h(row, o + s3, l.pnwg, (uint32_t)x.nwg, hk, H);
+    set_bits_h(row, o + s4, l.iter, x.iter, hk, H);
 }
 
+// The unit's own fields (not its barrier's, which follow them in the record).
 __device__ __forceinline__ void write_unit(uint32_t* row, const Layout& l, int g, const UnitS& u,
                                            const uint64_t* hk, uint64_t& H) {
     const int o = l.off_units + g * l.unit_bits;
+    const int s1 = 3 + l.uk, s2 = s1 + l.nwg, s3 = s2 + l.sent, s4 = s3 + l.items;
+    const int width = s4 + l.ends;
+    if (width <= 62) {
+        const uint64_t v = (uint64_t)(uint32_t)u.pc | ((uint64_t)(uint32_t)u.k << 3) |
+                           ((uint64_t)(uint32_t)u.nwg << s1) | ((uint64_t)(uint32_t)u.sent << s2) |
+                           ((uint64_t)(uint32_t)u.got_items << s3) |
+                           ((uint64_t)(uint32_t)u.got_ends << s4);
+        set_bits_h(row, o, width, v, hk, H);
+        return;
+    }
     set_bits_h(row, o, 3, (uint32_t)u.pc, hk, H);
     set_bits_h(row, o + 3, l.uk, (uint32_t)u.k, hk, H);
-    set_bits_h(row, o + 3 + l.uk, l.nwg, (uint32_t)u.nwg, hk, H);
-    set_bits_h(row, o + 3 + l.uk + l.nwg, l.sent, (uint32_t)u.sent, hk, H);
-    set_bits_h(row, o + 3 + l.uk + l.nwg + l.sent, l.items, (uint32_t)u.got_items, hk, H);
-    set_bits_h(row, o + 3 + l.uk + l.nwg + l.sent + l.items, l.ends, (uint32_t)u.got_ends, hk, H);
+    set_bits_h(row, o + s1, l.nwg, (uint32_t)u.nwg, hk, H);
+    set_bits_h(row, o + s2, l.sent, (uint32_t)u.sent, hk, H);
+    set_bits_h(row, o + s3, l.items, (uint32_t)u.got_items, hk, H);
+    set_bits_h(row, o + s4, l.ends, (uint32_t)u.got_ends, hk, H);
 }
 
 // In-place successors for the transitions behind the combinatorial state
@@ -305,6 +326,8 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
     __shared__ uint64_t hk[32];  // hash coefficients K_i
     extern __shared__ uint32_t dyn[];
     if (threadIdx.x < 32) hk[threadIdx.x] = hash_coef(threadIdx.x);
+    // unpack_fields writes the time's low word only
+    if ((threadIdx.x & 31) == 0) parent[threadIdx.x >> 5].time = 0;
     __syncthreads();
     // rows are SW words apart (16-byte aligned); words [words, SW-2) are guard padding
     uint32_t* pwords = dyn + wib * (34 * SW);  // parent words

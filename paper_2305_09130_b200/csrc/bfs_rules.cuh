@@ -28,7 +28,7 @@
 namespace mctb {
 
 // one entry per packed field: word i (5 bits) | shift (5) | width (6) |
-// byte offset in MState (13) | store size (2: 0 = 16-bit, 1 = 32-bit, 2 = 64-bit)
+// byte offset in MState (13) | store size (2: 0 = 16-bit, 1 = 32-bit)
 constexpr int kMaxFields = 10 + 3 * kMaxDev + 8 * kMaxUnit + 7 * kMaxPex + kMaxLoc;
 
 __host__ __device__ inline uint32_t field_entry(int off, int width, size_t dst, int sz) {
@@ -44,7 +44,7 @@ __host__ inline int build_field_table(const MachDesc& m, const Layout& l, uint32
         out[n++] = field_entry(off, width, dst, sz);
         off += width;
     };
-    add(l.time, offsetof(MState, time), 2);
+    add(l.time, offsetof(MState, time), 1);  // low word; l.time <= 32 (run_bfs)
     add(l.nrp, offsetof(MState, nrp_work), 1);
     add(l.allnwe, offsetof(MState, all_nwe), 1);
     add(1, offsetof(MState, fin), 1);
@@ -88,6 +88,8 @@ __host__ inline int build_field_table(const MachDesc& m, const Layout& l, uint32
 
 // Warp-parallel unpack: lane f extracts fields f, f+32, ... into the shared
 // MState (the caller syncs the warp).  `in` holds >= words+1 readable words.
+// The time field is written as the low word of MState::time: the caller keeps
+// the high word zero.
 __device__ __forceinline__ void unpack_fields(const uint32_t* __restrict__ ftab, int nf,
                                               const uint32_t* in, MState& s, int lane) {
     char* base = reinterpret_cast<char*>(&s);
@@ -98,8 +100,7 @@ __device__ __forceinline__ void unpack_fields(const uint32_t* __restrict__ ftab,
         const uint64_t x = (uint64_t)(in[i] & kData) | ((uint64_t)(in[i + 1] & kData) << kWordBits);
         const uint32_t v = (uint32_t)(x >> sh) & (uint32_t)((1ull << w) - 1);
         if (sz == 0) *reinterpret_cast<uint16_t*>(base + dst) = (uint16_t)v;
-        else if (sz == 1) *reinterpret_cast<uint32_t*>(base + dst) = v;
-        else *reinterpret_cast<int64_t*>(base + dst) = (int64_t)v;
+        else *reinterpret_cast<uint32_t*>(base + dst) = v;
     }
 }
 
@@ -138,7 +139,7 @@ __device__ __forceinline__ int bfs_slot_rules(const MachDesc& m, const MState& s
     }
     k -= m.nwd;
     if (k < m.n_units) {
-        const int g = k, d = g / m.nwu;
+        const int g = k, d = m.nwd == 1 ? 0 : g / m.nwu;
         const UnitS& un = s.unit[g];
         const DevS& dv = s.dev[d];
         // device_rules: offered by the unit's device
@@ -279,23 +280,22 @@ __host__ __device__ inline uint64_t hash_full(const uint32_t* w, int n) {
     return h;
 }
 
-// set_bits (pack.cuh) that also updates the linear hash H (coefficients k).
-__device__ __forceinline__ void set_bits_h(uint32_t* w, int off, int width, uint32_t v,
+// set_bits (pack.cuh) of a field up to 62 bits wide (at most three words) that
+// also updates the linear hash H (coefficients k).
+__device__ __forceinline__ void set_bits_h(uint32_t* w, int off, int width, uint64_t v,
                                            const uint64_t* k, uint64_t& H) {
-    if (!width) return;
-    const int i = div31(off), sh = off - i * kWordBits;
-    const uint64_t mask = ((1ull << width) - 1) << sh;
-    const bool two = sh + width > kWordBits;
-    const uint32_t o0 = w[i], o1 = two ? w[i + 1] : 0u;
-    uint64_t cur = (uint64_t)(o0 & kData) | ((uint64_t)(o1 & kData) << kWordBits);
-    cur = (cur & ~mask) | (((uint64_t)v << sh) & mask);
-    const uint32_t n0 = ((uint32_t)cur & kData) | kGuard;
-    w[i] = n0;
-    H += ((uint64_t)n0 - (uint64_t)o0) * k[i];
-    if (two) {
-        const uint32_t n1 = ((uint32_t)(cur >> kWordBits) & kData) | kGuard;
-        w[i + 1] = n1;
-        H += ((uint64_t)n1 - (uint64_t)o1) * k[i + 1];
+    int i = div31(off), b = off - i * kWordBits;
+    while (width > 0) {
+        const int take = min(kWordBits - b, width);
+        const uint32_t mask = ((1u << take) - 1u) << b;
+        const uint32_t o = w[i];
+        const uint32_t n = (o & ~mask) | (((uint32_t)v << b) & mask);
+        w[i] = n;
+        H += ((uint64_t)n - (uint64_t)o) * k[i];
+        v >>= take;
+        width -= take;
+        b = 0;
+        ++i;
     }
 }
 
