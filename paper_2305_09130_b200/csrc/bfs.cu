@@ -347,6 +347,12 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         n_states = n_trans = 0;
     };
     bool local = false;  // the warp continues with a successor it discovered itself
+    // the configuration's global state count and the error flag, re-read every
+    // 64 expansions (not on every state's critical path): the visited cap and an
+    // error stop the sweep a few states late, which only bounds extra work
+    unsigned long long g_states = 0;
+    int g_err = 0;
+    unsigned since = 0;
     uint64_t H = 0;      // hash of the parent (known for a kept successor)
     // queue entries are claimed in runs: a warp that finds its entries already
     // filled doubles its next claim (up to 8), one that has to wait claims one
@@ -409,6 +415,11 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
         if (cfg != cur_cfg) {
             flush();
             cur_cfg = cfg;
+            since = 0;
+        }
+        if ((since++ & 63) == 0) {
+            g_states = ld_relaxed64(&a.stats[cfg].states);
+            g_err = (int)ld_relaxed32((const uint32_t*)a.error);
         }
         const BfsDesc& d = a.descs[cfg];
         const int lognwe = __ffs(d.m.nwe) - 1;
@@ -454,7 +465,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
                     atomicExch(a.error, 3);
                 }
             }
-        } else if (*(volatile unsigned long long*)&st.states + n_states >= a.cfg_cap) {
+        } else if (g_states + n_states >= a.cfg_cap) {
             // explore.cpp:28: a full visited set inserts nothing more
             if (lane == 0) st.capped = 1;
         } else {
@@ -507,7 +518,7 @@ __global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
             }
         }
         __syncwarp();
-        local = kept && !*(volatile int*)a.error;
+        local = kept && !g_err;
         if (local) {
             if (lane < SW - 2) pwords[lane] = kwords[lane];
             H = H_kept;
