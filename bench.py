@@ -325,7 +325,8 @@ def run_b200(args):
             "clocks": clk,
         }
         if world == 1 and not args.no_secondary:
-            line["secondary"] = secondary_metrics(m, with_reference=not args.no_cpu_baseline)
+            line["secondary"] = secondary_metrics(m, with_reference=not args.no_cpu_baseline,
+                                                  sm_clock_mhz=clk_mhz)
         if world == 1 and not args.no_cpu_baseline:
             v, kind, thr, n, st, el = reference_sample(args.cpu_sample_secs)
             line["cpu_baseline"] = {
@@ -338,7 +339,17 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
-def secondary_metrics(m, with_reference=True):
+def hbm_peak_gbps():
+    """The measured copy bandwidth of this pool (MEASURED_PEAKS.json), else the
+    profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
     """The other north-star paths, one measurement each (reported, not the headline):
     time-to-optimum of `tune` (BASELINE configs[0..1] scale), the interleaving
     exploration (configs[3]) and the swarm trajectories (configs[2])."""
@@ -371,21 +382,47 @@ def secondary_metrics(m, with_reference=True):
                                  r.stats.checks_run, r.stats.states_visited_total, r.trace.steps)
                              and sha(rr["trace"]) == sha(r.trace.transitions))
     out["tune"] = tune
-    # (2) exploration of one configuration's full interleaving space (5.6e7 states)
-    info = []
+    # (2) exploration of one configuration's full interleaving space (configs[3]:
+    # ~10^8 states with the visited-state hash table in HBM)
+    import torch
     plat16 = m.PlatformConfig(1, 1, 16, 4)
-    x = m.explore_configs(plat16, m.ProblemSpec.abstract(32), [m.TuningParams(16, 2)],
-                          max_states=400_000_000, info=info)[0]
+    m.explore_configs(plat16, m.ProblemSpec.abstract(16), [m.TuningParams(16, 1)])  # warm
+    info = []
+    t0 = time.perf_counter()
+    x = m.explore_configs(plat16, m.ProblemSpec.abstract(EXPLORE_SIZE),
+                          [m.TuningParams(*EXPLORE_PARAMS)], max_states=400_000_000, info=info)[0]
+    wall = time.perf_counter() - t0
     words = info[0].key_words
-    ex = {"workload": "explore_machine, abstract kernel, size 32, platform (1,1,16,4), "
-                      "(wg,ts)=(16,2): every interleaving",
+    line_bytes = 64 if words <= 14 else 128
+    kern_s = info[0].kernel_us * 1e-6
+    rate = x.states_visited / kern_s
+    outdeg = x.transitions_applied / max(1, x.states_visited)
+    # algorithmic bytes per state: its slot line written once and read once at
+    # expansion, one slot line read per generated successor (the probe), 8 B of queue
+    bps = line_bytes * (2 + outdeg) + 8
+    hbm_peak, hbm_src = hbm_peak_gbps()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    clk = sm_clock_mhz
+    issue_peak = sms * 4 * clk * 1e6  # warp instructions/s (one issue per SMSP per cycle)
+    ex = {"workload": f"explore_machine, abstract kernel, size {EXPLORE_SIZE}, platform (1,1,16,4), "
+                      f"(wg,ts)={EXPLORE_PARAMS}: every interleaving",
           "states": x.states_visited, "transitions": x.transitions_applied,
-          "complete": x.complete, "kernel_ms": info[0].kernel_us / 1e3,
-          "states_per_s": x.states_visited / (info[0].kernel_us * 1e-6),
-          "key_words": words,
-          "algorithmic_bytes_per_state": 8 + 8 * words + 8 + 8 * (
-              x.transitions_applied / max(1, x.states_visited))}
-    ex["achieved_GBps"] = ex["algorithmic_bytes_per_state"] * ex["states_per_s"] / 1e9
+          "complete": x.complete, "kernel_ms": kern_s * 1e3, "api_seconds": wall,
+          "states_per_s": rate, "states_per_s_api": x.states_visited / wall,
+          "key_words": words, "slot_bytes": line_bytes, "table_slots": info[0].table_slots,
+          "roofline": {
+              "bound": "latency: dependent L2/HBM round trips per state (probe, claim, queue)",
+              "hbm": {"achieved": bps * rate / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": bps * rate / 1e9 / hbm_peak, "peak_source": hbm_src,
+                      "algorithmic_bytes_per_state": bps,
+                      "traffic_bytes_per_state": EXPLORE_DRAM_BYTES_PER_STATE,
+                      "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum / states "
+                                        "(profiles/)"},
+              "issue": {"achieved": EXPLORE_INST_PER_STATE * rate / 1e9,
+                        "peak": issue_peak / 1e9, "unit": "G warp-inst/s",
+                        "frac": EXPLORE_INST_PER_STATE * rate / issue_peak,
+                        "warp_inst_per_state": EXPLORE_INST_PER_STATE,
+                        "peak_source": f"{sms} SMs x 4 SMSPs x 1 issue/cycle x {clk:.0f} MHz"}}}
     if ref is not None:
         t0 = time.perf_counter()
         rx = ref.explore((1, 1, 8, 4), 32, 0, 8, 2)
@@ -440,6 +477,14 @@ def secondary_metrics(m, with_reference=True):
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
 # (profiles/r01_argmin_v2_ncu.txt).  Re-measured after every kernel change.
 INT_OPS_PER_CONFIG = 27.9
+
+# configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
+# state (smsp__inst_executed.sum / states; DRAM read + write bytes / states),
+# re-measured after every change of explore_kernel (profiles/).
+EXPLORE_SIZE = 64
+EXPLORE_PARAMS = (16, 2)
+EXPLORE_INST_PER_STATE = 1116.0
+EXPLORE_DRAM_BYTES_PER_STATE = 1193.0
 
 
 def main():

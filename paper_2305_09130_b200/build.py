@@ -42,7 +42,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *sources()]
+    extra = os.environ.get("MCTB_NVCC_EXTRA", "").split()  # experiments (e.g. -DMCTB_BFS_MINB=5)
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", LIB + ".tmp", *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

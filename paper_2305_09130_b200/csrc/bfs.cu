@@ -63,6 +63,10 @@ struct BfsArgs {
 
 namespace {
 
+#ifndef MCTB_BFS_MINB
+#define MCTB_BFS_MINB 4  // resident blocks per SM the register allocation targets
+#endif
+
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kBfsThreads = 256;
 
@@ -316,7 +320,7 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 }
 
 template <int SW>
-__global__ void __launch_bounds__(kBfsThreads) explore_kernel(BfsArgs a) {
+__global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(BfsArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     // per warp in shared memory: the parent (unpacked and packed) and its enabled
     // list; per lane: one packed successor row.  Only the generic transitions
