@@ -51,7 +51,7 @@ struct BfsArgs {
     // tq = (tail << 32) | outstanding: queue reservations and the count of states
     // discovered but not yet expanded move together in one atomic
     unsigned long long* tq;
-    const uint32_t* ftab;  // [n_cfg * kMaxFields] field tables (bfs_rules.cuh)
+    const uint2* ftab;     // [n_cfg * kMaxFields] field tables (bfs_rules.cuh)
     const int* nfields;    // [n_cfg]
     BfsStats* stats;  // [n_cfg]
     int* error;       // 1 table full, 2 queue full, 3 model bug
@@ -360,42 +360,52 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     uint64_t H = 0;      // hash of the parent (known for a kept successor)
     // queue entries are claimed in runs: a warp that finds its entries already
     // filled doubles its next claim (up to 8), one that has to wait claims one
-    unsigned long long h_next = 0, h_end = 0;
+    unsigned long long h_next = 0, h_end = 0, h_run = 0;
     unsigned claim = 1;
+    uint32_t peek = kEmpty;  // lane j: entry h_run + j of the current run, as first read
     for (;;) {
         if (!local) {
             if (h_next == h_end) {
                 unsigned long long h0 = 0;
                 if (lane == 0) h0 = atomicAdd(a.head, (unsigned long long)claim);
-                h_next = __shfl_sync(0xffffffffu, h0, 0);
+                h_run = h_next = __shfl_sync(0xffffffffu, h0, 0);
                 h_end = h_next + claim;
+                // read the whole run at once and start the filled entries' slot lines
+                // on their way to L2; a later pop of a filled entry needs no poll
+                peek = lane < (int)claim && h_run + lane < a.queue_cap
+                           ? ld_relaxed32(&a.queue[h_run + lane])
+                           : kEmpty;
+                if (peek != kEmpty)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.table + (uint64_t)peek * SW));
             }
             const unsigned long long h = h_next++;
             if (h >= a.queue_cap) break;
-            // wait until entry h is pushed, or the sweep is over
-            uint32_t slot = kEmpty;
+            uint32_t slot = __shfl_sync(0xffffffffu, peek, (int)(h - h_run));
             bool waited = false;
-            if (lane == 0) {
-                unsigned ns = 64;
-                for (unsigned it = 0;; ++it) {
-                    slot = ld_relaxed32(&a.queue[h]);  // relaxed poll: no L1 invalidation
-                    if (slot != kEmpty) break;
-                    waited = true;
-                    // the shared counters are read rarely: they are the working warps'
-                    // atomics' cache line
-                    if ((it & 15) == 15 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
-                                            ld_relaxed32((const uint32_t*)a.error)))
-                        break;
-                    if (it > (1u << 23)) {  // watchdog: outstanding states never arrive
-                        atomicExch(a.error, 7);
-                        break;
+            if (slot == kEmpty) {
+                // wait until entry h is pushed, or the sweep is over
+                if (lane == 0) {
+                    unsigned ns = 64;
+                    for (unsigned it = 0;; ++it) {
+                        slot = ld_relaxed32(&a.queue[h]);  // relaxed poll: no L1 invalidation
+                        if (slot != kEmpty) break;
+                        waited = true;
+                        // the shared counters are read rarely: they are the working warps'
+                        // atomics' cache line
+                        if ((it & 15) == 15 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
+                                                ld_relaxed32((const uint32_t*)a.error)))
+                            break;
+                        if (it > (1u << 23)) {  // watchdog: outstanding states never arrive
+                            atomicExch(a.error, 7);
+                            break;
+                        }
+                        __nanosleep(ns);
+                        if (ns < 1024) ns <<= 1;
                     }
-                    __nanosleep(ns);
-                    if (ns < 1024) ns <<= 1;
                 }
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+                waited = __shfl_sync(0xffffffffu, waited, 0);
             }
-            slot = __shfl_sync(0xffffffffu, slot, 0);
-            waited = __shfl_sync(0xffffffffu, waited, 0);
             claim = waited ? 1u : (claim < 8u ? claim * 2u : 8u);
             if (slot == kEmpty) break;
             // one coalesced line read; a word without its guard bit is still being
@@ -599,7 +609,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         words = std::max(words, descs[c].l.words);
     }
     // field tables of the table-driven unpack
-    std::vector<uint32_t> ftab((size_t)n_cfg * kMaxFields);
+    std::vector<uint2> ftab((size_t)n_cfg * kMaxFields);
     std::vector<int> nfields(n_cfg);
     for (int c = 0; c < n_cfg; ++c)
         nfields[c] = build_field_table(descs[c].m, descs[c].l, ftab.data() + (size_t)c * kMaxFields);
@@ -646,7 +656,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
         a.check_inv = check_invariants ? 1 : 0;
         const size_t sz_table = cap * 4 * (size_t)sw, sz_q = qcap * 4;
-        const size_t sz_ftab = ftab.size() * 4 + nfields.size() * 4;
+        const size_t sz_ftab = ftab.size() * 8 + nfields.size() * 4;
         const size_t sz_misc = 512 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg + sz_ftab;
         void* blob = nullptr;
         MCTB_CUDA(cudaMallocAsync(&blob, sz_table + sz_q + sz_misc, st));
@@ -660,10 +670,10 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.op_hist = getenv("MCTB_BFS_OPHIST") ? (unsigned long long*)(misc + 32) : nullptr;
         a.stats = (BfsStats*)(misc + 512);
         a.descs = (BfsDesc*)(misc + 512 + sizeof(BfsStats) * n_cfg);
-        uint32_t* d_ftab = (uint32_t*)(misc + 512 + (sizeof(BfsStats) + sizeof(BfsDesc)) * n_cfg);
+        uint2* d_ftab = (uint2*)(misc + 512 + (sizeof(BfsStats) + sizeof(BfsDesc)) * n_cfg);
         a.ftab = d_ftab;
         a.nfields = (const int*)(d_ftab + ftab.size());
-        MCTB_CUDA(cudaMemcpyAsync(d_ftab, ftab.data(), ftab.size() * 4, cudaMemcpyHostToDevice, st));
+        MCTB_CUDA(cudaMemcpyAsync(d_ftab, ftab.data(), ftab.size() * 8, cudaMemcpyHostToDevice, st));
         MCTB_CUDA(cudaMemcpyAsync(d_ftab + ftab.size(), nfields.data(), nfields.size() * 4,
                                   cudaMemcpyHostToDevice, st));
         MCTB_CUDA(cudaMemsetAsync(a.table, 0, sz_table, st));

@@ -27,18 +27,22 @@
 
 namespace mctb {
 
-// one entry per packed field: word i (5 bits) | shift (5) | width (6) |
-// byte offset in MState (13) | store size (2: 0 = 16-bit, 1 = 32-bit)
+// one entry per packed field: {word i (5 bits) | shift sh (5) | 31 - sh (5) |
+// byte offset in MState (13, from bit 16) | store size (bit 29: 0 = 16-bit,
+// 1 = 32-bit), value mask}
 constexpr int kMaxFields = 10 + 3 * kMaxDev + 8 * kMaxUnit + 7 * kMaxPex + kMaxLoc;
 
-__host__ __device__ inline uint32_t field_entry(int off, int width, size_t dst, int sz) {
+__host__ __device__ inline uint2 field_entry(int off, int width, size_t dst, int sz) {
     const int i = off / kWordBits, sh = off % kWordBits;
-    return (uint32_t)i | ((uint32_t)sh << 5) | ((uint32_t)width << 10) | ((uint32_t)dst << 16) |
-           ((uint32_t)sz << 29);
+    uint2 e;
+    e.x = (uint32_t)i | ((uint32_t)sh << 5) | ((uint32_t)(kWordBits - sh) << 10) |
+          ((uint32_t)dst << 16) | ((uint32_t)sz << 29);
+    e.y = (uint32_t)((1ull << width) - 1);
+    return e;
 }
 
 // The field table of a layout, in pack() order (pack.cuh).  Returns the count.
-__host__ inline int build_field_table(const MachDesc& m, const Layout& l, uint32_t* out) {
+__host__ inline int build_field_table(const MachDesc& m, const Layout& l, uint2* out) {
     int n = 0, off = l.cfg;
     auto add = [&](int width, size_t dst, int sz) {
         out[n++] = field_entry(off, width, dst, sz);
@@ -89,18 +93,18 @@ __host__ inline int build_field_table(const MachDesc& m, const Layout& l, uint32
 // Warp-parallel unpack: lane f extracts fields f, f+32, ... into the shared
 // MState (the caller syncs the warp).  `in` holds >= words+1 readable words.
 // The time field is written as the low word of MState::time: the caller keeps
-// the high word zero.
-__device__ __forceinline__ void unpack_fields(const uint32_t* __restrict__ ftab, int nf,
+// the high word zero.  A field's bits are the data bits [sh, 31) of word i
+// followed by the low bits of word i+1 (pack.cuh: 31 data bits per word).
+__device__ __forceinline__ void unpack_fields(const uint2* __restrict__ ftab, int nf,
                                               const uint32_t* in, MState& s, int lane) {
     char* base = reinterpret_cast<char*>(&s);
     for (int f = lane; f < nf; f += 32) {
-        const uint32_t e = __ldg(ftab + f);
-        const int i = e & 31, sh = (e >> 5) & 31, w = (e >> 10) & 63;
-        const uint32_t dst = (e >> 16) & 0x1fff, sz = e >> 29;
-        const uint64_t x = (uint64_t)(in[i] & kData) | ((uint64_t)(in[i + 1] & kData) << kWordBits);
-        const uint32_t v = (uint32_t)(x >> sh) & (uint32_t)((1ull << w) - 1);
-        if (sz == 0) *reinterpret_cast<uint16_t*>(base + dst) = (uint16_t)v;
-        else *reinterpret_cast<uint32_t*>(base + dst) = v;
+        const uint2 e = __ldg(ftab + f);
+        const int i = e.x & 31, sh = (e.x >> 5) & 31, rsh = (e.x >> 10) & 31;
+        const uint32_t v = (((in[i] & kData) >> sh) | (in[i + 1] << rsh)) & e.y;
+        const uint32_t dst = (e.x >> 16) & 0x1fff;
+        if (e.x & (1u << 29)) *reinterpret_cast<uint32_t*>(base + dst) = v;
+        else *reinterpret_cast<uint16_t*>(base + dst) = (uint16_t)v;
     }
 }
 
