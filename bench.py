@@ -386,7 +386,7 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
     # ~10^8 states with the visited-state hash table in HBM)
     import torch
     plat16 = m.PlatformConfig(1, 1, 16, 4)
-    m.explore_configs(plat16, m.ProblemSpec.abstract(16), [m.TuningParams(16, 1)])  # warm
+    m.explore_configs(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(16), [m.TuningParams(4, 2)])  # warm
     info = []
     t0 = time.perf_counter()
     x = m.explore_configs(plat16, m.ProblemSpec.abstract(EXPLORE_SIZE),
