@@ -3,7 +3,7 @@
  * OpenCL programs").  C ABI: plain pointers and sizes only.
  *
  * Each entry point replaces one interface of the reference C++ core
- * (/root/reference/proj/include/mctune/*.hpp); the citation is on the
+ * (/root/reference/proj/include/mctune/{model,explore,search}.hpp); the citation is on the
  * declaration.  Conventions shared by all calls:
  *   plat   : int[4] = {nd, nu, np, gmt}                 (model.hpp:37-44 PlatformConfig)
  *   size   : input length, a power of two >= 4           (model.hpp:53-64 ProblemSpec)

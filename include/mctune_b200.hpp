@@ -1,0 +1,677 @@
+// mctune_b200.hpp — the C++ host API of the B200 search engine.
+//
+// A header-only mirror of the reference library's public interface
+// (/root/reference/proj/include/mctune/{model,explore,search}.hpp): the same
+// type names, fields, function signatures, argument meanings and exception
+// classes, implemented on the C ABI of include/mctune_b200.h (every model time
+// is computed by sm_100a kernels; there is no CPU path — calls throw NoDevice
+// without a B200).  Code written against `mctune::` compiles against this
+// header through include/compat/mctune/*.hpp, which alias the namespace.
+//
+// Link: -L<repo>/paper_2305_09130_b200 -lmctune_b200 (C++20).
+#ifndef MCTUNE_B200_HPP
+#define MCTUNE_B200_HPP
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <optional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mctune_b200.h"
+
+namespace mctune_b200 {
+
+/// Model time, in clock ticks (model.hpp:12).
+using Tick = std::int64_t;
+
+// ------------------------------------------------------------------ errors
+/// Invalid user input (model.hpp:15-18).
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// Internal contract violation of the transition system (model.hpp:21-24).
+struct ModelBug : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// A trace failed to replay (explore.hpp:14-17).
+struct CorruptTrace : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// No sm_100 device is visible (the engine has no CPU path).
+struct NoDevice : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// A GPU capacity limit (state packing, visited table) was exceeded.
+struct LimitError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == MCTB_OK) return;
+    const std::string msg = mctb_last_error() ? mctb_last_error() : "";
+    switch (rc) {
+        case MCTB_CONFIG_ERROR: throw ConfigError(msg);
+        case MCTB_MODEL_BUG: throw ModelBug(msg);
+        case MCTB_CORRUPT_TRACE: throw CorruptTrace(msg);
+        case MCTB_NO_DEVICE: throw NoDevice(msg.empty() ? "no sm_100 device" : msg);
+        case MCTB_LIMIT: throw LimitError(msg);
+        default: throw std::runtime_error("CUDA error: " + msg);
+    }
+}
+}  // namespace detail
+
+// ------------------------------------------------------------------ model (model.hpp)
+constexpr bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+/// Exact log2 of a power of two (model.cpp:94-99).
+inline int log2_exact(int v) {
+    if (!is_pow2(v)) throw ConfigError("not a power of two: " + std::to_string(v));
+    int k = 0;
+    while ((1 << k) < v) ++k;
+    return k;
+}
+
+/// Architecture constants of the abstract platform (model.hpp:37-44).
+struct PlatformConfig {
+    int nd = 1;
+    int nu = 1;
+    int np = 4;
+    int gmt = 4;
+
+    void validate() const {  // model.cpp:101-106
+        if (nd < 1 || nu < 1 || np < 1 || gmt < 1)
+            throw ConfigError("platform constants nd, nu, np, gmt must all be >= 1");
+        if (!is_pow2(np)) throw ConfigError("np must be a power of two, got " + std::to_string(np));
+    }
+    bool operator==(const PlatformConfig&) const = default;
+};
+
+enum class KernelKind : std::uint8_t { Abstract, Minimum };
+
+inline const char* to_string(KernelKind k) {
+    return k == KernelKind::Abstract ? "abstract" : "minimum";
+}
+
+inline KernelKind kernel_kind_from_string(const std::string& s) {  // model.cpp:112-116
+    if (s == "abstract") return KernelKind::Abstract;
+    if (s == "minimum") return KernelKind::Minimum;
+    throw ConfigError("unknown kernel kind '" + s + "' (expected abstract or minimum)");
+}
+
+/// The problem instance (model.hpp:53-64).
+struct ProblemSpec {
+    int size = 8;
+    KernelKind kernel = KernelKind::Abstract;
+    std::vector<std::int64_t> input;  // minimum kernel only, length == size
+
+    static ProblemSpec abstract(int size) {
+        ProblemSpec p;
+        p.size = size;
+        p.validate();
+        return p;
+    }
+    /// Minimum kernel; empty input selects the default glob[i] = size - i.
+    static ProblemSpec minimum(int size, std::vector<std::int64_t> input = {}) {
+        ProblemSpec p;
+        p.size = size;
+        p.kernel = KernelKind::Minimum;
+        if (input.empty() && size > 0)
+            for (int i = 0; i < size; ++i) input.push_back(size - i);
+        p.input = std::move(input);
+        p.validate();
+        return p;
+    }
+    void validate() const {  // model.cpp:140-149
+        if (size < 4 || !is_pow2(size))
+            throw ConfigError("size must be a power of two >= 4, got " + std::to_string(size));
+        if (kernel == KernelKind::Minimum) {
+            if (static_cast<int>(input.size()) != size)
+                throw ConfigError("minimum kernel needs an input array of length size");
+        } else if (!input.empty()) {
+            throw ConfigError("abstract kernel takes no input array");
+        }
+    }
+};
+
+/// The two tuning parameters (model.hpp:67-72).
+struct TuningParams {
+    int wg = 0;
+    int ts = 0;
+    bool operator==(const TuningParams&) const = default;
+};
+
+/// Launch shape derived from (platform, size, params) (model.hpp:75-83).
+struct LaunchPlan {
+    int wgs = 0;
+    int nwd = 0;
+    int nwu = 0;
+    int nwe = 0;
+    int all_nwe = 0;
+    bool operator==(const LaunchPlan&) const = default;
+};
+
+/// model.cpp:151-159
+inline void validate_params(int size, const TuningParams& params) {
+    const int hi = size / 2;
+    if (!is_pow2(params.wg) || params.wg < 2 || params.wg > hi)
+        throw ConfigError("wg must be a power of two in [2, size/2], got " + std::to_string(params.wg));
+    if (!is_pow2(params.ts) || params.ts < 2 || params.ts > hi)
+        throw ConfigError("ts must be a power of two in [2, size/2], got " + std::to_string(params.ts));
+}
+
+/// Listing-3 launch arithmetic (model.cpp:161-177), mctb_derive_launch.
+inline LaunchPlan derive_launch(const PlatformConfig& platform, int size, const TuningParams& params) {
+    const int plat[4] = {platform.nd, platform.nu, platform.np, platform.gmt};
+    int out[5];
+    detail::check(mctb_derive_launch(plat, size, params.wg, params.ts, out));
+    return LaunchPlan{out[0], out[1], out[2], out[3], out[4]};
+}
+
+/// All (wg, ts) = (2^i, 2^j), i, j in [1, n-1], ascending (model.cpp:179-189).
+inline std::vector<TuningParams> enumerate_configs(int size) {
+    if (size < 4 || !is_pow2(size))
+        throw ConfigError("size must be a power of two >= 4, got " + std::to_string(size));
+    const int n = log2_exact(size);
+    std::vector<TuningParams> out;
+    for (int i = 1; i < n; ++i)
+        for (int j = 1; j < n; ++j) out.push_back(TuningParams{1 << i, 1 << j});
+    return out;
+}
+
+/// kernel.cpp:84-87: the minimum kernel needs wg * ts <= size.
+inline bool config_feasible(const ProblemSpec& problem, const TuningParams& params) {
+    return problem.kernel == KernelKind::Abstract || params.wg * params.ts <= problem.size;
+}
+
+// ------------------------------------------------------------------ machine (machine.hpp)
+/// Transition labels (machine.hpp:50-70).
+enum class Op : std::uint8_t {
+    ClockTick, ClockHalt, HostGo, HostReactGo, HostStop, HostSetFin, DeviceUnitGo, DeviceDone,
+    DeviceUnitStop, UnitPexGo, UnitDone, UnitPexStop, UnitBarrierStop, PexReport, PexEffect,
+    PexArrive, PexItemDone, PexEndDone, BarrierRelease
+};
+
+/// One atomic step of the transition system (machine.hpp:78-88).
+struct Transition {
+    std::uint16_t actor = 0;
+    std::uint16_t peer = 0xffff;
+    Op op = Op::ClockTick;
+    std::int32_t arg = 0;
+    bool operator==(const Transition&) const = default;
+};
+
+/// Scheduling policies of Machine::run (machine.hpp:219) plus the engine's own.
+enum class SchedPolicy : std::uint8_t {
+    RoundRobin = MCTB_POLICY_ROUND_ROBIN,
+    SeededRandom = MCTB_POLICY_MT19937,  // std::mt19937_64, bit-exact with the reference
+    FirstEnabled = MCTB_POLICY_FIRST,    // the first DFS path of explore_machine
+    Philox = MCTB_POLICY_PHILOX,         // counter-based swarm trajectory
+    TickLast = MCTB_POLICY_TICK_LAST     // lock-step schedule
+};
+
+/// Machine::run's outcome (machine.hpp:184-190): final time, transition count,
+/// and glob[0] for the minimum kernel.
+struct RunOutcome {
+    Tick time = 0;
+    long long transitions = 0;
+    std::optional<std::int64_t> result;
+};
+
+namespace detail {
+struct Args {
+    int plat[4];
+    int size, kernel;
+    const std::int64_t* input;
+    Args(const PlatformConfig& p, const ProblemSpec& prob)
+        : plat{p.nd, p.nu, p.np, p.gmt},
+          size(prob.size),
+          kernel(prob.kernel == KernelKind::Minimum ? 1 : 0),
+          input(prob.kernel == KernelKind::Minimum && !prob.input.empty() ? prob.input.data()
+                                                                         : nullptr) {}
+};
+
+inline std::vector<Transition> unpack(const std::vector<std::int32_t>& buf, long long n) {
+    std::vector<Transition> t(static_cast<std::size_t>(n));
+    for (long long i = 0; i < n; ++i)
+        t[i] = Transition{static_cast<std::uint16_t>(buf[4 * i]),
+                          static_cast<std::uint16_t>(buf[4 * i + 1]),
+                          static_cast<Op>(buf[4 * i + 2]), buf[4 * i + 3]};
+    return t;
+}
+
+inline std::vector<std::int32_t> pack(const std::vector<Transition>& t) {
+    std::vector<std::int32_t> b(4 * t.size());
+    for (std::size_t i = 0; i < t.size(); ++i) {
+        b[4 * i] = t[i].actor;
+        b[4 * i + 1] = t[i].peer;
+        b[4 * i + 2] = static_cast<std::int32_t>(t[i].op);
+        b[4 * i + 3] = t[i].arg;
+    }
+    return b;
+}
+
+// Runs `call(trace, cap, &len)` with a trace buffer that grows once to the
+// reported length when the first capacity is too small.
+template <class F>
+std::vector<Transition> with_trace(F&& call) {
+    std::int64_t cap = 1 << 16, len = 0;
+    std::vector<std::int32_t> buf(4 * cap);
+    check(call(buf.data(), cap, &len));
+    if (len > cap) {
+        cap = len;
+        buf.assign(4 * cap, 0);
+        check(call(buf.data(), cap, &len));
+    }
+    return unpack(buf, std::min(len, cap));
+}
+
+using Clock = std::chrono::steady_clock;
+inline double since(Clock::time_point t0) {
+    return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+}  // namespace detail
+
+/// Machine::run (machine.hpp:224-227) on the GPU.
+inline RunOutcome run(const PlatformConfig& platform, const ProblemSpec& problem,
+                      const TuningParams& params, SchedPolicy policy, std::uint64_t seed = 0,
+                      std::vector<Transition>* trace_out = nullptr) {
+    const detail::Args a(platform, problem);
+    std::int64_t out[4];
+    auto call = [&](std::int32_t* tr, std::int64_t cap, std::int64_t* len) {
+        return mctb_simulate(a.plat, a.size, a.kernel, a.input, params.wg, params.ts,
+                             static_cast<int>(policy), seed, 0, out, tr, cap, len);
+    };
+    if (trace_out) {
+        *trace_out = detail::with_trace(call);
+    } else {
+        std::int64_t len = 0;
+        detail::check(call(nullptr, 0, &len));
+    }
+    RunOutcome r;
+    r.time = out[0];
+    r.transitions = out[1];
+    if (problem.kernel == KernelKind::Minimum) r.result = out[2];
+    return r;
+}
+
+// ------------------------------------------------------------------ explore (explore.hpp)
+/// Checked properties (explore.hpp:23-36).
+struct Property {
+    enum class Kind : std::uint8_t { OverTime, NonTermination };
+    Kind kind = Kind::NonTermination;
+    Tick bound = 0;
+    static Property over_time(Tick t) { return Property{Kind::OverTime, t}; }
+    static Property non_termination() { return Property{Kind::NonTermination, 0}; }
+    bool violated_by(Tick final_time) const {
+        return kind == Kind::NonTermination || final_time <= bound;
+    }
+};
+
+/// explore.hpp:38-44.  max_states is the per-configuration visited cap; the
+/// engine's exploration is exact (Bitstate is rejected like the reference's
+/// bisection rejects it) and has no depth or wall-clock cut.
+struct ExploreLimits {
+    long long max_depth = 4'000'000;
+    long long max_states = 5'000'000;
+    double wall_budget_secs = 0.0;
+    enum class Mode : std::uint8_t { Exact, Bitstate };
+    Mode mode = Mode::Exact;
+};
+
+/// explore.hpp:46-56.
+struct ExploreStats {
+    long long states_visited = 0;
+    long long transitions_applied = 0;
+    long long max_depth_reached = 0;
+    double wall_seconds = 0.0;
+    bool limit_hit = false;
+    int configs_explored = 0;
+    int configs_skipped = 0;
+
+    void absorb(const ExploreStats& o) {
+        states_visited += o.states_visited;
+        transitions_applied += o.transitions_applied;
+        max_depth_reached = std::max(max_depth_reached, o.max_depth_reached);
+        wall_seconds += o.wall_seconds;
+        limit_hit = limit_hit || o.limit_hit;
+        configs_explored += o.configs_explored;
+        configs_skipped += o.configs_skipped;
+    }
+};
+
+/// A replayable counterexample (explore.hpp:60-65).
+struct Trace {
+    std::vector<Transition> transitions;
+    Tick final_time = 0;
+    TuningParams params{};
+    long long steps = 0;
+};
+
+/// explore.hpp:67-72.
+struct Verdict {
+    bool violated = false;
+    bool exhaustive = false;
+    std::optional<Trace> trace;
+    ExploreStats stats;
+};
+
+/// Every interleaving of one configuration, plus the terminal-time range (a
+/// proof of the minimal time over all schedules) — explore_machine
+/// (explore.hpp:88-93) without the per-state hooks.
+struct ExploreResult {
+    bool complete = false;
+    ExploreStats stats;
+    Tick min_time = -1, max_time = -1;
+    long long terminal_states = 0, deadlocks = 0, invariant_violations = 0;
+};
+
+inline std::vector<ExploreResult> explore_configs(const PlatformConfig& platform,
+                                                  const ProblemSpec& problem,
+                                                  const std::vector<TuningParams>& configs,
+                                                  const ExploreLimits& limits = {},
+                                                  bool check_invariants = false) {
+    const detail::Args a(platform, problem);
+    std::vector<std::int32_t> c;
+    for (const auto& p : configs) {
+        c.push_back(p.wg);
+        c.push_back(p.ts);
+    }
+    std::vector<std::int64_t> out(9 * configs.size());
+    std::int64_t info[4];
+    const auto t0 = detail::Clock::now();
+    detail::check(mctb_explore(a.plat, a.size, a.kernel, a.input, c.data(),
+                               static_cast<int>(configs.size()), limits.max_states,
+                               check_invariants ? 1 : 0, out.data(), info));
+    const double wall = detail::since(t0);
+    std::vector<ExploreResult> res(configs.size());
+    for (std::size_t i = 0; i < configs.size(); ++i) {
+        const std::int64_t* o = out.data() + 9 * i;
+        ExploreResult& r = res[i];
+        r.complete = o[0] != 0;
+        r.stats.states_visited = o[1];
+        r.stats.transitions_applied = o[2];
+        r.stats.max_depth_reached = o[3];
+        r.stats.limit_hit = !r.complete;
+        r.stats.configs_explored = 1;
+        r.stats.wall_seconds = wall;
+        r.min_time = o[4];
+        r.max_time = o[5];
+        r.terminal_states = o[6];
+        r.deadlocks = o[7];
+        r.invariant_violations = o[8];
+    }
+    return res;
+}
+
+inline ExploreResult explore_machine(const PlatformConfig& platform, const ProblemSpec& problem,
+                                     const TuningParams& params, const ExploreLimits& limits = {}) {
+    return explore_configs(platform, problem, {params}, limits).front();
+}
+
+/// Exhaustive check of the over-time property across the whole parameter
+/// space (explore.hpp:95-101).
+inline Verdict check_overtime(const PlatformConfig& platform, const ProblemSpec& problem, Tick T,
+                              const ExploreLimits& limits) {
+    if (limits.mode != ExploreLimits::Mode::Exact)
+        throw ConfigError("the GPU check is exact mode only");
+    const detail::Args a(platform, problem);
+    std::int64_t out[12];
+    const auto t0 = detail::Clock::now();
+    auto tr = detail::with_trace([&](std::int32_t* buf, std::int64_t cap, std::int64_t* len) {
+        return mctb_check_overtime(a.plat, a.size, a.kernel, a.input, T, limits.max_states, out,
+                                   buf, cap, len);
+    });
+    Verdict v;
+    v.violated = out[0] != 0;
+    v.exhaustive = out[1] != 0;
+    v.stats.states_visited = out[2];
+    v.stats.max_depth_reached = out[3];
+    v.stats.transitions_applied = out[4];
+    v.stats.configs_explored = static_cast<int>(out[5]);
+    v.stats.configs_skipped = static_cast<int>(out[6]);
+    v.stats.limit_hit = !v.exhaustive;
+    v.stats.wall_seconds = detail::since(t0);
+    if (v.violated)
+        v.trace = Trace{std::move(tr), out[7], TuningParams{static_cast<int>(out[8]),
+                                                            static_cast<int>(out[9])},
+                        out[10]};
+    return v;
+}
+
+/// Re-applies a trace from the initial state (explore.hpp:113-116); throws
+/// CorruptTrace on divergence.  Returns the terminal time and, for the
+/// minimum kernel, glob[0].
+inline RunOutcome replay(const PlatformConfig& platform, const ProblemSpec& problem,
+                         const Trace& trace) {
+    const detail::Args a(platform, problem);
+    const auto buf = detail::pack(trace.transitions);
+    std::int64_t out[2];
+    detail::check(mctb_replay(a.plat, a.size, a.kernel, a.input, trace.params.wg, trace.params.ts,
+                              buf.data(), static_cast<std::int64_t>(trace.transitions.size()),
+                              trace.final_time, out));
+    RunOutcome r;
+    r.time = out[0];
+    r.transitions = static_cast<long long>(trace.transitions.size());
+    if (problem.kernel == KernelKind::Minimum) r.result = out[1];
+    return r;
+}
+
+/// trace_to_text (report.hpp, report.cpp:82-97).
+inline std::string trace_to_text(const PlatformConfig& platform, const ProblemSpec& problem,
+                                 const Trace& trace) {
+    const detail::Args a(platform, problem);
+    const auto buf = detail::pack(trace.transitions);
+    const auto n = static_cast<std::int64_t>(trace.transitions.size());
+    const std::int64_t len = mctb_trace_text(a.plat, a.size, a.kernel, a.input, trace.params.wg,
+                                             trace.params.ts, buf.data(), n, nullptr, 0);
+    if (len < 0) detail::check(MCTB_CORRUPT_TRACE);
+    std::string s(static_cast<std::size_t>(len) + 1, '\0');
+    mctb_trace_text(a.plat, a.size, a.kernel, a.input, trace.params.wg, trace.params.ts,
+                    buf.data(), n, s.data(), len + 1);
+    s.resize(static_cast<std::size_t>(len));
+    return s;
+}
+
+// ------------------------------------------------------------------ search (search.hpp)
+enum class TuneMethod : std::uint8_t { Bisect, Swarm, Sweep };
+
+inline const char* to_string(TuneMethod m) {
+    return m == TuneMethod::Bisect ? "bisect" : m == TuneMethod::Swarm ? "swarm" : "sweep";
+}
+
+struct TuneStats {
+    int checks_run = 0;
+    long long states_visited_total = 0;
+    double wall_seconds = 0.0;
+};
+
+/// search.hpp:22-35.
+struct TuneResult {
+    Tick t_min = 0;
+    TuningParams params{};
+    Trace trace;
+    Tick t_ini = 0;
+    TuneStats stats;
+    TuneMethod method = TuneMethod::Bisect;
+    bool proven = false;
+    Tick first_trail_time = 0;
+
+    /// t_min / first-trail time, in (0, 1].
+    double first_trail_optimality() const {
+        if (first_trail_time <= 0) return 1.0;
+        return static_cast<double>(t_min) / static_cast<double>(first_trail_time);
+    }
+};
+
+struct SweepRow {
+    int size = 0;
+    int wg = 0;
+    int ts = 0;
+    Tick time = 0;
+    long long transitions = 0;
+    bool ok = true;
+    std::string note;  // "infeasible" or "deadlock" when !ok
+};
+
+struct RankedTrail {
+    Tick time = 0;
+    int wg = 0;
+    int ts = 0;
+    long long transitions = 0;
+};
+
+struct ExtractedParams {
+    int wg = 0;
+    int ts = 0;
+    Tick time = 0;
+};
+
+/// Simulates one randomly chosen feasible configuration (std::mt19937_64(seed)
+/// pick, SeededRandom schedule) and returns its final time (search.cpp:94-102).
+inline Tick estimate_initial_time(const PlatformConfig& platform, const ProblemSpec& problem,
+                                  std::uint64_t seed) {
+    platform.validate();
+    problem.validate();
+    std::vector<TuningParams> feasible;
+    for (const auto& c : enumerate_configs(problem.size))
+        if (config_feasible(problem, c)) feasible.push_back(c);
+    if (feasible.empty()) throw ConfigError("no feasible configurations for this problem");
+    std::mt19937_64 rng(seed);
+    const TuningParams cfg = feasible[static_cast<std::size_t>(rng() % feasible.size())];
+    return run(platform, problem, cfg, SchedPolicy::SeededRandom, seed).time;
+}
+
+namespace detail {
+inline TuneResult tune_call(const PlatformConfig& platform, const ProblemSpec& problem, Tick t_hi,
+                            std::uint64_t seed, const ExploreLimits& limits) {
+    const Args a(platform, problem);
+    std::int64_t out[10];
+    const auto t0 = Clock::now();
+    auto tr = with_trace([&](std::int32_t* buf, std::int64_t cap, std::int64_t* len) {
+        return mctb_tune(a.plat, a.size, a.kernel, a.input, t_hi, seed, limits.max_states, out,
+                         buf, cap, len, nullptr);
+    });
+    TuneResult r;
+    r.t_min = out[0];
+    r.params = TuningParams{static_cast<int>(out[1]), static_cast<int>(out[2])};
+    r.t_ini = out[3];
+    r.proven = out[4] != 0;
+    r.stats.checks_run = static_cast<int>(out[5]);
+    r.stats.states_visited_total = out[6];
+    r.first_trail_time = out[7];
+    r.trace = Trace{std::move(tr), out[0], r.params, out[8]};
+    r.method = TuneMethod::Bisect;
+    r.stats.wall_seconds = since(t0);
+    return r;
+}
+}  // namespace detail
+
+/// Counterexample-guided binary search for the minimal termination time
+/// (search.hpp:57-62): same verdicts, statistics and trace as the reference.
+inline TuneResult bisect_min_time(const PlatformConfig& platform, const ProblemSpec& problem,
+                                  Tick t_hi, const ExploreLimits& limits) {
+    if (limits.mode != ExploreLimits::Mode::Exact) throw ConfigError("bisection needs exact mode");
+    if (t_hi < 1) throw ConfigError("t_hi must be >= 1");
+    return detail::tune_call(platform, problem, t_hi, 0, limits);
+}
+
+/// The `tune` command (tools/main.cpp): estimate_initial_time(seed), then
+/// bisect_min_time from it, in one GPU pass.
+inline TuneResult tune(const PlatformConfig& platform, const ProblemSpec& problem,
+                       std::uint64_t seed = 1, const ExploreLimits& limits = {}) {
+    if (limits.mode != ExploreLimits::Mode::Exact) throw ConfigError("bisection needs exact mode");
+    return detail::tune_call(platform, problem, 0, seed, limits);
+}
+
+/// Randomised search (search.hpp:64-71): rounds of `workers` x 4096
+/// counter-based Philox trajectories with the reference's stop rule.
+/// Heuristic: never a proof.  trails_out receives the first round's terminal
+/// runs (time, params, steps; no transition lists).
+inline TuneResult swarm_min_time(const PlatformConfig& platform, const ProblemSpec& problem,
+                                 int workers, const ExploreLimits& limits, std::uint64_t seed,
+                                 std::vector<Trace>* trails_out = nullptr) {
+    if (workers < 1) throw ConfigError("swarm needs at least one worker");
+    const detail::Args a(platform, problem);
+    const std::int64_t per_round = static_cast<std::int64_t>(workers) * 4096;
+    const std::int64_t tcap = trails_out ? per_round : 0;
+    std::vector<std::int64_t> trails(4 * std::max<std::int64_t>(tcap, 1));
+    std::int64_t out[10], nt = 0;
+    const auto t0 = detail::Clock::now();
+    auto tr = detail::with_trace([&](std::int32_t* buf, std::int64_t cap, std::int64_t* len) {
+        return mctb_swarm(a.plat, a.size, a.kernel, a.input, per_round, 64, seed,
+                          limits.max_depth, out, buf, cap, len, trails.data(), tcap, &nt);
+    });
+    TuneResult r;
+    r.t_min = out[0];
+    r.params = TuningParams{static_cast<int>(out[1]), static_cast<int>(out[2])};
+    r.t_ini = out[3];
+    r.stats.checks_run = static_cast<int>(out[4]) - 1;
+    r.stats.states_visited_total = out[5];
+    r.first_trail_time = out[6];
+    r.trace = Trace{std::move(tr), out[0], r.params, out[7]};
+    r.method = TuneMethod::Swarm;
+    r.proven = false;
+    r.stats.wall_seconds = detail::since(t0);
+    if (trails_out)
+        for (std::int64_t i = 0; i < nt; ++i)
+            trails_out->push_back(Trace{{}, trails[4 * i],
+                                        TuningParams{static_cast<int>(trails[4 * i + 1]),
+                                                     static_cast<int>(trails[4 * i + 2])},
+                                        trails[4 * i + 3]});
+    return r;
+}
+
+/// Deterministic simulation of every enumerated configuration, sorted like
+/// the reference (search.hpp:73-77).
+inline std::vector<SweepRow> exhaustive_sweep(const PlatformConfig& platform,
+                                              const ProblemSpec& problem) {
+    const detail::Args a(platform, problem);
+    const int n = static_cast<int>(enumerate_configs(problem.size).size());
+    std::vector<std::int64_t> rows(6 * static_cast<std::size_t>(n));
+    std::int64_t nr = 0;
+    detail::check(mctb_sweep(a.plat, a.size, a.kernel, a.input, rows.data(), n, &nr));
+    std::vector<SweepRow> out;
+    for (std::int64_t i = 0; i < nr; ++i) {
+        const std::int64_t* r = rows.data() + 6 * i;
+        SweepRow row;
+        row.size = problem.size;
+        row.wg = static_cast<int>(r[0]);
+        row.ts = static_cast<int>(r[1]);
+        row.time = r[2];
+        row.transitions = r[3];
+        row.ok = r[4] != 0;
+        row.note = r[5] == 1 ? "infeasible" : r[5] == 2 ? "deadlock" : "";
+        out.push_back(row);
+    }
+    return out;
+}
+
+/// Reads (wg, ts, time) out of a counterexample after replay validation
+/// (search.hpp:86-88).
+inline ExtractedParams extract_params(const PlatformConfig& platform, const ProblemSpec& problem,
+                                      const Trace& trace) {
+    const RunOutcome end = replay(platform, problem, trace);
+    return ExtractedParams{trace.params.wg, trace.params.ts, end.time};
+}
+
+/// Stable sort of trail summaries by (time, transitions) (search.hpp:90-91).
+inline std::vector<RankedTrail> rank_trails(const std::vector<Trace>& traces) {
+    std::vector<RankedTrail> out;
+    for (const auto& t : traces) out.push_back(RankedTrail{t.final_time, t.params.wg, t.params.ts, t.steps});
+    std::stable_sort(out.begin(), out.end(), [](const RankedTrail& x, const RankedTrail& y) {
+        return x.time != y.time ? x.time < y.time : x.transitions < y.transitions;
+    });
+    return out;
+}
+
+/// Number of sm_100 devices the engine sees.
+inline int device_count() { return mctb_device_count(); }
+
+}  // namespace mctune_b200
+
+#endif  // MCTUNE_B200_HPP

@@ -1,0 +1,107 @@
+// The C++ host API (include/mctune_b200.hpp) through the reference-style
+// drop-in headers (include/compat/mctune/*.hpp): written against `mctune::`
+// exactly as a caller of the reference library would, run on a B200.
+#define MINI_DOCTEST_MAIN
+#include "doctest.h"
+
+#include <mctune/explore.hpp>
+#include <mctune/model.hpp>
+#include <mctune/search.hpp>
+
+using namespace mctune;
+
+namespace {
+const PlatformConfig kPlat{1, 1, 4, 4};
+}
+
+TEST_CASE("launch shapes and the configuration space") {
+    const LaunchPlan p = derive_launch(kPlat, 1024, {16, 32});
+    CHECK(p == LaunchPlan{2, 1, 1, 4, 4});
+    CHECK(enumerate_configs(1024).size() == 81);
+    CHECK_THROWS_AS(derive_launch(PlatformConfig{1, 1, 3, 4}, 8, {2, 2}), ConfigError);
+    CHECK_THROWS_AS(ProblemSpec::abstract(12), ConfigError);
+}
+
+TEST_CASE("paper Table 1: size 8 on (1,1,4,4) tunes to 44 at (4,4)") {
+    const ProblemSpec problem = ProblemSpec::abstract(8);
+    const TuneResult r = bisect_min_time(kPlat, problem, 100, ExploreLimits{});
+    CHECK(r.t_min == 44);
+    CHECK(r.params == TuningParams{4, 4});
+    CHECK(r.proven);
+    CHECK(r.trace.final_time == 44);
+    CHECK(r.method == TuneMethod::Bisect);
+    CHECK(replay(kPlat, problem, r.trace).time == 44);
+    CHECK(extract_params(kPlat, problem, r.trace).time == 44);
+    const Verdict below = check_overtime(kPlat, problem, 43, ExploreLimits{});
+    CHECK_FALSE(below.violated);
+    CHECK(below.exhaustive);
+    CHECK_THROWS_AS(bisect_min_time(kPlat, problem, 43, ExploreLimits{}), ConfigError);
+    ExploreLimits bitstate;
+    bitstate.mode = ExploreLimits::Mode::Bitstate;
+    CHECK_THROWS_AS(bisect_min_time(kPlat, problem, 100, bitstate), ConfigError);
+}
+
+TEST_CASE("tune from the estimated bound: size 64") {
+    const ProblemSpec problem = ProblemSpec::abstract(64);
+    const Tick est = estimate_initial_time(kPlat, problem, 1);
+    const TuneResult r = tune(kPlat, problem, 1);
+    CHECK(r.t_ini == est);
+    CHECK(r.t_min == 324);
+    CHECK(r.params == TuningParams{4, 32});
+    CHECK(r.proven);
+    CHECK(r.first_trail_optimality() > 0.0);
+    CHECK(r.first_trail_optimality() <= 1.0);
+    const auto rows = exhaustive_sweep(kPlat, problem);
+    CHECK(rows.front().time == r.t_min);
+}
+
+TEST_CASE("every schedule of a configuration ends at the lock-step time") {
+    const ProblemSpec problem = ProblemSpec::abstract(16);
+    for (const auto& cfg : enumerate_configs(16)) {
+        std::vector<Transition> tr;
+        const RunOutcome rr = run(kPlat, problem, cfg, SchedPolicy::RoundRobin, 0, &tr);
+        const RunOutcome sr = run(kPlat, problem, cfg, SchedPolicy::SeededRandom, 7);
+        CHECK(rr.time == sr.time);
+        CHECK(static_cast<long long>(tr.size()) == rr.transitions);
+        const ExploreResult ex = explore_machine(kPlat, problem, cfg);
+        CHECK(ex.complete);
+        CHECK(ex.min_time == rr.time);
+        CHECK(ex.max_time == rr.time);
+        CHECK(ex.deadlocks == 0);
+    }
+}
+
+TEST_CASE("minimum kernel: infeasible rows, result and replay") {
+    const ProblemSpec problem = ProblemSpec::minimum(16);
+    const auto rows = exhaustive_sweep(kPlat, problem);
+    REQUIRE(rows.size() == 9);
+    int flagged = 0;
+    for (const auto& r : rows) flagged += !r.ok && r.note == "infeasible";
+    CHECK(flagged == 3);
+    CHECK(rows.front().time == 23);
+    std::vector<Transition> tr;
+    const RunOutcome o = run(kPlat, problem, {4, 4}, SchedPolicy::RoundRobin, 0, &tr);
+    REQUIRE(o.result.has_value());
+    CHECK(*o.result == 1);  // glob[0] = min of size - i
+    Trace t{tr, o.time, {4, 4}, o.transitions};
+    CHECK(replay(kPlat, problem, t).time == o.time);
+    CHECK(!trace_to_text(kPlat, problem, t).empty());
+    t.transitions.pop_back();
+    CHECK_THROWS_AS(replay(kPlat, problem, t), CorruptTrace);
+}
+
+TEST_CASE("swarm agrees with bisection at desk scale") {
+    const ProblemSpec problem = ProblemSpec::abstract(8);
+    std::vector<Trace> trails;
+    const TuneResult s = swarm_min_time(kPlat, problem, 2, ExploreLimits{}, 7, &trails);
+    CHECK(s.t_min == 44);
+    CHECK(s.params == TuningParams{4, 4});
+    CHECK_FALSE(s.proven);
+    CHECK(replay(kPlat, problem, s.trace).time == 44);
+    CHECK(!trails.empty());
+    const auto ranked = rank_trails(trails);
+    CHECK(ranked.front().time == 44);
+    const TuneResult again = swarm_min_time(kPlat, problem, 2, ExploreLimits{}, 7);
+    CHECK(again.trace.transitions == s.trace.transitions);
+    CHECK_THROWS_AS(swarm_min_time(kPlat, problem, 0, ExploreLimits{}, 1), ConfigError);
+}
