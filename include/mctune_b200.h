@@ -129,7 +129,10 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
 /* explore_machine (explore.hpp:272-277) over several configurations in one GPU sweep
  * (configs = int32[2 * n] of (wg, ts)); max_states = the reference's per-machine visited
  * cap (ExploreLimits::max_states, default 5e6 when <= 0); flags bit 0 = check
- * Machine::check_invariants (machine.cpp:719-756) and tick gating on every state.
+ * Machine::check_invariants (machine.cpp:719-756) and tick gating on every state;
+ * bits 8-11 = P > 1 splits the visited set into P hash partitions on this device,
+ * the exchange of the multi-GPU sweep (mctb_explore_mp_*) run on one GPU; bit 1 =
+ * use the multi-GPU kernel's system-scope memory operations.
  * out = int64[9 * n]: {complete, states_visited, transitions_applied, max_depth_reached,
  *                      min_final_time, max_final_time, terminal_states, deadlocks,
  *                      invariant_violations}

@@ -38,23 +38,35 @@
 
 namespace mctb {
 
+constexpr int kMaxParts = 8;
+
+// One hash partition of the visited set: its table, work queue and counters.
+// A state belongs to partition owner(h) = (hi32(h) * P) >> 32; the partitions
+// of a sweep live on one device (a single-GPU partitioned run) or one per GPU
+// (peer memory over NVLink, bfs_mp.cu).
+struct BfsPart {
+    uint32_t* table;           // [cap * SW]: slot = {key, padding, tag}
+    uint32_t* queue;           // [queue_cap] slot indices, EMPTY until pushed
+    unsigned long long* head;
+    // tq = (tail << 32) | outstanding: queue reservations and the count of states
+    // discovered but not yet expanded move together in one atomic
+    unsigned long long* tq;
+    int* error;                // 1 table full, 2 queue full, 3 model bug, >= 5 watchdog
+};
+
 struct BfsArgs {
     const BfsDesc* descs;
     int n_cfg;
     int words;                 // key words per slot (max over configurations)
     int cfg_bits;
-    uint64_t cap_mask;         // table capacity - 1 (power of two)
-    uint32_t* table;           // [cap * SW]: slot = {key, padding, tag}
-    uint32_t* queue;           // [queue_cap] slot indices, EMPTY until pushed
+    uint64_t cap_mask;         // table capacity - 1 (power of two), every partition
     uint64_t queue_cap;
-    unsigned long long* head;
-    // tq = (tail << 32) | outstanding: queue reservations and the count of states
-    // discovered but not yet expanded move together in one atomic
-    unsigned long long* tq;
+    BfsPart part[kMaxParts];
+    int n_parts;               // P
+    int part0, n_here;         // partitions this launch expands: [part0, part0 + n_here)
     const uint2* ftab;     // [n_cfg * kMaxFields] field tables (bfs_rules.cuh)
     const int* nfields;    // [n_cfg]
     BfsStats* stats;  // [n_cfg]
-    int* error;       // 1 table full, 2 queue full, 3 model bug
     uint64_t cfg_cap; // per-configuration visited cap (ExploreLimits::max_states)
     int keep;         // continue with the first new successor (no queue round trip)
     unsigned long long* op_hist;  // generic successors per op (diagnostics)
@@ -70,30 +82,71 @@ namespace {
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kBfsThreads = 256;
 
+// Memory operations on the shared structures (tables, queues, counters).
+// SYS = the partitions span GPUs (peer memory): system scope; else GPU scope.
+template <bool SYS>
 __device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (SYS) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
+template <bool SYS>
 __device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (SYS) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
+template <bool SYS>
 __device__ __forceinline__ void ld_relaxed_v4(const uint32_t* p, uint32_t* v) {
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-                 : "l"(p)
-                 : "memory");
+    if (SYS)
+        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "l"(p)
+                     : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "l"(p)
+                     : "memory");
 }
 
-// One slot line (SW words: key + padding + tag) from L2, 16 bytes per load.
-template <int SW>
+template <bool SYS>
+__device__ __forceinline__ void st_relaxed32(uint32_t* p, uint32_t v) {
+    if (SYS) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <bool SYS>
+__device__ __forceinline__ unsigned long long atom_add(unsigned long long* p, unsigned long long v) {
+    return SYS ? atomicAdd_system(p, v) : atomicAdd(p, v);
+}
+
+template <bool SYS>
+__device__ __forceinline__ unsigned long long atom_cas(unsigned long long* p, unsigned long long c,
+                                                       unsigned long long v) {
+    return SYS ? atomicCAS_system(p, c, v) : atomicCAS(p, c, v);
+}
+
+template <bool SYS>
+__device__ __forceinline__ void set_error(int* p, int code) {
+    if (SYS) atomicExch_system(p, code);
+    else atomicExch(p, code);
+}
+
+// One slot line (SW words: key + padding + tag), 16 bytes per load.
+template <int SW, bool SYS>
 __device__ __forceinline__ void ld_line(const uint32_t* p, uint32_t (&v)[SW]) {
 #pragma unroll
-    for (int c = 0; c < SW / 4; ++c) ld_relaxed_v4(p + 4 * c, v + 4 * c);
+    for (int c = 0; c < SW / 4; ++c) ld_relaxed_v4<SYS>(p + 4 * c, v + 4 * c);
+}
+
+// Partition of a state: the high half of its hash (the slot uses the low bits).
+__device__ __forceinline__ int owner_of(uint64_t h, int n_parts) {
+    return n_parts == 1 ? 0 : (int)(((h >> 32) * (uint64_t)n_parts) >> 32);
 }
 
 // The SW-2 key/padding words of a slot (the tag is not touched).
@@ -113,21 +166,23 @@ __device__ __forceinline__ void copy_key(uint32_t* dst, const uint32_t* src) {
     *reinterpret_cast<uint2*>(dst + SW - 4) = *reinterpret_cast<const uint2*>(src + SW - 4);
 }
 
-// Returns the slot of a newly inserted key, -1 if already present, -2 if full.
+// Inserts into partition `pt`.  Returns the slot of a newly inserted key, -1
+// if already present, -2 if the table is full, -3 on a stall (watchdog).
 // `row` holds the key padded with guard words to SW-2 words.
-template <int SW>
-__device__ long long table_insert(const BfsArgs& a, const uint32_t* row, uint64_t h) {
+template <int SW, bool SYS>
+__device__ long long table_insert(const BfsArgs& a, const BfsPart& pt, const uint32_t* row,
+                                  uint64_t h) {
     const unsigned long long fp = h | 1ull;  // nonzero: 0 marks an empty slot
     uint64_t i = h & a.cap_mask;
     // a probe sequence this long only happens in a table that is too full: report it
     // (the sweep restarts with a larger table) instead of scanning the whole table
     for (uint64_t probe = 0; probe < 4096; ++probe, i = (i + 1) & a.cap_mask) {
-        uint32_t* sl = a.table + i * SW;
+        uint32_t* sl = pt.table + i * SW;
         uint32_t v[SW];
-        ld_line<SW>(sl, v);
+        ld_line<SW, SYS>(sl, v);
         unsigned long long t = (unsigned long long)v[SW - 2] | ((unsigned long long)v[SW - 1] << 32);
         if (t == 0) {
-            t = atomicCAS(reinterpret_cast<unsigned long long*>(sl + SW - 2), 0ull, fp);
+            t = atom_cas<SYS>(reinterpret_cast<unsigned long long*>(sl + SW - 2), 0ull, fp);
             if (t == 0) {
                 st_key<SW>(sl, row);
                 return (long long)i;
@@ -150,38 +205,69 @@ __device__ long long table_insert(const BfsArgs& a, const uint32_t* row, uint64_
             }
             // the claimer is still writing the key
             if (spins > (1u << 21)) {  // watchdog: a key that never completes
-                atomicExch(a.error, 5);
+                set_error<SYS>(pt.error, 5);
                 return -3;
             }
             __nanosleep(ns);
             if (ns < 512) ns <<= 1;
-            ld_line<SW>(sl, v);
+            ld_line<SW, SYS>(sl, v);
         }
     }
     return -2;
 }
 
-// Pushes the lanes' new slots (fresh lanes) with one queue reservation per warp.
-// Returns the number pushed (on every lane).
-__device__ __forceinline__ unsigned push_fresh(const BfsArgs& a, bool fresh, long long slot) {
+// Pushes the lanes' new slots (fresh lanes) onto their owners' queues with one
+// reservation per owner per warp.  Returns the number pushed (on every lane).
+template <bool SYS>
+__device__ __forceinline__ unsigned push_fresh(const BfsArgs& a, bool fresh, long long slot, int owner) {
     const int lane = threadIdx.x & 31;
-    const unsigned mask = __ballot_sync(0xffffffffu, fresh);
-    if (!mask) return 0;
-    const int leader = __ffs(mask) - 1;
-    const unsigned cnt = __popc(mask);
-    unsigned long long pos0 = 0;
-    if (lane == leader) {
-        pos0 = atomicAdd(a.tq, ((unsigned long long)cnt << 32) | cnt) >> 32;
-        if (pos0 + cnt > a.queue_cap) atomicExch(a.error, 2);
+    unsigned mask = __ballot_sync(0xffffffffu, fresh);
+    const unsigned total = __popc(mask);
+    while (mask) {
+        const int leader = __ffs(mask) - 1;
+        const int o = __shfl_sync(0xffffffffu, owner, leader);
+        const unsigned grp = __ballot_sync(0xffffffffu, fresh && owner == o);
+        const BfsPart& pt = a.part[o];
+        const unsigned cnt = __popc(grp);
+        unsigned long long pos0 = 0;
+        if (lane == leader) {
+            pos0 = atom_add<SYS>(pt.tq, ((unsigned long long)cnt << 32) | cnt) >> 32;
+            if (pos0 + cnt > a.queue_cap) set_error<SYS>(pt.error, 2);
+        }
+        pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+        if (grp & (1u << lane)) {
+            const unsigned long long pos = pos0 + __popc(grp & ((1u << lane) - 1));
+            // relaxed: the consumer re-reads the slot until every guard bit is set
+            if (pos < a.queue_cap) st_relaxed32<SYS>(&pt.queue[pos], (uint32_t)slot);
+        }
+        mask &= ~grp;
     }
-    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-    if (fresh) {
-        const unsigned long long pos = pos0 + __popc(mask & ((1u << lane) - 1));
-        // relaxed: the consumer re-reads the slot until every guard bit is set
-        if (pos < a.queue_cap) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&a.queue[pos]),
-                                            "r"((uint32_t)slot) : "memory");
+    return total;
+}
+
+// Any partition's error flag (read by idle and every-64th-state checks).
+template <bool SYS>
+__device__ __forceinline__ int any_error(const BfsArgs& a) {
+    int e = 0;
+    for (int p = 0; p < a.n_parts; ++p) e |= (int)ld_relaxed32<SYS>((const uint32_t*)a.part[p].error);
+    return e;
+}
+
+// Global quiescence over the partitions: every pushed state has been expanded.
+// One partition: outstanding == 0.  Several: pass 1 reads each partition's
+// expanded count (tail - outstanding), pass 2 its tail; both are monotone, so
+// equal sums mean that no state was outstanding at the end of pass 1 — and
+// only an outstanding state can push another.
+template <bool SYS>
+__device__ __forceinline__ bool quiescent(const BfsArgs& a) {
+    if (a.n_parts == 1) return (uint32_t)ld_relaxed64<SYS>(a.part[0].tq) == 0;
+    unsigned long long done = 0, tail = 0;
+    for (int p = 0; p < a.n_parts; ++p) {
+        const unsigned long long t = ld_relaxed64<SYS>(a.part[p].tq);
+        done += (t >> 32) - (t & 0xffffffffull);
     }
-    return cnt;
+    for (int p = 0; p < a.n_parts; ++p) tail += ld_relaxed64<SYS>(a.part[p].tq) >> 32;
+    return done == tail;
 }
 
 // Record writers for the in-place successors (field order of pack()): the
@@ -319,9 +405,12 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
     return v;
 }
 
-template <int SW>
+template <int SW, bool SYS>
 __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(BfsArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    // the partition this warp expands (round-robin over the launch's partitions)
+    const int mp = a.part0 + (int)(((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % a.n_here);
+    const BfsPart& me = a.part[mp];
     // per warp in shared memory: the parent (unpacked and packed) and its enabled
     // list; per lane: one packed successor row.  Only the generic transitions
     // materialise an unpacked successor in (L1-resident) local memory.
@@ -367,16 +456,16 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
         if (!local) {
             if (h_next == h_end) {
                 unsigned long long h0 = 0;
-                if (lane == 0) h0 = atomicAdd(a.head, (unsigned long long)claim);
+                if (lane == 0) h0 = atomicAdd(me.head, (unsigned long long)claim);
                 h_run = h_next = __shfl_sync(0xffffffffu, h0, 0);
                 h_end = h_next + claim;
                 // read the whole run at once and start the filled entries' slot lines
                 // on their way to L2; a later pop of a filled entry needs no poll
                 peek = lane < (int)claim && h_run + lane < a.queue_cap
-                           ? ld_relaxed32(&a.queue[h_run + lane])
+                           ? ld_relaxed32<SYS>(&me.queue[h_run + lane])
                            : kEmpty;
                 if (peek != kEmpty)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.table + (uint64_t)peek * SW));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(me.table + (uint64_t)peek * SW));
             }
             const unsigned long long h = h_next++;
             if (h >= a.queue_cap) break;
@@ -387,16 +476,14 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                 if (lane == 0) {
                     unsigned ns = 64;
                     for (unsigned it = 0;; ++it) {
-                        slot = ld_relaxed32(&a.queue[h]);  // relaxed poll: no L1 invalidation
+                        slot = ld_relaxed32<SYS>(&me.queue[h]);  // relaxed poll: no L1 invalidation
                         if (slot != kEmpty) break;
                         waited = true;
                         // the shared counters are read rarely: they are the working warps'
                         // atomics' cache line
-                        if ((it & 15) == 15 && ((uint32_t)ld_relaxed64(a.tq) == 0 ||
-                                                ld_relaxed32((const uint32_t*)a.error)))
-                            break;
+                        if ((it & 15) == 15 && (quiescent<SYS>(a) || any_error<SYS>(a))) break;
                         if (it > (1u << 23)) {  // watchdog: outstanding states never arrive
-                            atomicExch(a.error, 7);
+                            set_error<SYS>(me.error, 7);
                             break;
                         }
                         __nanosleep(ns);
@@ -410,13 +497,13 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             if (slot == kEmpty) break;
             // one coalesced line read; a word without its guard bit is still being
             // written by the slot's claimer: read again
-            const uint32_t* src = a.table + (uint64_t)slot * SW;
+            const uint32_t* src = me.table + (uint64_t)slot * SW;
             uint32_t w;
             for (unsigned spins = 0;; ++spins) {
-                w = lane < SW - 2 ? ld_relaxed32(src + lane) : kGuard;
+                w = lane < SW - 2 ? ld_relaxed32<SYS>(src + lane) : kGuard;
                 if (__all_sync(0xffffffffu, w & kGuard)) break;
                 if (spins > (1u << 22)) {  // watchdog: a pushed key that never completes
-                    if (lane == 0) atomicExch(a.error, 6);
+                    if (lane == 0) set_error<SYS>(me.error, 6);
                     break;
                 }
                 __nanosleep(64);
@@ -432,8 +519,8 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             since = 0;
         }
         if ((since++ & 63) == 0) {
-            g_states = ld_relaxed64(&a.stats[cfg].states);
-            g_err = (int)ld_relaxed32((const uint32_t*)a.error);
+            g_states = ld_relaxed64<false>(&a.stats[cfg].states);
+            g_err = any_error<SYS>(a);
         }
         const BfsDesc& d = a.descs[cfg];
         const int lognwe = __ffs(d.m.nwe) - 1;
@@ -476,7 +563,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                     atomicMax(&st.max_time, (long long)s.time);
                 } else {
                     atomicAdd(&st.deadlocks, 1ull);
-                    atomicExch(a.error, 3);
+                    set_error<SYS>(me.error, 3);
                 }
             }
         } else if (g_states + n_states >= a.cfg_cap) {
@@ -487,6 +574,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
                 long long ins = -1;
+                int owner = mp;
                 uint64_t Hc = H;
                 if (e < ne) {
                     copy_key<SW>(row, pwords);
@@ -500,20 +588,23 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                             Hc = 0;
                             for (int k = 0; k < a.words; ++k) Hc += (uint64_t)row[k] * hk[k];
                         } else {
-                            atomicExch(a.error, 3);
+                            set_error<SYS>(me.error, 3);
                         }
                     }
                     if (ok) {
-                        ins = table_insert<SW>(a, row, fmix64(Hc));
-                        if (ins == -2) atomicExch(a.error, 1);
+                        const uint64_t hh = fmix64(Hc);
+                        owner = owner_of(hh, a.n_parts);
+                        ins = table_insert<SW, SYS>(a, a.part[owner], row, hh);
+                        if (ins == -2) set_error<SYS>(me.error, 1);
                     }
                 }
                 bool fresh = ins >= 0;
                 int keeper = -1;
                 if (!kept && a.keep) {
-                    // keep the first new successor: no queue round trip on the chain; it
-                    // inherits the parent's place in `outstanding`
-                    const unsigned m = __ballot_sync(0xffffffffu, fresh);
+                    // keep the first new successor of this warp's partition: no queue
+                    // round trip on the chain; it inherits the parent's place in
+                    // `outstanding`
+                    const unsigned m = __ballot_sync(0xffffffffu, fresh && owner == mp);
                     if (m) {
                         keeper = __ffs(m) - 1;
                         if (lane == keeper) fresh = false;
@@ -522,7 +613,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                         H_kept = __shfl_sync(0xffffffffu, Hc, keeper);
                     }
                 }
-                n_states += push_fresh(a, fresh, ins);
+                n_states += push_fresh<SYS>(a, fresh, ins, owner);
                 if (keeper >= 0) {
                     __syncwarp();
                     const uint32_t* kr = pwords + (2 + keeper) * SW;
@@ -538,16 +629,17 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             H = H_kept;
             __syncwarp();
         } else if (lane == 0) {
-            atomicAdd(a.tq, ~0ull);  // this state is expanded: outstanding - 1
+            atom_add<SYS>(me.tq, ~0ull);  // this state is expanded: outstanding - 1
         }
     }
     flush();
 }
 
-template <int SW>
+template <int SW, bool SYS>
 __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
     // one initial state per configuration (explore.cpp:98-105), or the given
-    // packed states of configuration 0 (a multi-source exploration)
+    // packed states of configuration 0 (a multi-source exploration), each into
+    // its owner partition
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t key[SW];
     for (int k = 0; k < SW; ++k) key[k] = kGuard;
@@ -563,17 +655,17 @@ __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
         initial_state(d.m, s);
         pack(d, c, s, key);
     }
-    const long long ins = table_insert<SW>(a, key, fmix64(hash_full(key, a.words)));
+    const uint64_t h = fmix64(hash_full(key, a.words));
+    const BfsPart& pt = a.part[owner_of(h, a.n_parts)];
+    const long long ins = table_insert<SW, SYS>(a, pt, key, h);
     if (ins == -1) return;  // a repeated seed
     if (ins < 0) {
-        atomicExch(a.error, 1);
+        set_error<SYS>(pt.error, 1);
         return;
     }
-    const int c_ = cfg;
-    atomicAdd(&a.stats[c_].states, 1ull);
-    const unsigned long long pos = atomicAdd(a.tq, (1ull << 32) | 1ull) >> 32;
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&a.queue[pos]), "r"((uint32_t)ins)
-                 : "memory");
+    atomicAdd(&a.stats[cfg].states, 1ull);
+    const unsigned long long pos = atom_add<SYS>(pt.tq, (1ull << 32) | 1ull) >> 32;
+    st_relaxed32<SYS>(&pt.queue[pos], (uint32_t)ins);
 }
 
 }  // namespace
@@ -587,132 +679,226 @@ Layout bfs_layout(const MachDesc& m, int n_cfg) {
     return make_layout(m, n_cfg, groups * m.wg * per_item + 1);
 }
 
-int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
-            cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds) {
-    const int n_cfg = (int)hs.size();
-    std::vector<BfsDesc> descs(n_cfg);
-    int32_t* d_ids = nullptr;
-    int rc = upload_desc(hs[0], st, &d_ids);
+// Descriptors, packed layouts and field tables of a sweep (bfs_plan) — shared by
+// the single-device run (run_bfs) and the multi-GPU partitions (mctb_explore_mp_*).
+struct BfsPlan {
+    int n_cfg = 0, words = 1, sw = 16;
+    std::vector<BfsDesc> descs;
+    std::vector<uint2> ftab;
+    std::vector<int> nfields;
+    int32_t* d_ids = nullptr;  // minimum-kernel value ids (device)
+};
+
+static int bfs_plan(std::vector<MachHost>& hs, cudaStream_t st, BfsPlan* pl) {
+    pl->n_cfg = (int)hs.size();
+    pl->descs.resize(pl->n_cfg);
+    int rc = upload_desc(hs[0], st, &pl->d_ids);
     if (rc) return rc;
-    int words = 1;
-    for (int c = 0; c < n_cfg; ++c) {
+    for (int c = 0; c < pl->n_cfg; ++c) {
         MachDesc m = hs[c].d;
-        m.input_id = d_ids;
-        // time bound: every tick consumes >= 1 busy tick of some element
-        descs[c].m = m;
-        descs[c].l = bfs_layout(m, n_cfg);
-        if (descs[c].l.time > 32 || descs[c].l.words > kMaxWords) {
+        m.input_id = pl->d_ids;
+        pl->descs[c].m = m;
+        pl->descs[c].l = bfs_layout(m, pl->n_cfg);
+        if (pl->descs[c].l.time > 32 || pl->descs[c].l.words > kMaxWords) {
             set_error("state does not fit the GPU packing (time > 2^32 or > 24 words)");
-            cudaFreeAsync(d_ids, st);
+            cudaFreeAsync(pl->d_ids, st);
+            pl->d_ids = nullptr;
             return MCTB_LIMIT;
         }
-        words = std::max(words, descs[c].l.words);
+        pl->words = std::max(pl->words, pl->descs[c].l.words);
     }
     // field tables of the table-driven unpack
-    std::vector<uint2> ftab((size_t)n_cfg * kMaxFields);
-    std::vector<int> nfields(n_cfg);
-    for (int c = 0; c < n_cfg; ++c)
-        nfields[c] = build_field_table(descs[c].m, descs[c].l, ftab.data() + (size_t)c * kMaxFields);
+    pl->ftab.assign((size_t)pl->n_cfg * kMaxFields, uint2{0, 0});
+    pl->nfields.assign(pl->n_cfg, 0);
+    for (int c = 0; c < pl->n_cfg; ++c)
+        pl->nfields[c] = build_field_table(pl->descs[c].m, pl->descs[c].l,
+                                           pl->ftab.data() + (size_t)c * kMaxFields);
     // slot stride: key words + guard padding + 8-byte tag in one 64- or 128-byte line
-    const int sw = words <= 14 ? 16 : 32;
-    void (*kern)(BfsArgs) = sw == 16 ? explore_kernel<16> : explore_kernel<32>;
-    void (*seed)(BfsArgs, const uint32_t*, int) = sw == 16 ? seed_kernel<16> : seed_kernel<32>;
+    pl->sw = pl->words <= 14 ? 16 : 32;
+    return MCTB_OK;
+}
+
+using ExploreFn = void (*)(BfsArgs);
+using SeedFn = void (*)(BfsArgs, const uint32_t*, int);
+
+static ExploreFn explore_fn(int sw, bool sys) {
+    if (sw == 16) return sys ? explore_kernel<16, true> : explore_kernel<16, false>;
+    return sys ? explore_kernel<32, true> : explore_kernel<32, false>;
+}
+static SeedFn seed_fn(int sw, bool sys) {
+    if (sw == 16) return sys ? seed_kernel<16, true> : seed_kernel<16, false>;
+    return sys ? seed_kernel<32, true> : seed_kernel<32, false>;
+}
+
+// Persistent grid of the exploration kernel: blocks per SM and dynamic shared memory.
+static int bfs_grid(ExploreFn kern, int sw, int* grid, size_t* dyn_smem) {
     int dev = 0, sms = 0, per_sm = 0;
     MCTB_CUDA(cudaGetDevice(&dev));
     MCTB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t dyn_smem = (size_t)(kBfsThreads / 32) * 34 * sw * sizeof(uint32_t);
+    *dyn_smem = (size_t)(kBfsThreads / 32) * 34 * sw * sizeof(uint32_t);
     // static (parent states, enabled lists) + dynamic (rows) may exceed the 48 KB default
     MCTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)dyn_smem));
-    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBfsThreads,
-                                                            dyn_smem));
+                                   (int)*dyn_smem));
+    MCTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBfsThreads, *dyn_smem));
     if (per_sm < 1) per_sm = 1;
-    // local-memory working set: keep the resident warps' successor states L1-sized
+    // 4 blocks of 256 threads is the register-file limit at 64 registers; more
+    // resident warps (a register-capped build) spill and run slower
     if (const char* e = getenv("MCTB_BFS_BLOCKS_PER_SM")) per_sm = std::min(per_sm, atoi(e));
     else per_sm = std::min(per_sm, 4);
+    *grid = sms * per_sm;
+    return MCTB_OK;
+}
+
+// Bytes of one partition (table + queue + counters) and the counters' offset.
+static size_t part_bytes(uint64_t cap, int sw, size_t* misc_off) {
+    const size_t sz_table = cap * 4 * (size_t)sw, sz_q = (cap / 2) * 4;
+    *misc_off = sz_table + sz_q;
+    return sz_table + sz_q + 256;
+}
+
+static void part_at(char* base, uint64_t cap, int sw, BfsPart* p) {
+    size_t misc_off = 0;
+    part_bytes(cap, sw, &misc_off);
+    p->table = (uint32_t*)base;
+    p->queue = (uint32_t*)(base + cap * 4 * (size_t)sw);
+    char* misc = base + misc_off;
+    p->head = (unsigned long long*)misc;
+    p->tq = (unsigned long long*)(misc + 8);
+    p->error = (int*)(misc + 24);
+}
+
+static int part_clear(char* base, uint64_t cap, int sw, cudaStream_t st) {
+    size_t misc_off = 0;
+    part_bytes(cap, sw, &misc_off);
+    MCTB_CUDA(cudaMemsetAsync(base, 0, cap * 4 * (size_t)sw, st));
+    MCTB_CUDA(cudaMemsetAsync(base + cap * 4 * (size_t)sw, 0xff, (cap / 2) * 4, st));
+    MCTB_CUDA(cudaMemsetAsync(base + misc_off, 0, 256, st));
+    return MCTB_OK;
+}
+
+// The shared block of a launch: statistics, descriptors, field tables (+ the
+// op histogram of diagnostics).  Returns its size.
+static size_t shared_bytes(const BfsPlan& pl) {
+    return 512 + (sizeof(BfsStats) + sizeof(BfsDesc)) * pl.n_cfg + pl.ftab.size() * 8 +
+           pl.nfields.size() * 4;
+}
+
+static int shared_init(const BfsPlan& pl, char* blk, BfsArgs* a, cudaStream_t st) {
+    a->op_hist = getenv("MCTB_BFS_OPHIST") ? (unsigned long long*)(blk + 32) : nullptr;
+    a->stats = (BfsStats*)(blk + 512);
+    a->descs = (BfsDesc*)(blk + 512 + sizeof(BfsStats) * pl.n_cfg);
+    uint2* d_ftab = (uint2*)(blk + 512 + (sizeof(BfsStats) + sizeof(BfsDesc)) * pl.n_cfg);
+    a->ftab = d_ftab;
+    a->nfields = (const int*)(d_ftab + pl.ftab.size());
+    MCTB_CUDA(cudaMemsetAsync(blk, 0, 512, st));
+    MCTB_CUDA(cudaMemcpyAsync(d_ftab, pl.ftab.data(), pl.ftab.size() * 8, cudaMemcpyHostToDevice, st));
+    MCTB_CUDA(cudaMemcpyAsync(d_ftab + pl.ftab.size(), pl.nfields.data(), pl.nfields.size() * 4,
+                              cudaMemcpyHostToDevice, st));
+    std::vector<BfsStats> init(pl.n_cfg);
+    for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0, 0};
+    MCTB_CUDA(cudaMemcpyAsync(a->stats, init.data(), sizeof(BfsStats) * pl.n_cfg,
+                              cudaMemcpyHostToDevice, st));
+    MCTB_CUDA(cudaMemcpyAsync((void*)a->descs, pl.descs.data(), sizeof(BfsDesc) * pl.n_cfg,
+                              cudaMemcpyHostToDevice, st));
+    a->n_cfg = pl.n_cfg;
+    a->words = pl.words;
+    a->cfg_bits = pl.descs[0].l.cfg;
+    return MCTB_OK;
+}
+
+static int seed_launch(const BfsPlan& pl, const BfsArgs& a, bool sys, const std::vector<uint32_t>* seeds,
+                       cudaStream_t st) {
+    uint32_t* d_seeds = nullptr;
+    int n_seeds = 0;
+    if (seeds && !seeds->empty()) {
+        n_seeds = (int)(seeds->size() / pl.words);
+        MCTB_CUDA(cudaMallocAsync(&d_seeds, seeds->size() * 4, st));
+        MCTB_CUDA(cudaMemcpyAsync(d_seeds, seeds->data(), seeds->size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    const int n_first = seeds ? n_seeds : pl.n_cfg;
+    seed_fn(pl.sw, sys)<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds);
+    if (d_seeds) cudaFreeAsync(d_seeds, st);
+    MCTB_CUDA(cudaGetLastError());
+    return MCTB_OK;
+}
+
+int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
+            cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds, int n_parts,
+            bool sys_scope) {
+    if (n_parts < 1 || n_parts > kMaxParts) {
+        set_error("partitions must be in [1, 8]");
+        return MCTB_CONFIG_ERROR;
+    }
+    BfsPlan pl;
+    int rc = bfs_plan(hs, st, &pl);
+    if (rc) return rc;
+    const int n_cfg = pl.n_cfg, sw = pl.sw;
+    const ExploreFn kern = explore_fn(sw, sys_scope);
+    int grid = 0;
+    size_t dyn_smem = 0;
+    if ((rc = bfs_grid(kern, sw, &grid, &dyn_smem))) return rc;
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double slot_bytes = 4.0 * sw + 2.0;  // slot line + queue (half the slots)
     // capacity grows 8x on overflow; the sweep restarts (all counts are rebuilt)
     // first capacity: enough for the bound up to 2^28 slots (a restart loses the
-    // work done, so large sweeps start large); then 8x per overflow
+    // work done, so large sweeps start large); then 8x per overflow.  Split over
+    // the partitions (each holds ~1/P of the states).
     uint64_t cap = 1ull << 20;
     while (cap < 2 * std::min<uint64_t>(max_states, 1ull << 27)) cap <<= 1;
     const uint64_t cap_limit = [&] {
         uint64_t c = 1024;
-        while ((double)(c * 2) * slot_bytes < 0.8 * (double)free_b) c <<= 1;
+        while ((double)(c * 2) * slot_bytes * n_parts < 0.8 * (double)free_b) c <<= 1;
         return c;
     }();
+    if (n_parts > 1) {
+        uint64_t c = 1ull << 16;
+        while (c * n_parts < cap) c <<= 1;
+        cap = c;
+    }
     cap = std::min(cap, cap_limit);
+    const bool trace = getenv("MCTB_BFS_TRACE") != nullptr;
     for (;;) {
-        const uint64_t qcap = cap / 2;
         BfsArgs a{};
-        a.n_cfg = n_cfg;
-        a.words = words;
-        a.cfg_bits = descs[0].l.cfg;
         a.cap_mask = cap - 1;
-        a.queue_cap = qcap;
+        a.queue_cap = cap / 2;
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
         a.check_inv = check_invariants ? 1 : 0;
-        const size_t sz_table = cap * 4 * (size_t)sw, sz_q = qcap * 4;
-        const size_t sz_ftab = ftab.size() * 8 + nfields.size() * 4;
-        const size_t sz_misc = 512 + sizeof(BfsStats) * n_cfg + sizeof(BfsDesc) * n_cfg + sz_ftab;
+        a.n_parts = n_parts;
+        a.part0 = 0;
+        a.n_here = n_parts;
+        size_t misc_off = 0;
+        const size_t pb = (part_bytes(cap, sw, &misc_off) + 255) & ~(size_t)255;
         void* blob = nullptr;
-        MCTB_CUDA(cudaMallocAsync(&blob, sz_table + sz_q + sz_misc, st));
+        MCTB_CUDA(cudaMallocAsync(&blob, pb * n_parts + shared_bytes(pl), st));
         char* b = (char*)blob;
-        a.table = (uint32_t*)b;
-        a.queue = (uint32_t*)(b + sz_table);
-        char* misc = b + sz_table + sz_q;
-        a.head = (unsigned long long*)misc;
-        a.tq = (unsigned long long*)(misc + 8);
-        a.error = (int*)(misc + 24);
-        a.op_hist = getenv("MCTB_BFS_OPHIST") ? (unsigned long long*)(misc + 32) : nullptr;
-        a.stats = (BfsStats*)(misc + 512);
-        a.descs = (BfsDesc*)(misc + 512 + sizeof(BfsStats) * n_cfg);
-        uint2* d_ftab = (uint2*)(misc + 512 + (sizeof(BfsStats) + sizeof(BfsDesc)) * n_cfg);
-        a.ftab = d_ftab;
-        a.nfields = (const int*)(d_ftab + ftab.size());
-        MCTB_CUDA(cudaMemcpyAsync(d_ftab, ftab.data(), ftab.size() * 8, cudaMemcpyHostToDevice, st));
-        MCTB_CUDA(cudaMemcpyAsync(d_ftab + ftab.size(), nfields.data(), nfields.size() * 4,
-                                  cudaMemcpyHostToDevice, st));
-        MCTB_CUDA(cudaMemsetAsync(a.table, 0, sz_table, st));
-        MCTB_CUDA(cudaMemsetAsync(a.queue, 0xff, sz_q, st));
-        MCTB_CUDA(cudaMemsetAsync(misc, 0, 512, st));
-        std::vector<BfsStats> init(n_cfg);
-        for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0, 0};
-        MCTB_CUDA(cudaMemcpyAsync(a.stats, init.data(), sizeof(BfsStats) * n_cfg,
-                                  cudaMemcpyHostToDevice, st));
-        MCTB_CUDA(cudaMemcpyAsync((void*)a.descs, descs.data(), sizeof(BfsDesc) * n_cfg,
-                                  cudaMemcpyHostToDevice, st));
-        uint32_t* d_seeds = nullptr;
-        int n_seeds = 0;
-        if (seeds && !seeds->empty()) {
-            n_seeds = (int)(seeds->size() / words);
-            MCTB_CUDA(cudaMallocAsync(&d_seeds, seeds->size() * 4, st));
-            MCTB_CUDA(cudaMemcpyAsync(d_seeds, seeds->data(), seeds->size() * 4,
-                                      cudaMemcpyHostToDevice, st));
+        for (int p = 0; p < n_parts; ++p) {
+            part_at(b + pb * p, cap, sw, &a.part[p]);
+            if ((rc = part_clear(b + pb * p, cap, sw, st))) return rc;
         }
-        const int n_first = seeds ? n_seeds : n_cfg;
-        seed<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds);
-        if (d_seeds) cudaFreeAsync(d_seeds, st);
-        MCTB_CUDA(cudaGetLastError());
+        if ((rc = shared_init(pl, b + pb * n_parts, &a, st))) return rc;
+        if ((rc = seed_launch(pl, a, sys_scope, seeds, st))) return rc;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
-        const bool trace = getenv("MCTB_BFS_TRACE") != nullptr;
         if (trace)
-            fprintf(stderr, "[bfs] launch cfgs=%d words=%d sw=%d cap=%llu grid=%d smem=%zu\n", n_cfg,
-                    words, sw, (unsigned long long)cap, sms * per_sm, dyn_smem);
-        kern<<<sms * per_sm, kBfsThreads, dyn_smem, st>>>(a);
+            fprintf(stderr, "[bfs] launch cfgs=%d words=%d sw=%d parts=%d cap=%llu grid=%d smem=%zu\n",
+                    n_cfg, pl.words, sw, n_parts, (unsigned long long)cap, grid, dyn_smem);
+        kern<<<grid, kBfsThreads, dyn_smem, st>>>(a);
         cudaEventRecord(e1, st);
         MCTB_CUDA(cudaGetLastError());
         res->stats.resize(n_cfg);
-        unsigned long long misc_h[32];
+        std::vector<unsigned long long> misc_h(32 * n_parts);
         MCTB_CUDA(cudaMemcpyAsync(res->stats.data(), a.stats, sizeof(BfsStats) * n_cfg,
                                   cudaMemcpyDeviceToHost, st));
-        MCTB_CUDA(cudaMemcpyAsync(misc_h, misc, 256, cudaMemcpyDeviceToHost, st));
+        for (int p = 0; p < n_parts; ++p)
+            MCTB_CUDA(cudaMemcpyAsync(misc_h.data() + 32 * p, b + pb * p + misc_off, 256,
+                                      cudaMemcpyDeviceToHost, st));
+        unsigned long long hist[32] = {};
+        if (a.op_hist)
+            MCTB_CUDA(cudaMemcpyAsync(hist, b + pb * n_parts, 256, cudaMemcpyDeviceToHost, st));
         MCTB_CUDA(cudaStreamSynchronize(st));
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
@@ -723,10 +909,14 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         res->states = 0;
         for (const auto& x : res->stats) res->states += x.states;
         res->levels = 0;
-        res->error = (int)(misc_h[3] & 0xffffffff);
+        res->error = 0;
+        for (int p = 0; p < n_parts; ++p)
+            res->error = std::max(res->error, (int)(misc_h[32 * p + 3] & 0xffffffff));
         if (trace)
-            fprintf(stderr, "[bfs] done %.3f ms error=%d head=%llu tail=%llu outstanding=%llu\n", ms,
-                    res->error, misc_h[0], misc_h[1] >> 32, misc_h[1] & 0xffffffffull);
+            for (int p = 0; p < n_parts; ++p)
+                fprintf(stderr, "[bfs] part %d: %.3f ms error=%d head=%llu tail=%llu outstanding=%llu\n",
+                        p, ms, (int)(misc_h[32 * p + 3] & 0xffffffff), misc_h[32 * p],
+                        misc_h[32 * p + 1] >> 32, misc_h[32 * p + 1] & 0xffffffffull);
         if (res->error >= 5) {
             // a watchdog fired (bfs.cu spin loops): report instead of hanging
             char msg[256];
@@ -735,7 +925,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
                      res->error, misc_h[0], misc_h[1] >> 32, misc_h[1] & 0xffffffffull);
             fprintf(stderr, "[mctb] %s\n", msg);
             set_error(msg);
-            cudaFreeAsync(d_ids, st);
+            cudaFreeAsync(pl.d_ids, st);
             cudaStreamSynchronize(st);
             return MCTB_MODEL_BUG;
         }
@@ -744,21 +934,21 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         // flushed per warp, so the final count decides)
         for (auto& x : res->stats)
             if (x.states >= cfg_cap) x.capped = 1;
-        if (getenv("MCTB_BFS_OPHIST")) {
+        if (a.op_hist) {
             fprintf(stderr, "[explore] generic successors by op:");
             for (int o = 0; o < 19; ++o)
-                if (misc_h[4 + o]) fprintf(stderr, " op%d=%llu", o, misc_h[4 + o]);
+                if (hist[4 + o]) fprintf(stderr, " op%d=%llu", o, hist[4 + o]);
             fprintf(stderr, "\n");
         }
-        res->words = words;
-        res->capacity = cap;
+        res->words = pl.words;
+        res->capacity = cap * n_parts;
         if ((res->error == 1 || res->error == 2) && cap < cap_limit) {
             cap = std::min(cap * 8, cap_limit);
             continue;
         }
         break;
     }
-    cudaFreeAsync(d_ids, st);
+    cudaFreeAsync(pl.d_ids, st);
     MCTB_CUDA(cudaStreamSynchronize(st));
     return MCTB_OK;
 }
@@ -792,7 +982,11 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     BfsResult r;
     const uint64_t cap = max_states > 0 ? (uint64_t)max_states : 5000000ull;
-    rc = run_bfs(hs, cap * (uint64_t)n_configs, cap, &r, st, (flags & 1) != 0);
+    // flags: bit 0 invariants; bits 8-11 hash partitions on this device (0 = 1);
+    // bit 1 system-scope memory operations (the multi-GPU kernel variant)
+    const int n_parts = std::max(1, (flags >> 8) & 15);
+    rc = run_bfs(hs, cap * (uint64_t)n_configs, cap, &r, st, (flags & 1) != 0, nullptr, n_parts,
+                 (flags & 2) != 0);
     cudaStreamDestroy(st);
     if (rc) return rc;
     if (r.error == 3) {

@@ -39,13 +39,21 @@ class SweepInfo:
 
 def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
                     configs: Sequence[TuningParams], max_states: int = 5_000_000,
-                    info: list | None = None, check_invariants: bool = False) -> List[ExploreStats]:
+                    info: list | None = None, check_invariants: bool = False,
+                    partitions: int = 1, system_scope: bool = False) -> List[ExploreStats]:
+    """partitions > 1 splits the visited set into hash partitions on this device:
+    the successor exchange of the multi-GPU sweep, run on one GPU (same kernel,
+    same results); system_scope selects the multi-GPU kernel variant."""
+    if not 1 <= partitions <= 8:
+        from ._lib import ConfigError
+        raise ConfigError("partitions must be in [1, 8]")
     cfg = i32arr([v for c in configs for v in (c.wg, c.ts)])
     out = (C.c_int64 * (9 * len(configs)))()
     inf = (C.c_int64 * 4)()
     check(lib.mctb_explore(platform.as_array(), problem.size, problem.kernel,
                            problem.input_array(), cfg, len(configs), max_states,
-                           1 if check_invariants else 0, out, inf))
+                           (1 if check_invariants else 0) | (2 if system_scope else 0)
+                           | (partitions << 8 if partitions > 1 else 0), out, inf))
     if info is not None:
         info.append(SweepInfo(*inf))
     return [ExploreStats(bool(out[9 * i]), *out[9 * i + 1:9 * i + 9]) for i in range(len(configs))]
