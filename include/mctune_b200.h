@@ -141,6 +141,26 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
                  const int32_t* configs, int n_configs, int64_t max_states, int flags,
                  int64_t* out, int64_t* info);
 
+/* Multi-GPU explore_machine: one process per GPU (rank r of world <= 8), each
+ * owning the hash partition r of the visited set; successors owned by another
+ * rank are probed, claimed and queued in that rank's table over peer memory
+ * (NVLink P2P through CUDA IPC handles).  Protocol, every rank:
+ *   open (exports this rank's 64-byte IPC handle) -> all-gather the handles ->
+ *   connect -> barrier -> rank 0 only: seed -> barrier -> run -> barrier -> close.
+ * run's out = int64[8 * n]: this rank's share per configuration {states discovered,
+ * transitions applied, terminal states, min_final_time (INT64_MAX none),
+ * max_final_time (-1 none), deadlocks, invariant_violations, protocol transitions
+ * (max_depth_reached = this + max final time)} — sum / min / max over ranks;
+ * info = int64[4]: {total table slots, packed key words, kernel microseconds, error}.
+ * flags bit 0 = check invariants.  max_states as mctb_explore. */
+int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* input,
+                         const int32_t* configs, int n_configs, int64_t max_states, int world,
+                         int rank, int flags, void** ctx, void* handle);
+int mctb_explore_mp_connect(void* ctx, const void* handles);
+int mctb_explore_mp_seed(void* ctx);
+int mctb_explore_mp_run(void* ctx, int64_t* out, int64_t* info);
+void mctb_explore_mp_close(void* ctx);
+
 /* check_overtime (explore.hpp:279-284), exact mode.
  * out = int64[12]: {violated, exhaustive, states_visited, max_depth_reached,
  *                   transitions_applied, configs_explored, configs_skipped, final_time, wg,

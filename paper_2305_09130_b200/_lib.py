@@ -113,3 +113,12 @@ EXPORTED += ["mctb_check_overtime", "mctb_tune"]
 lib.mctb_swarm.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int64, C.c_int, C.c_uint64,
                            C.c_int64, i64p, i32p, C.c_int64, i64p, i64p, C.c_int64, i64p]
 EXPORTED.append("mctb_swarm")
+lib.mctb_explore_mp_open.argtypes = [i32p, C.c_int, C.c_int, i64p, i32p, C.c_int, C.c_int64,
+                                     C.c_int, C.c_int, C.c_int, C.POINTER(vp), C.c_char_p]
+lib.mctb_explore_mp_connect.argtypes = [vp, C.c_char_p]
+lib.mctb_explore_mp_seed.argtypes = [vp]
+lib.mctb_explore_mp_run.argtypes = [vp, i64p, i64p]
+lib.mctb_explore_mp_close.argtypes = [vp]
+lib.mctb_explore_mp_close.restype = None
+EXPORTED += ["mctb_explore_mp_open", "mctb_explore_mp_connect", "mctb_explore_mp_seed",
+             "mctb_explore_mp_run", "mctb_explore_mp_close"]

@@ -955,6 +955,30 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
 
 }  // namespace mctb
 
+namespace mctb {
+
+// One rank's share of a multi-GPU exploration (mctb_explore_mp_*): its hash
+// partition (cudaMalloc'd so it can be exported over CUDA IPC), the peers'
+// partitions mapped into this process, and the launch state.
+struct MpCtx {
+    int world = 1, rank = 0;
+    std::vector<MachHost> hs;
+    BfsPlan pl;
+    uint64_t cap = 0, cfg_cap = 0;
+    size_t pb = 0, misc_off = 0;
+    char* local = nullptr;
+    char* shared = nullptr;
+    char* peer[kMaxParts] = {};
+    BfsArgs a{};
+    cudaStream_t st = nullptr;
+    int grid = 0;
+    size_t smem = 0;
+    int n_cfg = 0, size = 0, kernel = 0, plat[4] = {};
+    std::vector<int32_t> configs;
+};
+
+}  // namespace mctb
+
 using namespace mctb;
 
 namespace mctb {
@@ -1029,6 +1053,173 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
         info[3] = (int64_t)(r.ms * 1000.0);
     }
     return MCTB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU exploration: one process per GPU, each owning one hash partition of
+// the visited set.  A successor owned by another rank is probed, claimed and
+// queued directly in that rank's table and queue over peer memory (NVLink P2P,
+// system-scope atomics); the sweep ends at global quiescence (quiescent()).
+
+int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* input,
+                         const int32_t* configs, int n_configs, int64_t max_states, int world,
+                         int rank, int flags, void** ctx, void* handle) {
+    int rc;
+    if (world < 1 || world > kMaxParts || rank < 0 || rank >= world) {
+        set_error("world must be in [1, 8] and rank in [0, world)");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (n_configs < 1) {
+        set_error("no configurations");
+        return MCTB_CONFIG_ERROR;
+    }
+    auto* c = new MpCtx;
+    c->world = world;
+    c->rank = rank;
+    c->n_cfg = n_configs;
+    c->size = size;
+    c->kernel = kernel;
+    for (int i = 0; i < 4; ++i) c->plat[i] = plat[i];
+    c->configs.assign(configs, configs + 2 * n_configs);
+    c->hs.resize(n_configs);
+    auto fail = [&](int code) {
+        delete c;
+        return code;
+    };
+    for (int k = 0; k < n_configs; ++k) {
+        if ((rc = check_machine(plat, size, kernel, configs[2 * k], configs[2 * k + 1]))) return fail(rc);
+        if ((rc = build_desc(plat, size, kernel, input, configs[2 * k], configs[2 * k + 1], &c->hs[k])))
+            return fail(rc);
+    }
+    if ((rc = require_device())) return fail(rc);
+    MCTB_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    if ((rc = bfs_plan(c->hs, c->st, &c->pl))) return fail(rc);
+    if ((rc = bfs_grid(explore_fn(c->pl.sw, true), c->pl.sw, &c->grid, &c->smem))) return fail(rc);
+    c->cfg_cap = max_states > 0 ? (uint64_t)max_states : 5000000ull;
+    // each partition holds ~1/world of the states, table load <= 1/2
+    const uint64_t total = c->cfg_cap * (uint64_t)n_configs;
+    uint64_t cap = 1ull << 16;
+    while (cap * world < 2 * std::min<uint64_t>(total, 1ull << 28)) cap <<= 1;
+    if (const char* e = getenv("MCTB_MP_CAP_LOG2")) cap = 1ull << atoi(e);
+    c->cap = cap;
+    c->pb = (part_bytes(cap, c->pl.sw, &c->misc_off) + 255) & ~(size_t)255;
+    MCTB_CUDA(cudaMalloc(&c->local, c->pb));
+    if ((rc = part_clear(c->local, cap, c->pl.sw, c->st))) return fail(rc);
+    MCTB_CUDA(cudaMalloc(&c->shared, shared_bytes(c->pl)));
+    BfsArgs& a = c->a;
+    if ((rc = shared_init(c->pl, c->shared, &a, c->st))) return fail(rc);
+    a.cap_mask = cap - 1;
+    a.queue_cap = cap / 2;
+    a.cfg_cap = c->cfg_cap;
+    a.keep = 1;
+    a.check_inv = (flags & 1) ? 1 : 0;
+    a.n_parts = world;
+    a.part0 = rank;
+    a.n_here = 1;
+    part_at(c->local, cap, c->pl.sw, &a.part[rank]);
+    MCTB_CUDA(cudaStreamSynchronize(c->st));
+    MCTB_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), c->local));
+    *ctx = c;
+    return MCTB_OK;
+}
+
+int mctb_explore_mp_connect(void* ctx, const void* handles) {
+    auto* c = static_cast<MpCtx*>(ctx);
+    const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        void* p = nullptr;
+        MCTB_CUDA(cudaIpcOpenMemHandle(&p, h[r], cudaIpcMemLazyEnablePeerAccess));
+        c->peer[r] = static_cast<char*>(p);
+        part_at(c->peer[r], c->cap, c->pl.sw, &c->a.part[r]);
+    }
+    return MCTB_OK;
+}
+
+int mctb_explore_mp_seed(void* ctx) {
+    auto* c = static_cast<MpCtx*>(ctx);
+    int rc = seed_launch(c->pl, c->a, true, nullptr, c->st);
+    if (rc) return rc;
+    MCTB_CUDA(cudaStreamSynchronize(c->st));
+    return MCTB_OK;
+}
+
+int mctb_explore_mp_run(void* ctx, int64_t* out, int64_t* info) {
+    auto* c = static_cast<MpCtx*>(ctx);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->st);
+    explore_fn(c->pl.sw, true)<<<c->grid, kBfsThreads, c->smem, c->st>>>(c->a);
+    cudaEventRecord(e1, c->st);
+    MCTB_CUDA(cudaGetLastError());
+    std::vector<BfsStats> stats(c->n_cfg);
+    unsigned long long misc_h[32];
+    MCTB_CUDA(cudaMemcpyAsync(stats.data(), c->a.stats, sizeof(BfsStats) * c->n_cfg,
+                              cudaMemcpyDeviceToHost, c->st));
+    MCTB_CUDA(cudaMemcpyAsync(misc_h, c->local + c->misc_off, 256, cudaMemcpyDeviceToHost, c->st));
+    MCTB_CUDA(cudaStreamSynchronize(c->st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const int err = (int)(misc_h[3] & 0xffffffff);
+    int logn = 0, lp = 0;
+    while ((1 << logn) < c->size) ++logn;
+    while ((1 << lp) < c->plat[2]) ++lp;
+    for (int k = 0; k < c->n_cfg; ++k) {
+        const BfsStats& s = stats[k];
+        int lw = 0, lt = 0;
+        while ((1 << lw) < c->configs[2 * k]) ++lw;
+        while ((1 << lt) < c->configs[2 * k + 1]) ++lt;
+        const Cost cm = lockstep_cost(c->kernel, logn, c->plat[3],
+                                      Config{c->plat[0], c->plat[1], lp, lw, lt});
+        int64_t* o = out + 8 * k;
+        // this rank's share: states it discovered, transitions and terminals of the
+        // states it expanded; the caller sums (min/max for the times) over ranks
+        o[0] = (int64_t)s.states;
+        o[1] = (int64_t)s.transitions;
+        o[2] = (int64_t)s.terminals;
+        o[3] = s.terminals ? s.min_time : INT64_MAX;
+        o[4] = s.terminals ? s.max_time : -1;
+        o[5] = (int64_t)s.deadlocks;
+        o[6] = (int64_t)s.violations;
+        o[7] = cm.steps - cm.time;  // protocol transitions: max depth = this + max time
+    }
+    if (info) {
+        info[0] = (int64_t)(c->cap * c->world);
+        info[1] = c->pl.words;
+        info[2] = (int64_t)(ms * 1000.0);
+        info[3] = err;
+    }
+    if (err == 3) {
+        set_error("model bug: deadlock or inapplicable transition during exploration");
+        return MCTB_MODEL_BUG;
+    }
+    if (err >= 5) {
+        set_error("exploration stalled (watchdog)");
+        return MCTB_MODEL_BUG;
+    }
+    if (err) {
+        set_error("a partition's visited table or queue is full (raise max_states)");
+        return MCTB_LIMIT;
+    }
+    return MCTB_OK;
+}
+
+void mctb_explore_mp_close(void* ctx) {
+    auto* c = static_cast<MpCtx*>(ctx);
+    if (!c) return;
+    for (int r = 0; r < c->world; ++r)
+        if (c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
+    if (c->local) cudaFree(c->local);
+    if (c->shared) cudaFree(c->shared);
+    if (c->pl.d_ids) cudaFreeAsync(c->pl.d_ids, c->st);
+    if (c->st) {
+        cudaStreamSynchronize(c->st);
+        cudaStreamDestroy(c->st);
+    }
+    delete c;
 }
 
 }  // extern "C"

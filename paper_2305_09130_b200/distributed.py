@@ -11,6 +11,12 @@
 
 The evaluators are injected so the same exchange logic runs over NCCL with
 the GPU kernels and over gloo with CPU checkers in tests/test_distributed.py.
+
+* `explore_multi_gpu`: the GPU sweep across ranks.  Each rank's exploration
+  kernel owns one hash partition of the visited set and inserts successors
+  owned by other ranks directly into their tables and queues over peer memory
+  (NVLink, CUDA IPC handles exchanged here); there is no host round trip per
+  frontier.  The host only exchanges the handles and reduces the statistics.
 """
 from __future__ import annotations
 
@@ -102,3 +108,64 @@ def partitioned_explore(initial: Iterable[Tuple[int, Hashable]],
     if world > 1:
         dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
     return len(visited), int(total.item())
+
+
+def explore_multi_gpu(platform, problem, configs, max_states: int = 5_000_000,
+                      check_invariants: bool = False, group=None):
+    """explore_configs over all ranks of the process group (one GPU per rank): the
+    same ExploreStats on every rank.  Rank r's device must be the current CUDA
+    device (torch.cuda.set_device(local_rank))."""
+    import ctypes as C
+
+    from ._lib import check, i32arr, lib
+    from .explore import ExploreStats, SweepInfo
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    n = len(configs)
+    cfg = i32arr([v for c in configs for v in (c.wg, c.ts)])
+    ctx = C.c_void_p()
+    handle = C.create_string_buffer(64)
+    check(lib.mctb_explore_mp_open(platform.as_array(), problem.size, problem.kernel,
+                                   problem.input_array(), cfg, n, max_states, world, rank,
+                                   1 if check_invariants else 0, C.byref(ctx), handle))
+    try:
+        handles = [bytes(handle.raw)]
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(handle.raw), group=group)
+        check(lib.mctb_explore_mp_connect(ctx, b"".join(handles)))
+        if world > 1:
+            dist.barrier(group=group)
+        if rank == 0:
+            check(lib.mctb_explore_mp_seed(ctx))
+        if world > 1:
+            dist.barrier(group=group)
+        out = (C.c_int64 * (8 * n))()
+        info = (C.c_int64 * 4)()
+        rc = lib.mctb_explore_mp_run(ctx, out, info)
+        mine = (rc, list(out), list(info))
+        parts = [mine]
+        if world > 1:
+            parts = [None] * world
+            dist.all_gather_object(parts, mine, group=group)
+            dist.barrier(group=group)  # no rank unmaps memory a peer's kernel still reads
+    finally:
+        lib.mctb_explore_mp_close(ctx)
+    for rc_r, _, _ in parts:
+        check(rc_r)
+    res = []
+    for k in range(n):
+        rows = [p[1][8 * k:8 * k + 8] for p in parts]
+        states = sum(r[0] for r in rows)
+        terminals = sum(r[2] for r in rows)
+        mn = min(r[3] for r in rows)
+        mx = max(r[4] for r in rows)
+        complete = states < max_states
+        res.append(ExploreStats(
+            complete, min(states, max_states), sum(r[1] for r in rows),
+            rows[0][7] + mx if terminals else -1, mn if terminals else -1,
+            mx if terminals else -1, terminals, sum(r[5] for r in rows), sum(r[6] for r in rows)))
+    kern_us = max(p[2][2] for p in parts)
+    return res, SweepInfo(parts[0][2][0], sum(r.states_visited for r in res), parts[0][2][1],
+                          kern_us)

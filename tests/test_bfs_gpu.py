@@ -94,3 +94,58 @@ def test_acceptance_6_minimum_kernel_trend(engine):
     b64 = max_wg_among_best(m.exhaustive_sweep(p, m.ProblemSpec.minimum(64)))
     tuned = m.tune(p, m.ProblemSpec.minimum(16))
     assert tuned.params.wg == b16 == 8 and b16 <= b64
+
+
+@pytest.mark.parametrize("parts,system_scope", [(2, False), (3, False), (8, False), (2, True)])
+def test_partitioned_exchange_equals_reference(engine, gold, parts, system_scope):
+    """The hash-partitioned sweep (the multi-GPU successor exchange, P partitions on
+    one device; system_scope = the multi-GPU kernel variant) reproduces every golden
+    exploration exactly, including states, transitions and max depth."""
+    m = engine
+    groups = {}
+    for c in gold("explore.json"):
+        groups.setdefault((tuple(c["plat"]), c["size"], c["kernel"]), []).append(c)
+    for (plat, size, kernel), cases in groups.items():
+        cfgs = [m.TuningParams(c["wg"], c["ts"]) for c in cases]
+        got = m.explore_configs(m.PlatformConfig(*plat), problem(m, size, kernel), cfgs,
+                                partitions=parts, system_scope=system_scope)
+        for c, g in zip(cases, got):
+            key = (plat, size, kernel, c["wg"], c["ts"], parts)
+            assert g.complete and g.deadlocks == 0, key
+            assert (g.states_visited, g.transitions_applied, g.max_depth_reached) == (
+                c["states"], c["transitions"], c["max_depth"]), key
+            assert (g.min_time, g.max_time, g.terminals) == (
+                c["min_time"], c["max_time"], c["n_terminal"]), key
+
+
+def test_partitioned_large_space_equals_single(engine):
+    """5.6e7 states split over 4 partitions: the same counts as one partition."""
+    m = engine
+    args = (m.PlatformConfig(1, 1, 16, 4), m.ProblemSpec.abstract(32), [m.TuningParams(16, 2)])
+    one = m.explore_configs(*args, max_states=100_000_000)[0]
+    four = m.explore_configs(*args, max_states=100_000_000, partitions=4)[0]
+    assert one.complete and one.states_visited == 56088395
+    assert four == one
+
+
+def test_multi_gpu_api_one_rank_equals_reference(engine, gold):
+    """mctb_explore_mp_* (open / connect / seed / run / close, system-scope kernel)
+    as one rank: the golden explorations exactly.  With more ranks the same kernel
+    inserts into the peers' partitions over NVLink (covered on one device by
+    test_partitioned_exchange_equals_reference)."""
+    m = engine
+    from paper_2305_09130_b200.distributed import explore_multi_gpu
+    groups = {}
+    for c in gold("explore.json"):
+        groups.setdefault((tuple(c["plat"]), c["size"], c["kernel"]), []).append(c)
+    for (plat, size, kernel), cases in list(groups.items())[:6]:
+        cfgs = [m.TuningParams(c["wg"], c["ts"]) for c in cases]
+        got, info = explore_multi_gpu(m.PlatformConfig(*plat), problem(m, size, kernel), cfgs)
+        assert info.states == sum(c["states"] for c in cases)
+        for c, g in zip(cases, got):
+            key = (plat, size, kernel, c["wg"], c["ts"])
+            assert g.complete and g.deadlocks == 0, key
+            assert (g.states_visited, g.transitions_applied, g.max_depth_reached) == (
+                c["states"], c["transitions"], c["max_depth"]), key
+            assert (g.min_time, g.max_time, g.terminals) == (
+                c["min_time"], c["max_time"], c["n_terminal"]), key
