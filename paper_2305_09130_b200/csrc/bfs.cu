@@ -179,8 +179,11 @@ __device__ long long table_insert(const BfsArgs& a, const BfsPart& pt, const uin
     for (uint64_t probe = 0; probe < 4096; ++probe, i = (i + 1) & a.cap_mask) {
         uint32_t* sl = pt.table + i * SW;
         uint32_t v[SW];
+        unsigned long long t;
+        // one line read: tag and key arrive together (claiming with a CAS issued
+        // alongside every read was measured 2.4x slower on wide spaces)
         ld_line<SW, SYS>(sl, v);
-        unsigned long long t = (unsigned long long)v[SW - 2] | ((unsigned long long)v[SW - 1] << 32);
+        t = (unsigned long long)v[SW - 2] | ((unsigned long long)v[SW - 1] << 32);
         if (t == 0) {
             t = atom_cas<SYS>(reinterpret_cast<unsigned long long*>(sl + SW - 2), 0ull, fp);
             if (t == 0) {
@@ -824,7 +827,7 @@ static int seed_launch(const BfsPlan& pl, const BfsArgs& a, bool sys, const std:
 
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds, int n_parts,
-            bool sys_scope) {
+            bool sys_scope, uint64_t first_cap) {
     if (n_parts < 1 || n_parts > kMaxParts) {
         set_error("partitions must be in [1, 8]");
         return MCTB_CONFIG_ERROR;
@@ -846,6 +849,10 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     // the partitions (each holds ~1/P of the states).
     uint64_t cap = 1ull << 20;
     while (cap < 2 * std::min<uint64_t>(max_states, 1ull << 27)) cap <<= 1;
+    // callers whose bound is loose (the tune sweeps: the reference's per-machine
+    // cap times the configurations) start small: a fresh multi-GB table costs
+    // more to map than the sweep takes
+    if (first_cap) cap = std::min(cap, first_cap);
     const uint64_t cap_limit = [&] {
         uint64_t c = 1024;
         while ((double)(c * 2) * slot_bytes * n_parts < 0.8 * (double)free_b) c <<= 1;

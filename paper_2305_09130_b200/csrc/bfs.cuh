@@ -33,13 +33,15 @@ struct BfsResult {
 // (ExploreLimits::max_states, explore.hpp:227-233).
 // seeds (optional): packed states of configuration 0 (layout bfs_layout(hs[0].d, 1))
 // to start from instead of the initial states — a multi-source exploration.
+// first_cap (0 = sized for max_states) bounds the first table; it grows 8x
+// (restarting the sweep) on overflow.
 // n_parts > 1 splits the visited set into hash partitions on this device (the
 // multi-GPU exchange path, exercised on one GPU); sys_scope selects the
 // system-scope memory operations of the multi-GPU kernel.
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants = false,
             const std::vector<uint32_t>* seeds = nullptr, int n_parts = 1,
-            bool sys_scope = false);
+            bool sys_scope = false, uint64_t first_cap = 0);
 
 // The packed layout the exploration uses for a configuration among n_cfg.
 Layout bfs_layout(const MachDesc& m, int n_cfg);

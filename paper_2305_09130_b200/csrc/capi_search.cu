@@ -83,7 +83,7 @@ int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
         BfsResult r;
         cudaStream_t st;
         MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib);
+        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib, 1, false, 1ull << 23);
         cudaStreamDestroy(st);
         if (rc) return rc;
         if (r.error) {
@@ -167,7 +167,8 @@ int prepare(Ctx& c, int64_t max_states) {
     // every interleaving of every configuration, one sweep.  The first DFS paths
     // (needed only for the configurations a probe finds violating) run lazily.
     const double t1 = now_ms();
-    rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st);
+    rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st, false, nullptr, 1,
+                 false, 1ull << 23);
     c.ms_bfs = now_ms() - t1;
     cudaStreamDestroy(st);
     if (rc) return rc;
