@@ -386,7 +386,12 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
     # ~10^8 states with the visited-state hash table in HBM)
     import torch
     plat16 = m.PlatformConfig(1, 1, 16, 4)
-    m.explore_configs(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(16), [m.TuningParams(4, 2)])  # warm
+    # one warm-up sweep of the same workload: the first call in a process maps the
+    # table's HBM into the stream-ordered pool (reported as cold_api_seconds)
+    t0 = time.perf_counter()
+    m.explore_configs(plat16, m.ProblemSpec.abstract(EXPLORE_SIZE),
+                      [m.TuningParams(*EXPLORE_PARAMS)], max_states=400_000_000)
+    cold = time.perf_counter() - t0
     info = []
     t0 = time.perf_counter()
     x = m.explore_configs(plat16, m.ProblemSpec.abstract(EXPLORE_SIZE),
@@ -408,6 +413,7 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
                       f"(wg,ts)={EXPLORE_PARAMS}: every interleaving",
           "states": x.states_visited, "transitions": x.transitions_applied,
           "complete": x.complete, "kernel_ms": kern_s * 1e3, "api_seconds": wall,
+          "cold_api_seconds": cold,
           "states_per_s": rate, "states_per_s_api": x.states_visited / wall,
           "key_words": words, "slot_bytes": line_bytes, "table_slots": info[0].table_slots,
           "roofline": {
