@@ -489,8 +489,8 @@ INT_OPS_PER_CONFIG = 27.9
 # re-measured after every change of explore_kernel (profiles/).
 EXPLORE_SIZE = 64
 EXPLORE_PARAMS = (16, 2)
-EXPLORE_INST_PER_STATE = 1116.0
-EXPLORE_DRAM_BYTES_PER_STATE = 1193.0
+EXPLORE_INST_PER_STATE = 1121.5
+EXPLORE_DRAM_BYTES_PER_STATE = 1057.8
 
 
 def main():

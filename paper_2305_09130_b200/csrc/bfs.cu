@@ -579,9 +579,10 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                 long long ins = -1;
                 int owner = mp;
                 uint64_t Hc = H;
+                bool ok = false;
                 if (e < ne) {
                     copy_key<SW>(row, pwords);
-                    bool ok = true;
+                    ok = true;
                     if (!fast_successor(d, s, en[e], row, hk, Hc)) {
                         if (a.op_hist) atomicAdd(&a.op_hist[en[e].op], 1ull);
                         copy_state(d.m, t, s);
@@ -594,12 +595,14 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                             set_error<SYS>(me.error, 3);
                         }
                     }
-                    if (ok) {
-                        const uint64_t hh = fmix64(Hc);
-                        owner = owner_of(hh, a.n_parts);
-                        ins = table_insert<SW, SYS>(a, a.part[owner], row, hh);
-                        if (ins == -2) set_error<SYS>(me.error, 1);
-                    }
+                }
+                // reconverge the per-op paths before the shared hash / insert code
+                __syncwarp();
+                if (ok) {
+                    const uint64_t hh = fmix64(Hc);
+                    if (a.n_parts > 1) owner = owner_of(hh, a.n_parts);
+                    ins = table_insert<SW, SYS>(a, a.part[owner], row, hh);
+                    if (ins == -2) set_error<SYS>(me.error, 1);
                 }
                 bool fresh = ins >= 0;
                 int keeper = -1;
