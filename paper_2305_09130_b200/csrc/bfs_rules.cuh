@@ -143,7 +143,7 @@ __device__ __forceinline__ int bfs_slot_rules(const MachDesc& m, const MState& s
     }
     k -= m.nwd;
     if (k < m.n_units) {
-        const int g = k, d = m.nwd == 1 ? 0 : g / m.nwu;
+        const int g = k, d = m.nwd == 1 ? 0 : div_nwu(m, g);
         const UnitS& un = s.unit[g];
         const DevS& dv = s.dev[d];
         // device_rules: offered by the unit's device

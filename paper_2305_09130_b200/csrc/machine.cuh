@@ -52,8 +52,42 @@ struct MachDesc {
     int32_t epi_len;     // epilogue instruction count
     int32_t max_id;      // value id of the MAX sentinel (minimum kernel)
     int32_t glob0_id;    // initial value id of glob[0]
+    // division-free hierarchy arithmetic (set_divisors): nwe is a power of two;
+    // the others divide by multiply-high with ceil(2^32 / d) (0 when d == 1)
+    int32_t lognwe;
+    uint32_t mag_nwu, mag_perdev, mag_ue;  // nwu, 1 + nwu (2 + nwe), 2 + nwe
     const int32_t* input_id;  // device: value id of input[i] (minimum kernel)
 };
+
+// x / d for 0 <= x, x * d < 2^32, given mag = ceil(2^32 / d) (0 for d == 1).
+__host__ __device__ inline int udiv_mag(int x, int d, uint32_t mag) {
+#ifdef __CUDA_ARCH__
+    (void)d;
+    return mag ? (int)__umulhi((uint32_t)x, mag) : x;
+#else
+    (void)mag;
+    return x / d;
+#endif
+}
+
+__host__ inline uint32_t div_magic(uint32_t d) {
+    return d <= 1 ? 0u : (uint32_t)(((1ull << 32) + d - 1) / d);
+}
+
+__host__ inline void set_divisors(MachDesc& m) {
+    int l = 0;
+    while ((1 << l) < m.nwe) ++l;
+    m.lognwe = l;
+    m.mag_nwu = div_magic((uint32_t)m.nwu);
+    m.mag_perdev = div_magic((uint32_t)(1 + m.nwu * (2 + m.nwe)));
+    m.mag_ue = div_magic((uint32_t)(2 + m.nwe));
+}
+
+__host__ __device__ inline int div_nwe(const MachDesc& m, int x) { return x >> m.lognwe; }
+__host__ __device__ inline int mod_nwe(const MachDesc& m, int x) { return x & (m.nwe - 1); }
+__host__ __device__ inline int div_nwu(const MachDesc& m, int x) {
+    return udiv_mag(x, m.nwu, m.mag_nwu);
+}
 
 struct Transition {
     uint16_t actor, peer;
@@ -101,12 +135,12 @@ __host__ __device__ inline int device_pid(const MachDesc& m, int d) {
     return 3 + d * (1 + m.nwu * (2 + m.nwe));
 }
 __host__ __device__ inline int unit_pid(const MachDesc& m, int g) {
-    const int d = g / m.nwu, u = g - d * m.nwu;
+    const int d = div_nwu(m, g), u = g - d * m.nwu;
     return device_pid(m, d) + 1 + u * (2 + m.nwe);
 }
 __host__ __device__ inline int barrier_pid(const MachDesc& m, int g) { return unit_pid(m, g) + 1; }
 __host__ __device__ inline int pex_pid(const MachDesc& m, int p) {
-    const int g = p / m.nwe;
+    const int g = div_nwe(m, p);
     return unit_pid(m, g) + 2 + (p - g * m.nwe);
 }
 
@@ -118,7 +152,7 @@ __host__ __device__ inline void role_of(const MachDesc& m, int pid, int& role, i
         return;
     }
     const int per_dev = 1 + m.nwu * (2 + m.nwe);
-    const int d = (pid - 3) / per_dev;
+    const int d = udiv_mag(pid - 3, per_dev, m.mag_perdev);
     int r = (pid - 3) - d * per_dev;
     if (r == 0) {
         role = 3;
@@ -126,7 +160,7 @@ __host__ __device__ inline void role_of(const MachDesc& m, int pid, int& role, i
         return;
     }
     r -= 1;
-    const int u = r / (2 + m.nwe);
+    const int u = udiv_mag(r, 2 + m.nwe, m.mag_ue);
     const int q = r - u * (2 + m.nwe);
     const int g = d * m.nwu + u;
     if (q == 0) {
@@ -361,14 +395,14 @@ __host__ __device__ inline int unit_rules(const MachDesc& m, const MState& s, in
         case U_REACTPEX:
         case U_STOPPEXES: {
             const int op = un.pc == U_STOPPEXES ? OP_UNITPEXSTOP : OP_UNITPEXGO;
-            const int arg = un.pc == U_STOPPEXES ? 0 : un.sent / m.nwe;
+            const int arg = un.pc == U_STOPPEXES ? 0 : div_nwe(m, un.sent);
             for (int e = 0; e < m.nwe; ++e)
                 if (s.pex[g * m.nwe + e].pc == P_WAITGO) MCTB_PUSH(upid, upid + 2 + e, op, arg);
             break;
         }
         case U_SENDUNITDONE:
-            if (s.dev[g / m.nwu].pc == D_WAITUNITDONE)
-                MCTB_PUSH(upid, device_pid(m, g / m.nwu), OP_UNITDONE, un.nwg);
+            if (s.dev[div_nwu(m, g)].pc == D_WAITUNITDONE)
+                MCTB_PUSH(upid, device_pid(m, div_nwu(m, g)), OP_UNITDONE, un.nwg);
             break;
         case U_STOPBARRIER:
             if (s.bar[g].pc == B_COUNTING && s.bar[g].count == 0)
@@ -388,7 +422,7 @@ __host__ __device__ inline int barrier_rules(const MachDesc& m, const MState& s,
 
 __host__ __device__ inline int pex_rules(const MachDesc& m, const MState& s, int p,
                                          Transition* out, int n) {
-    const int g = p / m.nwe;
+    const int g = div_nwe(m, p);
     const PexS& px = s.pex[p];
     const int upid = unit_pid(m, g);
     const int ppid = upid + 2 + (p - g * m.nwe);
@@ -540,7 +574,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
         case OP_DEVICEUNITGO: {
             if (role != 3 || prole != 4) return false;
             DevS& dv = s.dev[ord];
-            if (dv.pc != D_SENDUNITGO || pord / m.nwu != ord) return false;
+            if (dv.pc != D_SENDUNITGO || div_nwu(m, pord) != ord) return false;
             UnitS& un = s.unit[pord];
             const int nwg = dv.batch_base + dv.k;
             if (un.pc != U_WAITGO || t.arg != nwg) return false;
@@ -563,7 +597,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
         case OP_DEVICEUNITSTOP: {
             if (role != 3 || prole != 4) return false;
             DevS& dv = s.dev[ord];
-            if (dv.pc != D_STOPUNITS || pord / m.nwu != ord) return false;
+            if (dv.pc != D_STOPUNITS || div_nwu(m, pord) != ord) return false;
             UnitS& un = s.unit[pord];
             if (un.pc != U_WAITGO) return false;
             un.pc = U_STOPPEXES;
@@ -575,9 +609,9 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (role != 4 || prole != 6) return false;
             UnitS& un = s.unit[ord];
             if (un.pc != U_ACTIVATEPEX && un.pc != U_REACTPEX) return false;
-            if (pord / m.nwe != ord) return false;
+            if (div_nwe(m, pord) != ord) return false;
             PexS& px = s.pex[pord];
-            const int iter = un.sent / m.nwe;
+            const int iter = div_nwe(m, un.sent);
             if (px.pc != P_WAITGO || t.arg != iter) return false;
             px = pex_init(un.nwg, iter);  // start_activation, machine.cpp:164-172
             place_pex(m, px);
@@ -596,7 +630,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (role != 4) return false;
             UnitS& un = s.unit[ord];
             if (un.pc != U_SENDUNITDONE) return false;
-            DevS& dv = s.dev[ord / m.nwu];
+            DevS& dv = s.dev[div_nwu(m, ord)];
             if (dv.pc != D_WAITUNITDONE) return false;
             if (m.kernel == 0) s.all_nwe -= m.nwe;
             un = UnitS{0, 0, 0, 0, 0, 0};
@@ -609,7 +643,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
         case OP_UNITPEXSTOP: {
             if (role != 4 || prole != 6) return false;
             UnitS& un = s.unit[ord];
-            if (un.pc != U_STOPPEXES || pord / m.nwe != ord) return false;
+            if (un.pc != U_STOPPEXES || div_nwe(m, pord) != ord) return false;
             PexS& px = s.pex[pord];
             if (px.pc != P_WAITGO) return false;
             px.pc = P_EXITED;
@@ -641,7 +675,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (px.pc != P_RUN) return false;
             const Instr in = instr_at(m, px.phase, px.cursor);
             if (in.kind != IK_EFFECT || t.arg != px.cursor) return false;
-            const int g = ord / m.nwe, me = ord - g * m.nwe;
+            const int g = div_nwe(m, ord), me = ord - g * m.nwe;
             const int slot = g * m.np + me;  // myloc, machine.hpp:205
             int32_t v;
             int32_t* dst;
@@ -670,7 +704,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (role != 6) return false;
             PexS& px = s.pex[ord];
             if (px.pc != P_ARRIVEBARRIER && px.pc != P_ARRIVEGROUPEND) return false;
-            BarS& b = s.bar[ord / m.nwe];
+            BarS& b = s.bar[div_nwe(m, ord)];
             if (b.pc != B_COUNTING || b.count >= m.nwe) return false;
             b.count += 1;
             px.pc = px.pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
@@ -713,7 +747,7 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (role != 6) return false;
             PexS& px = s.pex[ord];
             if (px.pc != P_SENDITEMDONE) return false;
-            UnitS& un = s.unit[ord / m.nwe];
+            UnitS& un = s.unit[div_nwe(m, ord)];
             if (un.pc != U_SERVE) return false;
             un.got_items += 1;
             px = pex_init(0, 0);
@@ -725,10 +759,10 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             if (role != 6) return false;
             PexS& px = s.pex[ord];
             if (px.pc != P_SENDENDDONE) return false;
-            UnitS& un = s.unit[ord / m.nwe];
+            UnitS& un = s.unit[div_nwe(m, ord)];
             if (un.pc != U_SERVE) return false;
             un.got_ends += 1;
-            if (ord % m.nwe == 0) s.all_nwe -= 1;
+            if (mod_nwe(m, ord) == 0) s.all_nwe -= 1;
             px = pex_init(0, 0);
             if (un.got_ends == m.nwe) un.pc = U_SENDUNITDONE;
             return true;

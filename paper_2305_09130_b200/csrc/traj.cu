@@ -198,6 +198,7 @@ int build_desc(const int* plat, int size, int kernel, const int64_t* input, int 
     m.n_units = m.nwd * m.nwu;
     m.n_pex = m.n_units * m.nwe;
     m.n_proc = 3 + m.nwd + 2 * m.n_units + m.n_pex;
+    set_divisors(m);
     m.reps = size / ts;
     if (kernel == 0) {
         m.act_len = 4 * m.reps + 2;
