@@ -108,7 +108,8 @@ int mctb_simulate(const int* plat, int size, int kernel, const int64_t* input, i
  * explore.hpp:295-299 re-designed as counter-based random schedules):
  * trajectory t (= traj0 + i) runs configuration configs[t % n_configs]
  * (configs = int32[2 * n_configs] of (wg, ts)).
- * out = int64[6 * n_traj]: {time, steps, result, status, fnv1a64(trace), config}. */
+ * out = int64[6 * n_traj]: {time, steps, result, status, FNV-1a 64 of the trace over its
+ * 32-bit words {actor, peer, op, arg} (h ^= w; h *= 0x100000001b3), config}. */
 int mctb_trajectories(const int* plat, int size, int kernel, const int64_t* input,
                       const int32_t* configs, int n_configs, int policy, uint64_t seed,
                       uint64_t traj0, uint64_t n_traj, int64_t max_steps, int64_t* out);

@@ -1693,14 +1693,15 @@ int mo_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_t*
 
 /* Bulk CPU replay of GPU trajectories (checker for mctb_trajectories):
  * trajectory t = traj0 + i runs configs[t % n_configs] under `policy`;
- * out = int64[6 * n]: {time, steps, result, status, fnv1a64(trace words), config}. */
+ * out = int64[6 * n]: {time, steps, result, status, FNV-1a 64 over the trace's
+ * 32-bit words, config}. */
 static uint64_t fnv_words(uint64_t h, const mo_transition* t) {
+    /* FNV-1a over the four 32-bit words (one xor-multiply per word) */
     const int32_t w[4] = {t->actor, t->peer, t->op, t->arg};
-    for (int k = 0; k < 4; ++k)
-        for (int i = 0; i < 4; ++i) {
-            h ^= ((uint32_t)w[k] >> (8 * i)) & 0xff;
-            h *= 0x100000001b3ull;
-        }
+    for (int k = 0; k < 4; ++k) {
+        h ^= (uint32_t)w[k];
+        h *= 0x100000001b3ull;
+    }
     return h;
 }
 

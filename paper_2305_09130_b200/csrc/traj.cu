@@ -12,7 +12,7 @@
 //                floor(word * n / 2^32) — counter-based, so any trajectory is
 //                replayable on its own on the CPU (oracle mo_simulate policy 3).
 // Per trajectory it records time, transitions, glob[0] (minimum kernel), a
-// status, and a 64-bit FNV-1a hash of the transition sequence, so 10^6
+// status, and a 64-bit FNV-1a hash (over 32-bit words) of the transition sequence, so 10^6
 // trajectories are checked against CPU replays without shipping traces.
 #include <algorithm>
 #include <cstring>
@@ -46,13 +46,11 @@ __host__ __device__ inline void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
     out[3] = c3;
 }
 
+// FNV-1a over the transition's four 32-bit words {actor, peer, op, arg} (one
+// xor-multiply per word; the trace checksum the CPU replay recomputes).
 __host__ __device__ inline uint64_t fnv_mix(uint64_t h, uint32_t w) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        h ^= (w >> (8 * i)) & 0xff;
-        h *= 0x100000001b3ull;
-    }
-    return h;
+    h ^= w;
+    return h * 0x100000001b3ull;
 }
 
 __host__ __device__ inline uint64_t fnv_transition(uint64_t h, const Transition& t) {
