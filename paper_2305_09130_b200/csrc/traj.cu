@@ -67,7 +67,16 @@ __global__ void __launch_bounds__(128) traj_kernel(const MachDesc* __restrict__ 
                                                    uint64_t seed, uint64_t traj0, uint64_t n_traj,
                                                    int64_t max_steps, TrajOut* __restrict__ out,
                                                    int32_t* __restrict__ trace, int64_t trace_cap) {
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // warp w of group g runs the 32 trajectories of one configuration c: offset
+    // t = g * 32 * n_desc + lane * n_desc + c, so (traj0 + t) % n_desc is uniform in
+    // the warp (no divergence between configurations of different lengths); the
+    // id -> configuration mapping and the output layout are unchanged
+    const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t t = gid;
+    if (n_desc > 1) {
+        const uint64_t w = gid >> 5, grp = w / (uint64_t)n_desc, c = w - grp * (uint64_t)n_desc;
+        t = grp * 32ull * (uint64_t)n_desc + (gid & 31) * (uint64_t)n_desc + c;
+    }
     if (t >= n_traj) return;
     const uint64_t traj = traj0 + t;
     const MachDesc m = descs[n_desc == 1 ? 0 : traj % (uint64_t)n_desc];
@@ -252,7 +261,10 @@ int launch_trajectories(const MachDesc* d_descs, int n_desc, int policy, uint64_
                         int32_t* d_trace, int64_t trace_cap, cudaStream_t stream) {
     if (n_traj == 0) return MCTB_OK;
     const unsigned threads = 128;
-    const unsigned blocks = (unsigned)((n_traj + threads - 1) / threads);
+    // whole groups of 32 trajectories per configuration (see traj_kernel)
+    const uint64_t g = 32ull * (uint64_t)std::max(n_desc, 1);
+    const uint64_t span = n_desc > 1 ? (n_traj + g - 1) / g * g : n_traj;
+    const unsigned blocks = (unsigned)((span + threads - 1) / threads);
     switch (policy) {
         case MCTB_POLICY_ROUND_ROBIN:
             traj_kernel<MCTB_POLICY_ROUND_ROBIN><<<blocks, threads, 0, stream>>>(
