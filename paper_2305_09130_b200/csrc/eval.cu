@@ -99,31 +99,39 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                 // waves = ceil(dr / nwd) with nwd = nd below nd_thr (one working device per
                 // workgroup batch) and nwd = q above it.  Below nd_thr the quotient is
                 // strength-reduced along the nd digit: dr = Q*nd + R, and nd -> nd+1 gives
-                // R -= Q (one correction Q -= 1, R += nd+1 when R < 0 and Q <= nd+1, a real
-                // division otherwise), so the loop issues no XU (I2F/MUFU/F2I) work.
+                // R -= Q with at most one correction (Q -= 1, R += nd+1) once Q <= nd+1,
+                // predicated, so the hot loop has no branch and no XU (I2F/MUFU/F2I) work.
                 const uint32_t w_hi = q == 0 ? dr : (dr + q - 1) / q;
-                uint32_t Q = dr / nd;
-                int32_t R = (int32_t)(dr - Q * nd);
+                const uint32_t thr = q == 0 ? 0u : nd_thr;  // nd >= thr: waves = w_hi
+                // waves * D32 < kKeySat  <=>  waves <= wmax (32-bit saturating product)
+                const uint32_t wmax = (kKeySat - 1) / D32;
                 uint32_t best_k = 0xffffffffu;
-                for (uint32_t k = 0; k < run; ++k) {
-                    const uint32_t waves = (q == 0 || nd >= nd_thr) ? w_hi : Q + (R != 0);
-                    const uint64_t t = (uint64_t)waves * D32;
-                    const uint32_t tf = t < kKeySat ? (uint32_t)t : kKeySat;
+                uint32_t k = 0;
+                // one correction per step needs Q = dr / nd <= nd + 1, i.e.
+                // dr < nd (nd + 2): below that (small nd) divide exactly
+                for (; k < run && nd < 65536u && dr >= nd * (nd + 2); ++k, ++nd) {
+                    const uint32_t waves = nd >= thr ? w_hi : (dr + nd - 1) / nd;
+                    const uint32_t tf = waves <= wmax ? waves * D32 : kKeySat;
                     if (tf < best_tf) {
                         best_tf = tf;
                         best_k = k;
                     }
+                }
+                uint32_t Q = dr / nd;
+                int32_t R = (int32_t)(dr - Q * nd);
+                for (; k < run; ++k) {
+                    const uint32_t waves = nd >= thr ? w_hi : Q + (R != 0);
+                    const uint32_t tf = waves <= wmax ? waves * D32 : kKeySat;
+                    if (tf < best_tf) {
+                        best_tf = tf;
+                        best_k = k;
+                    }
+                    // nd -> nd + 1: dr = Q (nd+1) + (R - Q), at most one correction
                     ++nd;
                     R -= (int32_t)Q;
-                    if (R < 0) {
-                        if (Q <= nd) {
-                            Q -= 1;
-                            R += (int32_t)nd;
-                        } else {
-                            Q = dr / nd;
-                            R = (int32_t)(dr - Q * nd);
-                        }
-                    }
+                    const int32_t neg = R < 0;
+                    Q -= (uint32_t)neg;
+                    R += neg ? (int32_t)nd : 0;
                 }
                 if (best_k != 0xffffffffu) best_idx = base + best_k;
             }
