@@ -481,8 +481,8 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
 
 # Thread-level instructions executed per configuration by space_argmin_kernel<0>
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
-# (profiles/r01_argmin_v2_ncu.txt).  Re-measured after every kernel change.
-INT_OPS_PER_CONFIG = 27.9
+# (profiles/r01_argmin_v3_ncu.txt).  Re-measured after every kernel change.
+INT_OPS_PER_CONFIG = 23.57
 
 # configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
 # state (smsp__inst_executed.sum / states; DRAM read + write bytes / states),
