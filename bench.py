@@ -216,7 +216,7 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     key = torch.empty(1, dtype=torch.int64, device="cuda")
-    none_key = torch.tensor([1 << 62], dtype=torch.int64, device="cuda")  # > every real key
+    none_key = torch.tensor([(1 << 63) - 1], dtype=torch.int64, device="cuda")  # >= every key
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 256 MB > L2
     launches_per_step = 1  # argmin kernel (the key reset is a torch copy)
 
@@ -481,8 +481,8 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
 
 # Thread-level instructions executed per configuration by space_argmin_kernel<0>
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
-# (profiles/r01_argmin_v3_ncu.txt).  Re-measured after every kernel change.
-INT_OPS_PER_CONFIG = 23.57
+# (profiles/r01_argmin_v5_ncu.txt).  Re-measured after every kernel change.
+INT_OPS_PER_CONFIG = 14.67
 
 # configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
 # state (smsp__inst_executed.sum / states; DRAM read + write bytes / states),

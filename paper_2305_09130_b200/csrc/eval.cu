@@ -107,9 +107,9 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                 const uint32_t wmax = (kKeySat - 1) / D32;
                 uint32_t best_k = 0xffffffffu;
                 uint32_t k = 0;
-                // one correction per step needs Q = dr / nd <= nd + 1, i.e.
-                // dr < nd (nd + 2): below that (small nd) divide exactly
-                for (; k < run && nd < 65536u && dr >= nd * (nd + 2); ++k, ++nd) {
+                // one correction per step needs Q = (dr - 1) / nd <= nd + 1, implied by
+                // dr <= nd (nd + 2): below that (small nd) divide exactly
+                for (; k < run && nd < 65536u && dr > nd * (nd + 2); ++k, ++nd) {
                     const uint32_t waves = nd >= thr ? w_hi : (dr + nd - 1) / nd;
                     const uint32_t tf = waves <= wmax ? waves * D32 : kKeySat;
                     if (tf < best_tf) {
@@ -117,21 +117,41 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                         best_k = k;
                     }
                 }
-                uint32_t Q = dr / nd;
-                int32_t R = (int32_t)(dr - Q * nd);
+                // ceil(dr / nd) = floor((dr - 1) / nd) + 1 (dr >= 1): the recurrence runs
+                // on dm = dr - 1, so waves is one add (no R != 0 test)
+                const uint32_t dm = dr - 1;
+                uint32_t Q = dm / nd;
+                int32_t R = (int32_t)(dm - Q * nd);
+                // for nd < thr, nd <= q, so ceil(dr/nd) >= ceil(dr/q) = w_hi; for nd >= thr
+                // ceil(dr/nd) <= w_hi: waves = max(Q + 1, w_hi) in both ranges.  waves is
+                // non-increasing along nd, so the saturated configurations (waves > wmax)
+                // form a prefix of the run: the main loop needs no saturation test
                 for (; k < run; ++k) {
-                    const uint32_t waves = nd >= thr ? w_hi : Q + (R != 0);
-                    const uint32_t tf = waves <= wmax ? waves * D32 : kKeySat;
+                    if (max(Q + 1, w_hi) <= wmax) break;
+                    if (kKeySat < best_tf) {
+                        best_tf = kKeySat;
+                        best_k = k;
+                    }
+                    ++nd;
+                    R -= (int32_t)Q;
+                    if (R < 0) {
+                        Q -= 1;
+                        R += (int32_t)nd;
+                    }
+                }
+                for (; k < run; ++k) {
+                    const uint32_t tf = max(Q + 1, w_hi) * D32;
                     if (tf < best_tf) {
                         best_tf = tf;
                         best_k = k;
                     }
-                    // nd -> nd + 1: dr = Q (nd+1) + (R - Q), at most one correction
+                    // nd -> nd + 1: dm = Q (nd+1) + (R - Q), at most one correction
                     ++nd;
                     R -= (int32_t)Q;
-                    const int32_t neg = R < 0;
-                    Q -= (uint32_t)neg;
-                    R += neg ? (int32_t)nd : 0;
+                    if (R < 0) {
+                        Q -= 1;
+                        R += (int32_t)nd;
+                    }
                 }
                 if (best_k != 0xffffffffu) best_idx = base + best_k;
             }

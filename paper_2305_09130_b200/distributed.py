@@ -42,7 +42,7 @@ def sharded_space_argmin(total: int, local_argmin: Callable[[int, int], int],
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     first, count = shard(total, rank, world)
-    key = local_argmin(first, count) if count else (1 << 62)
+    key = local_argmin(first, count) if count else (1 << 63) - 1
     t = torch.tensor([min(key, (1 << 63) - 1)], dtype=torch.int64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)

@@ -70,3 +70,33 @@ def test_eval_table_matches_oracle(engine, oracle):
             assert (t[i], s[i]) == (want[0], want[1])
         else:
             assert t[i] == -1
+
+
+@pytest.mark.parametrize("space_id", range(3))
+def test_argmin_windows_match_oracle(engine, oracle, space_id):
+    """Many short windows [first, first+count) of large spaces, each against the
+    oracle's argmin: every window exercises one thread's run logic (the exact
+    small-nd prefix, the saturated prefix, the branch-free recurrence and the
+    index tie-break) instead of only the global winner."""
+    m = engine
+    spaces = [
+        m.Space(0, 1 << 10, 4, (1, 160000), (1, 64), (0, 9), (1, 9), (1, 9)),  # bench space
+        m.Space(1, 1 << 20, 7, (1, 5000), (1, 13), (0, 4), (1, 19), (1, 19)),  # saturating
+        m.Space(0, 1 << 6, 2, (3, 700), (2, 9), (0, 3)),
+    ]
+    sp = spaces[space_id]
+    import torch
+    from paper_2305_09130_b200.space import space_argmin_async
+    stream = torch.cuda.current_stream().cuda_stream
+    rng = random.Random(100 + space_id)
+    for _ in range(120):
+        count = rng.choice([1, 2, 3, 17, 200, 1000, 5000])
+        first = rng.randint(0, sp.count - count)
+        if rng.random() < 0.3:  # windows starting at small nd
+            first -= first % (sp.desc()[4] - sp.desc()[3] + 1)
+        # the packed key itself (device-resident call): windows of only infeasible
+        # configurations have a key too (saturated time, first index)
+        d_key = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device="cuda")
+        space_argmin_async(sp, first, count, d_key.data_ptr(), stream)
+        key, t, idx = oracle.space_argmin(list(sp.desc()), first, count)
+        assert int(d_key.item()) == key, (space_id, first, count)
