@@ -318,6 +318,7 @@ def run_b200(args):
                          "frac": achieved / peak_issue, "traffic": None,
                          "kernel": "space_argmin_kernel<0>", "kernel_ms": statistics.mean(kern_ms),
                          "ops_per_config": ops_per_cfg,
+                         "alu_pipe_frac_ncu": ALU_PIPE_FRAC_NCU,
                          "peak_source": "nominal INT32 issue rate at the sampled SM clock "
                                         f"({sms} SMs x 128 lanes x {clk_mhz:.0f} MHz); not in "
                                         "MEASURED_PEAKS.json",
@@ -483,6 +484,9 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
 # (profiles/r01_argmin_v5_ncu.txt).  Re-measured after every kernel change.
 INT_OPS_PER_CONFIG = 14.67
+# the binding pipe of that kernel in the same capture:
+# sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active
+ALU_PIPE_FRAC_NCU = 0.877
 
 # configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
 # state (smsp__inst_executed.sum / states; DRAM read + write bytes / states),
