@@ -273,134 +273,6 @@ __device__ __forceinline__ bool quiescent(const BfsArgs& a) {
     return done == tail;
 }
 
-// Record writers for the in-place successors (field order of pack()): the
-// record is composed in a register and written with one multi-word set (every
-// rewritten word also updates the state hash H); records wider than 62 bits
-// are written field by field.
-__device__ __forceinline__ void write_pex(uint32_t* row, const Layout& l, int p, const PexS& x,
-                                          const uint64_t* hk, uint64_t& H) {
-    const int o = l.off_pex + p * l.pex_bits;
-    const int s1 = 5 + l.cursor, s2 = s1 + l.busy, s3 = s2 + 1, s4 = s3 + l.pnwg;
-    if (l.pex_bits <= 62) {
-        const uint64_t v = (uint64_t)x.pc | ((uint64_t)x.phase << 4) | ((uint64_t)x.cursor << 5) |
-                           ((uint64_t)x.busy_left << s1) | ((uint64_t)x.reported << s2) |
-                           ((uint64_t)(uint32_t)x.nwg << s3) | ((uint64_t)x.iter << s4);
-        set_bits_h(row, o, l.pex_bits, v, hk, H);
-        return;
-    }
-    set_bits_h(row, o, 4, (uint32_t)x.pc, hk, H);
-    set_bits_h(row, o + 4, 1, (uint32_t)x.phase, hk, H);
-    set_bits_h(row, o + 5, l.cursor, x.cursor, hk, H);
-    set_bits_h(row, o + s1, l.busy, x.busy_left, hk, H);
-    set_bits_h(row, o + s2, 1, (uint32_t)x.reported, hk, H);
-    set_bits_h(row, o + s3, l.pnwg, (uint32_t)x.nwg, hk, H);
-    set_bits_h(row, o + s4, l.iter, x.iter, hk, H);
-}
-
-// The unit's own fields (not its barrier's, which follow them in the record).
-__device__ __forceinline__ void write_unit(uint32_t* row, const Layout& l, int g, const UnitS& u,
-                                           const uint64_t* hk, uint64_t& H) {
-    const int o = l.off_units + g * l.unit_bits;
-    const int s1 = 3 + l.uk, s2 = s1 + l.nwg, s3 = s2 + l.sent, s4 = s3 + l.items;
-    const int width = s4 + l.ends;
-    if (width <= 62) {
-        const uint64_t v = (uint64_t)(uint32_t)u.pc | ((uint64_t)(uint32_t)u.k << 3) |
-                           ((uint64_t)(uint32_t)u.nwg << s1) | ((uint64_t)(uint32_t)u.sent << s2) |
-                           ((uint64_t)(uint32_t)u.got_items << s3) |
-                           ((uint64_t)(uint32_t)u.got_ends << s4);
-        set_bits_h(row, o, width, v, hk, H);
-        return;
-    }
-    set_bits_h(row, o, 3, (uint32_t)u.pc, hk, H);
-    set_bits_h(row, o + 3, l.uk, (uint32_t)u.k, hk, H);
-    set_bits_h(row, o + s1, l.nwg, (uint32_t)u.nwg, hk, H);
-    set_bits_h(row, o + s2, l.sent, (uint32_t)u.sent, hk, H);
-    set_bits_h(row, o + s3, l.items, (uint32_t)u.got_items, hk, H);
-    set_bits_h(row, o + s4, l.ends, (uint32_t)u.got_ends, hk, H);
-}
-
-// In-place successors for the transitions behind the combinatorial state
-// explosion: an element reporting a busy tick or arriving at its barrier, and
-// the unit <-> element handshakes (activation, item done, group done, stop).
-// They touch one element record, its unit record and at most one header field;
-// the new values follow Machine::apply (machine.cpp:479-500, 518-530, 541-551,
-// 569-580, 618-646) and are written over the parent's packed words.  `tr` is in
-// the ordinal form of bfs_rules.cuh.  Every other transition goes through the
-// generic unpacked apply() (machine.cuh).
-__device__ __forceinline__ bool fast_successor(const BfsDesc& d, const MState& s,
-                                               const Transition& tr, uint32_t* row,
-                                               const uint64_t* hk, uint64_t& H) {
-    const Layout& l = d.l;
-    const MachDesc& m = d.m;
-    switch (tr.op) {
-        case OP_PEXREPORT: {
-            const int off = l.off_pex + tr.actor * l.pex_bits + l.poff_reported;
-            const int i = div31(off);
-            const uint32_t bit = 1u << (off - i * kWordBits);  // reported was 0
-            row[i] |= bit;
-            H += (uint64_t)bit * hk[i];
-            set_bits_h(row, l.off_nrp, l.nrp, (uint32_t)(s.nrp_work + 1), hk, H);
-            return true;
-        }
-        case OP_PEXARRIVE: {
-            const int p = tr.actor, g = tr.peer;
-            const int pc = s.pex[p].pc == P_ARRIVEBARRIER ? P_WAITBARRIER : P_WAITGROUPEND;
-            set_bits_h(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)pc, hk, H);
-            set_bits_h(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount,
-                       (uint32_t)(s.bar[g].count + 1), hk, H);
-            return true;
-        }
-        case OP_UNITPEXGO: {
-            const int g = tr.actor, p = tr.peer;
-            UnitS un = s.unit[g];
-            PexS px = pex_init(un.nwg, tr.arg);  // arg = sent / nwe
-            place_pex(m, px);
-            un.sent += 1;
-            if (un.pc == U_ACTIVATEPEX) {
-                if (++un.k == m.nwe) {
-                    un.pc = U_SERVE;
-                    un.k = 0;
-                }
-            } else {
-                un.pc = U_SERVE;
-            }
-            write_pex(row, l, p, px, hk, H);
-            write_unit(row, l, g, un, hk, H);
-            return true;
-        }
-        case OP_UNITPEXSTOP: {
-            const int g = tr.actor, p = tr.peer;
-            UnitS un = s.unit[g];
-            if (++un.k == m.nwe) un.pc = U_STOPBARRIER;
-            set_bits_h(row, l.off_pex + p * l.pex_bits, 4, (uint32_t)P_EXITED, hk, H);
-            write_unit(row, l, g, un, hk, H);
-            return true;
-        }
-        case OP_PEXITEMDONE: {
-            const int p = tr.actor, g = tr.peer;
-            UnitS un = s.unit[g];
-            un.got_items += 1;
-            if (un.sent < m.wg) un.pc = U_REACTPEX;
-            else if (m.kernel == 0 && un.got_items == m.wg) un.pc = U_SENDUNITDONE;
-            write_pex(row, l, p, pex_init(0, 0), hk, H);
-            write_unit(row, l, g, un, hk, H);
-            return true;
-        }
-        case OP_PEXENDDONE: {
-            const int p = tr.actor, g = tr.peer;
-            UnitS un = s.unit[g];
-            un.got_ends += 1;
-            if (un.got_ends == m.nwe) un.pc = U_SENDUNITDONE;
-            if ((p & (m.nwe - 1)) == 0)
-                set_bits_h(row, l.off_nrp + l.nrp, l.allnwe, (uint32_t)(s.all_nwe - 1), hk, H);
-            write_pex(row, l, p, pex_init(0, 0), hk, H);
-            write_unit(row, l, g, un, hk, H);
-            return true;
-        }
-        default: return false;
-    }
-}
-
 // 64-bit warp sum (every lane gets it)
 __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 #pragma unroll

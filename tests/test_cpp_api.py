@@ -71,3 +71,19 @@ def test_reference_model_and_search_tests_pass_on_the_gpu_engine():
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "13 test cases, 0 failed" in r.stdout
+
+
+@pytest.mark.skipif(not os.path.exists("/usr/local/cuda/bin/nvcc"), reason="no nvcc")
+def test_exploration_fast_paths_match_serial_semantics():
+    """tests/cpp/bfs_rules_check.cu, on the CPU: on random walks through 433
+    configurations, the exploration's per-process enumeration equals enabled(),
+    the table-driven unpack inverts pack(), and every in-place successor equals
+    pack(apply(...)) with its incremental hash equal to the full hash."""
+    _lib()
+    r = subprocess.run(["make", "-s", "-C", CPP, "_build/bfs_rules_check"], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
+    r = subprocess.run([os.path.join(CPP, "_build", "bfs_rules_check")], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert " 0 failed" in r.stdout
