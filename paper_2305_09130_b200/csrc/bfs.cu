@@ -730,7 +730,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     // cap times the configurations) start small: a fresh multi-GB table costs
     // more to map than the sweep takes
     if (first_cap) cap = std::min(cap, first_cap);
-    if (const char* e = getenv("MCTB_BFS_CAP_LOG2")) cap = 1ull << atoi(e);  // experiments
+    if (const char* e = getenv("MCTB_BFS_CAP_LOG2")) cap = 1ull << atoi(e);  // tests: force a restart
     const uint64_t cap_limit = [&] {
         uint64_t c = 1024;
         while ((double)(c * 2) * slot_bytes * n_parts < 0.8 * (double)free_b) c <<= 1;

@@ -149,3 +149,18 @@ def test_multi_gpu_api_one_rank_equals_reference(engine, gold):
                 c["states"], c["transitions"], c["max_depth"]), key
             assert (g.min_time, g.max_time, g.terminals) == (
                 c["min_time"], c["max_time"], c["n_terminal"]), key
+
+
+@pytest.mark.parametrize("parts", [1, 2])
+def test_table_overflow_restarts_with_identical_counts(engine, parts, monkeypatch):
+    """A first table far too small (2^16 slots for 1.3e5 states) overflows; the
+    sweep restarts 8x larger until it fits, and the counts are those of a sweep
+    that never overflowed."""
+    m = engine
+    args = (m.PlatformConfig(1, 2, 8, 4), m.ProblemSpec.abstract(32), [m.TuningParams(16, 2)])
+    want = m.explore_configs(*args, partitions=parts)[0]
+    monkeypatch.setenv("MCTB_BFS_CAP_LOG2", "16")
+    info = []
+    got = m.explore_configs(*args, partitions=parts, info=info)[0]
+    assert got == want and want.complete and want.states_visited == 131492
+    assert info[0].table_slots > (1 << 16) * parts
