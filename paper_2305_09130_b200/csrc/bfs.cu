@@ -174,9 +174,11 @@ __device__ long long table_insert(const BfsArgs& a, const BfsPart& pt, const uin
                                   uint64_t h) {
     const unsigned long long fp = h | 1ull;  // nonzero: 0 marks an empty slot
     uint64_t i = h & a.cap_mask;
-    // a probe sequence this long only happens in a table that is too full: report it
-    // (the sweep restarts with a larger table) instead of scanning the whole table
-    for (uint64_t probe = 0; probe < 4096; ++probe, i = (i + 1) & a.cap_mask) {
+    // a probe sequence this long only happens in a table that is too full (at load
+    // <= 1/2 linear probing's longest sequence over 1e8 keys is a few dozen): report
+    // it early — the sweep restarts with a larger table — instead of crawling
+    // through an overloaded one
+    for (uint64_t probe = 0; probe < 256; ++probe, i = (i + 1) & a.cap_mask) {
         uint32_t* sl = pt.table + i * SW;
         uint32_t v[SW];
         unsigned long long t;
@@ -718,9 +720,9 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double slot_bytes = 4.0 * sw + 2.0;  // slot line + queue (half the slots)
-    // capacity grows 8x on overflow; the sweep restarts (all counts are rebuilt)
+    // capacity grows 16x on overflow; the sweep restarts (all counts are rebuilt)
     // first capacity: enough for the bound up to 2^29 slots (a restart loses the
-    // work done, so large sweeps start large); then 8x per overflow.  Split over
+    // work done, so large sweeps start large); then 16x per overflow.  Split over
     // the partitions (each holds ~1/P of the states).
     // load <= 1/4 at the bound: linear probing then averages ~1.2 probes per
     // successor (at 1/2 it was ~1.6: 14% slower on the 1.37e8-state space)
@@ -828,7 +830,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         res->words = pl.words;
         res->capacity = cap * n_parts;
         if ((res->error == 1 || res->error == 2) && cap < cap_limit) {
-            cap = std::min(cap * 8, cap_limit);
+            cap = std::min(cap * 16, cap_limit);
             continue;
         }
         break;

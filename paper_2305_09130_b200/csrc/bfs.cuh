@@ -33,7 +33,7 @@ struct BfsResult {
 // (ExploreLimits::max_states, explore.hpp:227-233).
 // seeds (optional): packed states of configuration 0 (layout bfs_layout(hs[0].d, 1))
 // to start from instead of the initial states — a multi-source exploration.
-// first_cap (0 = sized for max_states) bounds the first table; it grows 8x
+// first_cap (0 = sized for max_states) bounds the first table; it grows 16x
 // (restarting the sweep) on overflow.
 // n_parts > 1 splits the visited set into hash partitions on this device (the
 // multi-GPU exchange path, exercised on one GPU); sys_scope selects the

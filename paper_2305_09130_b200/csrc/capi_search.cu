@@ -83,7 +83,7 @@ int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
         BfsResult r;
         cudaStream_t st;
         MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib, 1, false, 1ull << 23);
+        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib, 1, false, 1ull << 25);
         cudaStreamDestroy(st);
         if (rc) return rc;
         if (r.error) {
@@ -167,8 +167,16 @@ int prepare(Ctx& c, int64_t max_states) {
     // every interleaving of every configuration, one sweep.  The first DFS paths
     // (needed only for the configurations a probe finds violating) run lazily.
     const double t1 = now_ms();
+    // first table from the cost model: the explored states ran at ~3x the lock-step
+    // transitions summed over the configurations on the Table-1 platforms
+    // (sizes 8-512); 4x that at load 1/4, clamped to [2^22, 2^29] slots.  Wider
+    // spaces outgrow it and restart 16x larger.
+    uint64_t est = 0;
+    for (int k = 0; k < nc; ++k) est += (uint64_t)std::max<int64_t>(c.cm_steps[k], 1);
+    uint64_t first_cap = 1ull << 22;
+    while (first_cap < 12 * est && first_cap < (1ull << 29)) first_cap <<= 1;
     rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st, false, nullptr, 1,
-                 false, 1ull << 23);
+                 false, first_cap);
     c.ms_bfs = now_ms() - t1;
     cudaStreamDestroy(st);
     if (rc) return rc;
