@@ -24,6 +24,7 @@
 // are explored in the same sweep, tagged by a cfg field of the packed state;
 // per-configuration statistics give the reference's ExploreStats.
 #include <algorithm>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -702,6 +703,15 @@ static int seed_launch(const BfsPlan& pl, const BfsArgs& a, bool sys, const std:
     return MCTB_OK;
 }
 
+// Stream-ordered free at scope exit (every early error return included).
+struct AsyncFree {
+    void* p;
+    cudaStream_t st;
+    ~AsyncFree() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds, int n_parts,
             bool sys_scope, uint64_t first_cap) {
@@ -712,6 +722,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     BfsPlan pl;
     int rc = bfs_plan(hs, st, &pl);
     if (rc) return rc;
+    const AsyncFree ids_guard{pl.d_ids, st};
     const int n_cfg = pl.n_cfg, sw = pl.sw;
     const ExploreFn kern = explore_fn(sw, sys_scope);
     int grid = 0;
@@ -759,6 +770,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         const size_t pb = (part_bytes(cap, sw, &misc_off) + 255) & ~(size_t)255;
         void* blob = nullptr;
         MCTB_CUDA(cudaMallocAsync(&blob, pb * n_parts + shared_bytes(pl), st));
+        const AsyncFree blob_guard{blob, st};  // freed when this attempt ends
         char* b = (char*)blob;
         for (int p = 0; p < n_parts; ++p) {
             part_at(b + pb * p, cap, sw, &a.part[p]);
@@ -791,7 +803,6 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         cudaEventElapsedTime(&ms, e0, e1);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        cudaFreeAsync(blob, st);
         res->ms = ms;
         res->states = 0;
         for (const auto& x : res->stats) res->states += x.states;
@@ -812,8 +823,6 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
                      res->error, misc_h[0], misc_h[1] >> 32, misc_h[1] & 0xffffffffull);
             fprintf(stderr, "[mctb] %s\n", msg);
             set_error(msg);
-            cudaFreeAsync(pl.d_ids, st);
-            cudaStreamSynchronize(st);
             return MCTB_MODEL_BUG;
         }
         // explore.cpp:28-31: a visited set holding max_states refuses every later
@@ -835,7 +844,6 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         }
         break;
     }
-    cudaFreeAsync(pl.d_ids, st);
     MCTB_CUDA(cudaStreamSynchronize(st));
     return MCTB_OK;
 }
@@ -862,6 +870,18 @@ struct MpCtx {
     size_t smem = 0;
     int n_cfg = 0, size = 0, kernel = 0, plat[4] = {};
     std::vector<int32_t> configs;
+
+    ~MpCtx() {
+        for (int r = 0; r < kMaxParts; ++r)
+            if (peer[r]) cudaIpcCloseMemHandle(peer[r]);
+        if (local) cudaFree(local);
+        if (shared) cudaFree(shared);
+        if (pl.d_ids) cudaFreeAsync(pl.d_ids, st);
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+    }
 };
 
 }  // namespace mctb
@@ -960,7 +980,8 @@ int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* i
         set_error("no configurations");
         return MCTB_CONFIG_ERROR;
     }
-    auto* c = new MpCtx;
+    std::unique_ptr<MpCtx> holder(new MpCtx);  // every early return frees it (~MpCtx)
+    MpCtx* c = holder.get();
     c->world = world;
     c->rank = rank;
     c->n_cfg = n_configs;
@@ -969,10 +990,7 @@ int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* i
     for (int i = 0; i < 4; ++i) c->plat[i] = plat[i];
     c->configs.assign(configs, configs + 2 * n_configs);
     c->hs.resize(n_configs);
-    auto fail = [&](int code) {
-        delete c;
-        return code;
-    };
+    auto fail = [](int code) { return code; };
     for (int k = 0; k < n_configs; ++k) {
         if ((rc = check_machine(plat, size, kernel, configs[2 * k], configs[2 * k + 1]))) return fail(rc);
         if ((rc = build_desc(plat, size, kernel, input, configs[2 * k], configs[2 * k + 1], &c->hs[k])))
@@ -1006,7 +1024,7 @@ int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* i
     part_at(c->local, cap, c->pl.sw, &a.part[rank]);
     MCTB_CUDA(cudaStreamSynchronize(c->st));
     MCTB_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), c->local));
-    *ctx = c;
+    *ctx = holder.release();
     return MCTB_OK;
 }
 
@@ -1095,18 +1113,7 @@ int mctb_explore_mp_run(void* ctx, int64_t* out, int64_t* info) {
 }
 
 void mctb_explore_mp_close(void* ctx) {
-    auto* c = static_cast<MpCtx*>(ctx);
-    if (!c) return;
-    for (int r = 0; r < c->world; ++r)
-        if (c->peer[r]) cudaIpcCloseMemHandle(c->peer[r]);
-    if (c->local) cudaFree(c->local);
-    if (c->shared) cudaFree(c->shared);
-    if (c->pl.d_ids) cudaFreeAsync(c->pl.d_ids, c->st);
-    if (c->st) {
-        cudaStreamSynchronize(c->st);
-        cudaStreamDestroy(c->st);
-    }
-    delete c;
+    delete static_cast<MpCtx*>(ctx);  // ~MpCtx unmaps the peers and frees this rank's memory
 }
 
 }  // extern "C"
