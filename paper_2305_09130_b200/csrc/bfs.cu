@@ -76,6 +76,10 @@ struct BfsArgs {
 
 namespace {
 
+#ifndef MCTB_BFS_MAX_SLEEP
+#define MCTB_BFS_MAX_SLEEP 1024  // ns: longest back-off of an idle warp's queue poll
+#endif
+
 #ifndef MCTB_BFS_MINB
 #define MCTB_BFS_MINB 4  // resident blocks per SM the register allocation targets
 #endif
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                             break;
                         }
                         __nanosleep(ns);
-                        if (ns < 1024) ns <<= 1;
+                        if (ns < MCTB_BFS_MAX_SLEEP) ns <<= 1;
                     }
                 }
                 slot = __shfl_sync(0xffffffffu, slot, 0);
