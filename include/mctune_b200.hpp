@@ -669,6 +669,77 @@ inline std::vector<RankedTrail> rank_trails(const std::vector<Trace>& traces) {
     return out;
 }
 
+// ------------------------------------------------------------------ tuning spaces
+/// A tuning space beyond the reference's (wg, ts) grid: ranges over the
+/// platform shape too (nd, nu, log2 np) — the configuration loop of
+/// check_overtime (explore.cpp:171-200) as one exhaustive argmin kernel.
+/// Index order (least = preferred on ties): wg descending, ts descending, then
+/// np, nu, nd ascending; the reference's own space is Space::reference().
+struct Space {
+    KernelKind kernel = KernelKind::Abstract;
+    int size = 8, gmt = 4;
+    int nd_lo = 1, nd_hi = 1, nu_lo = 1, nu_hi = 1, log2np_lo = 2, log2np_hi = 2;
+    int log2wg_lo = 1, log2wg_hi = 0, log2ts_lo = 1, log2ts_hi = 0;  // hi 0: n - 1
+
+    static Space reference(const PlatformConfig& p, const ProblemSpec& prob) {
+        p.validate();
+        prob.validate();
+        Space s;
+        s.kernel = prob.kernel;
+        s.size = prob.size;
+        s.gmt = p.gmt;
+        s.nd_lo = s.nd_hi = p.nd;
+        s.nu_lo = s.nu_hi = p.nu;
+        s.log2np_lo = s.log2np_hi = log2_exact(p.np);
+        return s;
+    }
+    void desc(std::int64_t out[13]) const {
+        const int n = is_pow2(size) ? log2_exact(size) : 0;
+        const std::int64_t d[13] = {kernel == KernelKind::Minimum ? 1 : 0, size, gmt, nd_lo, nd_hi,
+                                    nu_lo, nu_hi, log2np_lo, log2np_hi, log2wg_lo,
+                                    log2wg_hi ? log2wg_hi : n - 1, log2ts_lo,
+                                    log2ts_hi ? log2ts_hi : n - 1};
+        std::copy(d, d + 13, out);
+    }
+    std::uint64_t count() const {
+        std::int64_t d[13];
+        desc(d);
+        const std::uint64_t n = mctb_space_count(d);
+        if (n == 0) detail::check(MCTB_CONFIG_ERROR);
+        return n;
+    }
+};
+
+struct SpaceResult {
+    std::uint64_t key = 0;   // (min(time, 2^30 - 1) << 33) | index
+    std::uint64_t index = 0;
+    Tick time = 0;
+    long long transitions = 0;
+    PlatformConfig platform;
+    TuningParams params;
+};
+
+/// The minimal-model-time configuration of [first, first + count) (count 0 =
+/// to the end of the space), ties to the smaller index: host buffers, one call.
+inline SpaceResult space_argmin(const Space& space, std::uint64_t first = 0,
+                                std::uint64_t count = 0) {
+    std::int64_t d[13];
+    space.desc(d);
+    if (count == 0) count = space.count() - first;
+    std::uint64_t key = 0;
+    std::int64_t out[8];
+    detail::check(mctb_space_argmin(d, first, count, &key, out));
+    SpaceResult r;
+    r.key = key;
+    r.index = key & ((1ull << MCTB_KEY_INDEX_BITS) - 1);
+    r.time = out[0];
+    r.transitions = out[1];
+    r.platform = PlatformConfig{static_cast<int>(out[2]), static_cast<int>(out[3]),
+                                static_cast<int>(out[4]), static_cast<int>(out[5])};
+    r.params = TuningParams{static_cast<int>(out[6]), static_cast<int>(out[7])};
+    return r;
+}
+
 /// Number of sm_100 devices the engine sees.
 inline int device_count() { return mctb_device_count(); }
 

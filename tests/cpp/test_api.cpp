@@ -105,3 +105,23 @@ TEST_CASE("swarm agrees with bisection at desk scale") {
     CHECK(again.trace.transitions == s.trace.transitions);
     CHECK_THROWS_AS(swarm_min_time(kPlat, problem, 0, ExploreLimits{}, 1), ConfigError);
 }
+
+TEST_CASE("tuning-space argmin: the reference's space and a generalised one") {
+    const ProblemSpec problem = ProblemSpec::abstract(64);
+    const SpaceResult r = mctune_b200::space_argmin(mctune_b200::Space::reference(kPlat, problem));
+    CHECK(r.time == 324);
+    CHECK(r.params == TuningParams{4, 32});
+    CHECK(r.platform == kPlat);
+    mctune_b200::Space g;
+    g.size = 1024;
+    g.gmt = 4;
+    g.nd_hi = 160000;
+    g.nu_hi = 64;
+    g.log2np_lo = 0;
+    g.log2np_hi = 9;
+    CHECK(g.count() == 8294400000ull);
+    const SpaceResult w = mctune_b200::space_argmin(g, 0, 1000000000ull);
+    CHECK(w.time == 5124);
+    CHECK(w.index == 92160000ull);
+    CHECK(w.params == TuningParams{512, 512});
+}
