@@ -493,8 +493,8 @@ ALU_PIPE_FRAC_NCU = 0.877
 # re-measured after every change of explore_kernel (profiles/).
 EXPLORE_SIZE = 64
 EXPLORE_PARAMS = (16, 2)
-EXPLORE_INST_PER_STATE = 1121.5
-EXPLORE_DRAM_BYTES_PER_STATE = 1057.8
+EXPLORE_INST_PER_STATE = 1066.1
+EXPLORE_DRAM_BYTES_PER_STATE = 1052.3
 
 
 def main():
