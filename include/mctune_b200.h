@@ -180,6 +180,12 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
               uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
               int64_t* trace_len, double* info);
 
+/* The bound-lowering probes of the last mctb_tune on the calling thread, in
+ * order: rows = int64[8 * cap] {T, violated, exhaustive, states_visited, wg, ts,
+ * final_time, steps} (the counterexample check_overtime(T) returns for a violated
+ * bound — its full trace is mctb_check_overtime(T)).  Returns the probe count. */
+int64_t mctb_tune_probes(int64_t* rows, int64_t cap);
+
 /* swarm_min_time (search.hpp:373-379) re-designed as rounds of per_round Philox
  * trajectories over every feasible configuration (max_rounds bounds the rounds).
  * out = int64[10]: {t_min, wg, ts, t_ini, rounds, transitions_total, first_trail_time,

@@ -13,7 +13,7 @@ from .model import (ABSTRACT, MINIMUM, LaunchPlan, PlatformConfig, ProblemSpec, 
 from .machine import (FIRST, MT19937, PHILOX, ROUND_ROBIN, SEEDED_RANDOM, Machine, RunOutcome,
                       Trace, TrajectoryBatch, replay, trace_to_text, trajectories)
 from .explore import ExploreStats, SweepInfo, explore_configs, explore_machine
-from .search import (RankedTrail, SweepRow, TuneResult, Verdict, bisect_min_time, check_overtime,
+from .search import (RankedTrail, SweepRow, TuneProbe, TuneResult, Verdict, bisect_min_time, check_overtime,
                      exhaustive_sweep, extract_params, rank_trails, swarm_min_time, tune)
 from . import report
 from .space import KEY_INDEX_BITS, KEY_SAT, KEY_TIME_BITS, Space, SpaceResult, space_argmin
@@ -26,6 +26,6 @@ __all__ = [
     "KEY_TIME_BITS", "config_feasible", "derive_launch", "device_count", "enumerate_configs",
     "exhaustive_sweep", "kernel_kind_from_string", "log2_exact", "space_argmin",
     "validate_params", "FIRST", "MT19937", "PHILOX", "ROUND_ROBIN", "SEEDED_RANDOM", "Machine",
-    "RunOutcome", "RankedTrail", "TuneResult", "Verdict", "bisect_min_time", "check_overtime",
+    "RunOutcome", "RankedTrail", "TuneProbe", "TuneResult", "Verdict", "bisect_min_time", "check_overtime",
     "extract_params", "rank_trails", "swarm_min_time", "tune", "ExploreStats", "SweepInfo", "explore_configs", "explore_machine", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
 ]

@@ -122,3 +122,6 @@ lib.mctb_explore_mp_close.argtypes = [vp]
 lib.mctb_explore_mp_close.restype = None
 EXPORTED += ["mctb_explore_mp_open", "mctb_explore_mp_connect", "mctb_explore_mp_seed",
              "mctb_explore_mp_run", "mctb_explore_mp_close"]
+lib.mctb_tune_probes.argtypes = [i64p, C.c_int64]
+lib.mctb_tune_probes.restype = C.c_int64
+EXPORTED.append("mctb_tune_probes")

@@ -331,6 +331,16 @@ int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* in
     return emit_trace(c, v, trace, cap, trace_len);
 }
 
+// Per-bound verdicts of the last mctb_tune on this thread (mctb_tune_probes).
+static thread_local std::vector<int64_t> g_probes;
+
+static void record_probe(int64_t T, const VerdictOut& v, const Ctx& c) {
+    const int64_t row[8] = {T, v.violated ? 1 : 0, v.exhaustive ? 1 : 0, v.states,
+                            v.violated ? c.wg[v.cfg] : 0, v.violated ? c.ts[v.cfg] : 0,
+                            v.violated ? v.final_time : -1, v.violated ? v.steps : -1};
+    g_probes.insert(g_probes.end(), row, row + 8);
+}
+
 // estimate_initial_time + bisect_min_time: the `tune` flow (tools/main.cpp:301-304).
 // t_hi <= 0 selects estimate_initial_time(seed).
 // out = {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total, first_trail_time,
@@ -371,11 +381,13 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         return MCTB_CONFIG_ERROR;
     }
     // search.cpp:106-160
+    g_probes.clear();
     int checks = 0;
     int64_t states_total = 0;
     bool proven = true;
     VerdictOut v = verdict(c, t_hi, &rc);
     if (rc) return rc;
+    record_probe(t_hi, v, c);
     ++checks;
     states_total += v.states;
     if (!v.violated) {
@@ -390,6 +402,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         const int64_t mid = lo + (hi - lo) / 2;
         const VerdictOut vm = verdict(c, mid, &rc);
         if (rc) return rc;
+        record_probe(mid, vm, c);
         ++checks;
         states_total += vm.states;
         if (vm.violated) {
@@ -404,6 +417,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     if (!lo_checked && lo == 0 && hi == 1) {
         const VerdictOut vz = verdict(c, 0, &rc);
         if (rc) return rc;
+        record_probe(0, vz, c);
         ++checks;
         if (vz.violated) {
             set_error("a run finished in zero ticks");
@@ -426,6 +440,14 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         info[4] = c.bfs.ms;  // exploration kernel time (CUDA events)
     }
     return emit_trace(c, best, trace, cap, trace_len);
+}
+
+int64_t mctb_tune_probes(int64_t* rows, int64_t cap) {
+    const int64_t n = (int64_t)(g_probes.size() / 8);
+    if (rows)
+        for (int64_t i = 0; i < std::min(n, cap); ++i)
+            std::memcpy(rows + 8 * i, g_probes.data() + 8 * i, 8 * sizeof(int64_t));
+    return n;
 }
 
 }  // extern "C"

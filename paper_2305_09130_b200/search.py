@@ -88,6 +88,20 @@ class TuneStats:
 
 
 @dataclass
+class TuneProbe:
+    """One bound of the bisection: check_overtime(T)'s verdict (explore.hpp:95-101)
+    and, when violated, its counterexample's configuration, time and length."""
+    T: int
+    violated: bool
+    exhaustive: bool
+    states_visited: int
+    wg: int
+    ts: int
+    final_time: int
+    steps: int
+
+
+@dataclass
 class TuneResult:
     """(search.hpp:330-342)"""
     t_min: int
@@ -100,6 +114,7 @@ class TuneResult:
     first_trail_time: int
     trace_exact: bool = True
     timings_ms: dict = None
+    probes: list = None  # TuneProbe per bisection bound (bisect/tune only)
 
     def first_trail_optimality(self) -> float:
         if self.first_trail_time <= 0:
@@ -142,11 +157,17 @@ def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: in
                         info))
     wall = _time.perf_counter() - t0
     trace = _trace_from(buf, n.value, out[0], out[1], out[2])
-    return TuneResult(out[0], TuningParams(out[1], out[2]), trace, out[3],
-                      TuneStats(out[5], out[6], wall), "bisect", bool(out[4]), out[7],
-                      bool(out[9]), {"cost_model": info[0], "first_paths": info[1],
-                                     "exploration": info[2], "explored_states": info[3],
-                                     "exploration_kernel": info[4]})
+    res = TuneResult(out[0], TuningParams(out[1], out[2]), trace, out[3],
+                     TuneStats(out[5], out[6], wall), "bisect", bool(out[4]), out[7],
+                     bool(out[9]), {"cost_model": info[0], "first_paths": info[1],
+                                    "exploration": info[2], "explored_states": info[3],
+                                    "exploration_kernel": info[4]})
+    # the bound-lowering probes, in order: one check_overtime(T) verdict each
+    k = lib.mctb_tune_probes(None, 0)
+    rows = (C.c_int64 * (8 * max(k, 1)))()
+    lib.mctb_tune_probes(rows, k)
+    res.probes = [TuneProbe(*rows[8 * i:8 * i + 8]) for i in range(k)]
+    return res
 
 
 def bisect_min_time(platform: PlatformConfig, problem: ProblemSpec, t_hi: int,

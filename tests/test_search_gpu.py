@@ -138,3 +138,25 @@ def test_schedule_dependent_counterexamples(engine, gold):
             c["states"], c["transitions"]), key
     for c in g["tunes"]:
         _tune_matches(m, c)
+
+
+def test_tune_probes_are_the_per_bound_checks(engine, gold):
+    """Every bound the bisection probes is reported with the verdict and the
+    counterexample check_overtime(T) returns on its own (the reference's per-bound
+    counterexamples), and they add up to checks_run / states_visited_total."""
+    m = engine
+    for c in gold("tune.json")[:8]:
+        plat = m.PlatformConfig(*c["plat"])
+        prob = (m.ProblemSpec.abstract(c["size"]) if c["kernel"] == 0
+                else m.ProblemSpec.minimum(c["size"]))
+        r = m.tune(plat, prob, seed=1)
+        assert len(r.probes) == r.stats.checks_run
+        assert sum(p.states_visited for p in r.probes) == r.stats.states_visited_total
+        assert r.probes[0].T == r.t_ini and r.probes[0].final_time == r.first_trail_time
+        for p in r.probes:
+            v = m.check_overtime(plat, prob, p.T)
+            assert (p.violated, p.exhaustive, p.states_visited) == (
+                v.violated, v.exhaustive, v.stats.states_visited), (c, p.T)
+            if v.violated:
+                assert (p.wg, p.ts, p.final_time, p.steps) == (
+                    v.trace.params.wg, v.trace.params.ts, v.trace.final_time, v.trace.steps)
