@@ -356,8 +356,9 @@ __host__ __device__ inline void write_unit(uint32_t* row, const Layout& l, int g
 }
 
 // In-place successors for the transitions behind the combinatorial state
-// explosion: an element reporting a busy tick or arriving at its barrier, and
-// the unit <-> element handshakes (activation, item done, group done, stop).
+// explosion: an element reporting a busy tick or arriving at its barrier, the
+// unit <-> element handshakes (activation, item done, group done, stop), and the
+// clock tick (one record per reported element: the chain step of deep graphs).
 // They touch one element record, its unit record and at most one header field;
 // the new values follow Machine::apply (machine.cpp:479-500, 518-530, 541-551,
 // 569-580, 618-646) and are written over the parent's packed words.  `tr` is in
@@ -369,6 +370,25 @@ __host__ __device__ inline bool fast_successor(const BfsDesc& d, const MState& s
     const Layout& l = d.l;
     const MachDesc& m = d.m;
     switch (tr.op) {
+        case OP_CLOCKTICK: {
+            // machine.cpp ClockTick (machine.cuh apply): time + 1, nrp_work = 0, and
+            // every reported element un-reports and burns one busy tick, advancing
+            // its cursor when the tick was its last (the enumeration only offers
+            // the tick when nrp_work == all_nwe, i.e. every busy element reported)
+            set_bits_h(row, l.cfg, l.time, (uint32_t)(s.time + 1), hk, H);
+            set_bits_h(row, l.off_nrp, l.nrp, 0u, hk, H);
+            for (int p = 0; p < m.n_pex; ++p) {
+                if (!s.pex[p].reported) continue;
+                PexS px = s.pex[p];
+                px.reported = 0;
+                if (--px.busy_left == 0) {
+                    px.cursor += 1;
+                    place_pex(m, px);
+                }
+                write_pex(row, l, p, px, hk, H);
+            }
+            return true;
+        }
         case OP_PEXREPORT: {
             const int off = l.off_pex + tr.actor * l.pex_bits + l.poff_reported;
             const int i = div31(off);
