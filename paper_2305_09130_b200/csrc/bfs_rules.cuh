@@ -357,8 +357,9 @@ __host__ __device__ inline void write_unit(uint32_t* row, const Layout& l, int g
 
 // In-place successors for the transitions behind the combinatorial state
 // explosion: an element reporting a busy tick or arriving at its barrier, the
-// unit <-> element handshakes (activation, item done, group done, stop), and the
-// clock tick (one record per reported element: the chain step of deep graphs).
+// unit <-> element handshakes (activation, item done, group done, stop), the
+// clock tick and the barrier release (one record per element concerned: the
+// chain steps of deep graphs).
 // They touch one element record, its unit record and at most one header field;
 // the new values follow Machine::apply (machine.cpp:479-500, 518-530, 541-551,
 // 569-580, 618-646) and are written over the parent's packed words.  `tr` is in
@@ -386,6 +387,38 @@ __host__ __device__ inline bool fast_successor(const BfsDesc& d, const MState& s
                     place_pex(m, px);
                 }
                 write_pex(row, l, p, px, hk, H);
+            }
+            return true;
+        }
+        case OP_BARRIERRELEASE: {
+            // machine.cpp BarrierRelease (machine.cuh apply): the count resets; a
+            // barrier releases its elements to their next instruction, a group end
+            // sends them to SENDENDDONE (element 0 of the minimum kernel starts the
+            // epilogue) and retires nwe - 1 of the working elements
+            const int g = tr.actor, p0 = g * m.nwe;
+            int wk = 0, wge = 0;
+            for (int e = 0; e < m.nwe; ++e) {
+                wk += s.pex[p0 + e].pc == P_WAITBARRIER;
+                wge += s.pex[p0 + e].pc == P_WAITGROUPEND;
+            }
+            if (wk != m.nwe && wge != m.nwe) return false;  // apply() reports the bug
+            set_bits_h(row, l.off_units + g * l.unit_bits + l.uoff_bcount, l.bcount, 0u, hk, H);
+            if (wge == m.nwe)
+                set_bits_h(row, l.off_nrp + l.nrp, l.allnwe, (uint32_t)(s.all_nwe - (m.nwe - 1)),
+                           hk, H);
+            for (int e = 0; e < m.nwe; ++e) {
+                PexS px = s.pex[p0 + e];
+                if (wk == m.nwe) {
+                    px.cursor += 1;
+                    place_pex(m, px);
+                } else if (e == 0 && has_epilogue(m)) {
+                    px.phase = 1;
+                    px.cursor = 0;
+                    place_pex(m, px);
+                } else {
+                    px.pc = P_SENDENDDONE;
+                }
+                write_pex(row, l, p0 + e, px, hk, H);
             }
             return true;
         }
