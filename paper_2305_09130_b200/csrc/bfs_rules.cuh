@@ -422,6 +422,43 @@ __host__ __device__ inline bool fast_successor(const BfsDesc& d, const MState& s
             }
             return true;
         }
+        case OP_PEXEFFECT: {
+            // machine.cpp PexEffect (machine.cuh apply), minimum kernel: min-combine a
+            // global item, a neighbour's slot, or (publish) the element's slot into
+            // glob[0]; then the next instruction
+            const int p = tr.actor, g = p >> m.lognwe, me = p - g * m.nwe;
+            const int slot = g * m.np + me;  // myloc, machine.hpp:205
+            PexS px = s.pex[p];
+            const Instr in = instr_at(m, px.phase, px.cursor);
+            int32_t v, cur;
+            int off, width;
+            const int off_glob0 = l.cfg + l.time + l.nrp + l.allnwe + 1 + l.nextwg + 3 + l.hostk + 1;
+            if (px.phase == 0) {
+                const int gid = m.wg > m.np ? px.nwg * m.wg + me + px.iter * m.np : px.nwg * m.wg + me;
+                const int idx = gid * m.ts + in.src;
+                if (idx < 0 || idx >= m.size) return false;  // apply() reports the bug
+                v = idx == 0 ? s.glob0 : m.input_id[idx];
+                cur = s.loc[slot];
+                off = l.off_loc + slot * l.loc;
+                width = l.loc;
+            } else if (in.src > 0) {
+                if (slot + in.src >= m.n_units * m.np) return false;
+                v = s.loc[slot + in.src];
+                cur = s.loc[slot];
+                off = l.off_loc + slot * l.loc;
+                width = l.loc;
+            } else {
+                v = s.loc[slot];
+                cur = s.glob0;
+                off = off_glob0;
+                width = l.glob0;
+            }
+            if (v < cur) set_bits_h(row, off, width, (uint32_t)v, hk, H);
+            px.cursor += 1;
+            place_pex(m, px);
+            write_pex(row, l, p, px, hk, H);
+            return true;
+        }
         case OP_PEXREPORT: {
             const int off = l.off_pex + tr.actor * l.pex_bits + l.poff_reported;
             const int i = div31(off);
