@@ -24,10 +24,11 @@
 // are explored in the same sweep, tagged by a cfg field of the packed state;
 // per-configuration statistics give the reference's ExploreStats.
 #include <algorithm>
-#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "bfs.cuh"
@@ -707,6 +708,87 @@ static int seed_launch(const BfsPlan& pl, const BfsArgs& a, bool sys, const std:
     return MCTB_OK;
 }
 
+// The visited tables live in one per-device buffer reused across sweeps:
+// cudaMalloc maps even 32 GB in a few ms, while growing the stream-ordered pool
+// cost ~80 ms per GB (B200), more than most sweeps take.  A sweep leases the
+// cached buffer when it is large enough, else allocates its own; on return the
+// larger of the two stays cached.
+namespace {
+struct TableCache {
+    std::mutex mu;
+    void* p[64] = {};
+    size_t bytes[64] = {};
+};
+TableCache& table_cache() {
+    static TableCache c;
+    return c;
+}
+}  // namespace
+
+static int table_lease(size_t bytes, void** out, size_t* got) {
+    int dev = 0;
+    MCTB_CUDA(cudaGetDevice(&dev));
+    TableCache& c = table_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.p[dev] && c.bytes[dev] >= bytes) {
+            *out = c.p[dev];
+            *got = c.bytes[dev];
+            c.p[dev] = nullptr;
+            c.bytes[dev] = 0;
+            return MCTB_OK;
+        }
+    }
+    if (cudaMalloc(out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        // the cached (smaller) buffer may be what is missing: release it and retry
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.p[dev]) {
+            cudaFree(c.p[dev]);
+            c.p[dev] = nullptr;
+            c.bytes[dev] = 0;
+        }
+        MCTB_CUDA(cudaMalloc(out, bytes));
+    }
+    *got = bytes;
+    return MCTB_OK;
+}
+
+static void table_return(void* p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    TableCache& c = table_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.p[dev] || c.bytes[dev] < bytes) {
+        if (c.p[dev]) cudaFree(c.p[dev]);
+        c.p[dev] = p;
+        c.bytes[dev] = bytes;
+    } else {
+        cudaFree(p);
+    }
+}
+
+static size_t table_cached_bytes() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    TableCache& c = table_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    return c.bytes[dev];
+}
+
+// A leased table buffer, returned when the attempt ends (after its stream drains).
+struct TableLease {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t st = nullptr;
+    ~TableLease() {
+        if (p) {
+            cudaStreamSynchronize(st);
+            table_return(p, bytes);
+        }
+    }
+};
+
 // Stream-ordered free at scope exit (every early error return included).
 struct AsyncFree {
     void* p;
@@ -734,6 +816,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     if ((rc = bfs_grid(kern, sw, &grid, &dyn_smem))) return rc;
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    free_b += table_cached_bytes();  // the cached table buffer is ours to reuse
     const double slot_bytes = 4.0 * sw + 2.0;  // slot line + queue (half the slots)
     // capacity grows 16x on overflow; the sweep restarts (all counts are rebuilt)
     // first capacity: enough for the bound up to 2^29 slots (a restart loses the
@@ -772,10 +855,10 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.n_here = n_parts;
         size_t misc_off = 0;
         const size_t pb = (part_bytes(cap, sw, &misc_off) + 255) & ~(size_t)255;
-        void* blob = nullptr;
-        MCTB_CUDA(cudaMallocAsync(&blob, pb * n_parts + shared_bytes(pl), st));
-        const AsyncFree blob_guard{blob, st};  // freed when this attempt ends
-        char* b = (char*)blob;
+        TableLease lease;  // returned to the cache when this attempt ends
+        lease.st = st;
+        if ((rc = table_lease(pb * n_parts + shared_bytes(pl), &lease.p, &lease.bytes))) return rc;
+        char* b = (char*)lease.p;
         for (int p = 0; p < n_parts; ++p) {
             part_at(b + pb * p, cap, sw, &a.part[p]);
             if ((rc = part_clear(b + pb * p, cap, sw, st))) return rc;
