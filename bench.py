@@ -454,12 +454,14 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
                                C.c_uint64(0), C.c_uint64(ntr), C.c_int64(200_000_000), outb)
     el = time.perf_counter() - t0
     assert rc == 0
+    kern_ms = lib.mctb_trajectories_kernel_ms()
     steps = sum(outb[1::6][:ntr])
     out["swarm"] = {"workload": "1e6 Philox4x32-10 schedule trajectories, abstract kernel, size 16, "
                                 "(1,1,4,4), all 9 configurations, through mctb_trajectories "
                                 "(host buffers: per-trajectory time, transitions, result, status, "
                                 "trace hash copied back)",
                     "seconds": el, "trajectories_per_s": ntr / el,
+                    "kernel_ms": kern_ms, "trajectories_per_s_kernel": ntr / (kern_ms * 1e-3),
                     "transitions_per_s": steps / el, "min_time": min(outb[0::6][:ntr])}
     if with_reference:
         # the same trajectories replayed by the CPU port (oracle, all host cores)

@@ -113,6 +113,9 @@ int mctb_simulate(const int* plat, int size, int kernel, const int64_t* input, i
 int mctb_trajectories(const int* plat, int size, int kernel, const int64_t* input,
                       const int32_t* configs, int n_configs, int policy, uint64_t seed,
                       uint64_t traj0, uint64_t n_traj, int64_t max_steps, int64_t* out);
+/* Device time (CUDA events on the launching stream) of the trajectory kernel of this
+ * thread's last mctb_trajectories call, in ms (the call's rate without its copies). */
+double mctb_trajectories_kernel_ms(void);
 
 /* replay (explore.hpp:301-304, explore.cpp:283-300) on the GPU; out = {final_time, result} */
 int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,

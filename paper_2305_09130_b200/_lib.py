@@ -71,6 +71,8 @@ lib.mctb_simulate.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.
                               C.c_uint64, C.c_uint64, i64p, i32p, C.c_int64, i64p]
 lib.mctb_trajectories.argtypes = [i32p, C.c_int, C.c_int, i64p, i32p, C.c_int, C.c_int,
                                   C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, i64p]
+lib.mctb_trajectories_kernel_ms.argtypes = []
+lib.mctb_trajectories_kernel_ms.restype = C.c_double
 lib.mctb_replay.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, i32p, C.c_int64,
                             C.c_int64, i64p]
 lib.mctb_trace_text.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, i32p, C.c_int64,
@@ -81,7 +83,7 @@ EXPORTED = [
     "mctb_last_error", "mctb_version", "mctb_device_count", "mctb_derive_launch",
     "mctb_space_count", "mctb_space_argmin_async", "mctb_space_argmin",
     "mctb_space_eval_async", "mctb_sweep", "mctb_int32_peak", "mctb_simulate",
-    "mctb_trajectories", "mctb_replay", "mctb_trace_text",
+    "mctb_trajectories", "mctb_trajectories_kernel_ms", "mctb_replay", "mctb_trace_text",
 ]
 
 

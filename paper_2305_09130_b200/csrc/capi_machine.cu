@@ -89,6 +89,8 @@ std::string label(const MachDesc& m, const Transition& t) {
     return "?";
 }
 
+thread_local double g_traj_kernel_ms = 0.0;  // last mctb_trajectories kernel time
+
 int stream_of(cudaStream_t* s) {
     static thread_local cudaStream_t st = nullptr;
     if (!st) MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -231,24 +233,35 @@ int mctb_trajectories(const int* plat, int size, int kernel, const int64_t* inpu
     MCTB_CUDA(cudaMemcpyAsync(desc.p, descs.data(), n_configs * sizeof(MachDesc),
                               cudaMemcpyHostToDevice, st));
     MCTB_CUDA(cudaMallocAsync(&o.p, std::max<uint64_t>(n_traj, 1) * sizeof(TrajOut), st));
+    DevBuf rec{nullptr, st};
+    MCTB_CUDA(cudaMallocAsync(&rec.p, std::max<uint64_t>(n_traj, 1) * 6 * sizeof(int64_t), st));
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (!ev[0]) {
+        MCTB_CUDA(cudaEventCreate(&ev[0]));
+        MCTB_CUDA(cudaEventCreate(&ev[1]));
+    }
+    MCTB_CUDA(cudaEventRecord(ev[0], st));
     if ((rc = launch_trajectories((MachDesc*)desc.p, n_configs, policy, seed, traj0, n_traj,
                                   max_steps, (TrajOut*)o.p, nullptr, 0, st)))
         return rc;
-    std::vector<TrajOut> h(n_traj);
-    MCTB_CUDA(cudaMemcpyAsync(h.data(), o.p, n_traj * sizeof(TrajOut), cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaEventRecord(ev[1], st));
+    // the records are formatted on the device and land in the caller's buffer
+    // with one copy (no host staging or per-record host loop)
+    if ((rc = launch_traj_records((TrajOut*)o.p, n_traj, kernel, (int64_t*)rec.p, st))) return rc;
+    MCTB_CUDA(cudaMemcpyAsync(out, rec.p, n_traj * 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     MCTB_CUDA(cudaStreamSynchronize(st));
-    for (uint64_t i = 0; i < n_traj; ++i) {
-        const TrajOut& t = h[i];
-        int64_t* r = out + 6 * i;
-        r[0] = t.time;
-        r[1] = t.steps;
-        r[2] = kernel == 1 ? hs[t.config].value(t.glob0) : INT64_MIN;
-        r[3] = t.status;
-        r[4] = (int64_t)t.hash;
-        r[5] = t.config;
-    }
+    float ms = 0.f;
+    MCTB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    g_traj_kernel_ms = ms;
+    if (kernel == 1)
+        for (uint64_t i = 0; i < n_traj; ++i) {
+            int64_t* r = out + 6 * i;
+            r[2] = hs[r[5]].value((int32_t)r[2]);
+        }
     return MCTB_OK;
 }
+
+double mctb_trajectories_kernel_ms(void) { return g_traj_kernel_ms; }
 
 int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
                 const int32_t* trace, int64_t len, int64_t final_time, int64_t* out) {

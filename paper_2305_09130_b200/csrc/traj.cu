@@ -62,8 +62,12 @@ __host__ __device__ inline uint64_t fnv_transition(uint64_t h, const Transition&
 
 namespace {
 
+#ifndef MCTB_TRAJ_MINB
+#define MCTB_TRAJ_MINB 12  // resident blocks per SM the register allocation targets (40 registers;
+                            // 1 -> 64 registers: 24.1 ms, 12: 15.9 ms, 16: 15.7 ms per 1e6 trajectories)
+#endif
 template <int POLICY>
-__global__ void __launch_bounds__(128) traj_kernel(const MachDesc* __restrict__ descs, int n_desc,
+__global__ void __launch_bounds__(128, MCTB_TRAJ_MINB) traj_kernel(const MachDesc* __restrict__ descs, int n_desc,
                                                    uint64_t seed, uint64_t traj0, uint64_t n_traj,
                                                    int64_t max_steps, TrajOut* __restrict__ out,
                                                    int32_t* __restrict__ trace, int64_t trace_cap) {
@@ -291,6 +295,31 @@ int launch_trajectories(const MachDesc* d_descs, int n_desc, int policy, uint64_
             return MCTB_CONFIG_ERROR;
     }
     return cuda_check(cudaGetLastError(), "traj_kernel");
+}
+
+// TrajOut -> the C ABI's int64[6] records {time, steps, result, status, hash, config}
+// on the device, so the host receives the caller's layout in one copy (result:
+// the glob[0] value id for the minimum kernel, mapped to its value by the host;
+// INT64_MIN for the abstract kernel).
+__global__ void traj_records_kernel(const TrajOut* __restrict__ in, uint64_t n, int kernel,
+                                    int64_t* __restrict__ rec) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const TrajOut t = in[i];
+    int64_t* r = rec + 6 * i;
+    r[0] = t.time;
+    r[1] = t.steps;
+    r[2] = kernel == 1 ? (int64_t)t.glob0 : INT64_MIN;
+    r[3] = t.status;
+    r[4] = (int64_t)t.hash;
+    r[5] = t.config;
+}
+
+int launch_traj_records(const TrajOut* d_in, uint64_t n, int kernel, int64_t* d_rec,
+                        cudaStream_t stream) {
+    if (n == 0) return MCTB_OK;
+    traj_records_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_in, n, kernel, d_rec);
+    return cuda_check(cudaGetLastError(), "traj_records_kernel");
 }
 
 int launch_replay(const MachDesc& m, const int32_t* d_trace, int64_t len, int64_t* d_step_time,

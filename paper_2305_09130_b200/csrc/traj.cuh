@@ -61,6 +61,8 @@ int upload_desc(MachHost& h, cudaStream_t stream, int32_t** d_ids);
 int launch_trajectories(const MachDesc* d_descs, int n_desc, int policy, uint64_t seed,
                         uint64_t traj0, uint64_t n_traj, int64_t max_steps, TrajOut* d_out,
                         int32_t* d_trace, int64_t trace_cap, cudaStream_t stream);
+int launch_traj_records(const TrajOut* d_in, uint64_t n, int kernel, int64_t* d_rec,
+                        cudaStream_t stream);
 int launch_replay(const MachDesc& m, const int32_t* d_trace, int64_t len, int64_t* d_step_time,
                   TrajOut* d_out, cudaStream_t stream);
 

@@ -17,4 +17,5 @@ for rep in range(2):
                                C.c_uint64(0), C.c_uint64(ntr), C.c_int64(200_000_000), outb)
     el = time.perf_counter() - t0
     steps = sum(outb[1::6][:ntr])
-    print('rc', rc, 'traj/s', ntr / el, 'transitions/s', steps / el, 'steps/traj', steps / ntr, flush=True)
+    kms = lib.mctb_trajectories_kernel_ms()
+    print('rc', rc, 'kernel_ms', kms, 'kernel traj/s', ntr / (kms * 1e-3), 'traj/s', ntr / el, 'transitions/s', steps / el, 'steps/traj', steps / ntr, flush=True)
