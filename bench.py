@@ -484,19 +484,19 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
 
 # Thread-level instructions executed per configuration by space_argmin_kernel<0>
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
-# (profiles/r01_argmin_v5_ncu.txt).  Re-measured after every kernel change.
-INT_OPS_PER_CONFIG = 14.67
+# (profiles/r01_argmin_v7_ncu.txt).  Re-measured after every kernel change.
+INT_OPS_PER_CONFIG = 12.16
 # the binding pipe of that kernel in the same capture:
 # sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active
-ALU_PIPE_FRAC_NCU = 0.877
+ALU_PIPE_FRAC_NCU = 0.832
 
 # configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
 # state (smsp__inst_executed.sum / states; DRAM read + write bytes / states),
 # re-measured after every change of explore_kernel (profiles/).
 EXPLORE_SIZE = 64
 EXPLORE_PARAMS = (16, 2)
-EXPLORE_INST_PER_STATE = 1066.1
-EXPLORE_DRAM_BYTES_PER_STATE = 1052.3
+EXPLORE_INST_PER_STATE = 1071.9  # profiles/r01_explore_v8_ncu.txt
+EXPLORE_DRAM_BYTES_PER_STATE = 1038.8
 
 
 def main():

@@ -51,6 +51,13 @@ __device__ __forceinline__ void cta_min_commit(uint64_t key, unsigned long long*
     }
 }
 
+// a * b + c with a multiplier unknown to ptxas: stays an IMAD (FMA pipe)
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
 template <int KERNEL>
 __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uint64_t first,
                                                                 uint64_t count,
@@ -145,13 +152,14 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                         best_tf = tf;
                         best_k = k;
                     }
-                    // nd -> nd + 1: dm = Q (nd+1) + (R - Q), at most one correction
+                    // nd -> nd + 1: dm = Q (nd+1) + (R - Q), at most one correction,
+                    // applied as c * nd with c = (R < 0) in {0, 1}: one IMAD (FMA pipe)
+                    // in place of a mask and an add on the saturated ALU pipe
                     ++nd;
                     R -= (int32_t)Q;
-                    if (R < 0) {
-                        Q -= 1;
-                        R += (int32_t)nd;
-                    }
+                    const uint32_t c = (uint32_t)R >> 31;
+                    Q -= c;
+                    R = (int32_t)mad_u32(c, nd, (uint32_t)R);
                 }
                 if (best_k != 0xffffffffu) best_idx = base + best_k;
             }
@@ -290,9 +298,14 @@ int launch_space_argmin(const SpaceDev& s, uint64_t first, uint64_t count, uint6
         return MCTB_CONFIG_ERROR;
     }
     if (count == 0) return MCTB_OK;
-    // persistent-style grid: 8 CTAs of 256 threads per SM, each thread a
-    // contiguous run of >= 16 indices
-    const uint64_t max_threads = (uint64_t)sm_count() * 8 * kThreads;
+    // 64 CTAs of 256 threads per SM (8 waves of the 8 resident CTAs), each thread a
+    // contiguous run of >= 16 indices.  Threads' costs differ (exact division for
+    // small nd, odometer carries), so one resident wave of long runs left half the
+    // warps idle at the tail; the hardware CTA scheduler balances the finer grid.
+    // configs[4] per step (1e9): 8 CTAs/SM 0.50 ms, 16 0.44, 32 0.40, 64 0.385,
+    // 128 0.40, 256 0.45
+    constexpr int kCtasPerSm = 64;
+    const uint64_t max_threads = (uint64_t)sm_count() * kCtasPerSm * kThreads;
     uint64_t per_thread = (count + max_threads - 1) / max_threads;
     if (per_thread < 16) per_thread = 16;
     const uint64_t threads = (count + per_thread - 1) / per_thread;
