@@ -5,12 +5,12 @@
  * Each entry point replaces one interface of the reference C++ core
  * (/root/reference/proj/include/mctune/{model,explore,search}.hpp); the citation is on the
  * declaration.  Conventions shared by all calls:
- *   plat   : int[4] = {nd, nu, np, gmt}                 (model.hpp:37-44 PlatformConfig)
- *   size   : input length, a power of two >= 4           (model.hpp:53-64 ProblemSpec)
- *   kernel : 0 = abstract, 1 = minimum                   (model.hpp:46 KernelKind)
+ *   plat   : int[4] = {nd, nu, np, gmt}                 (model.hpp:33-40 PlatformConfig)
+ *   size   : input length, a power of two >= 4           (model.hpp:48-58 ProblemSpec)
+ *   kernel : 0 = abstract, 1 = minimum                   (model.hpp:42 KernelKind)
  *   input  : int64[size] or NULL (minimum kernel; NULL = glob[i] = size - i)
  *   trace  : int32[4 * cap], one transition = {actor, peer, op, arg}
- *            (machine.hpp:78-88 Transition; op = ordinal of mctune::Op)
+ *            (machine.hpp:76-84 Transition; op = ordinal of mctune::Op)
  *   return : MCTB_OK, or the error class of the reference exception
  *            (ConfigError -> MCTB_CONFIG_ERROR, ModelBug -> MCTB_MODEL_BUG,
  *             CorruptTrace -> MCTB_CORRUPT_TRACE); text via mctb_last_error().
@@ -34,7 +34,7 @@ extern "C" {
 #define MCTB_NO_DEVICE 5
 #define MCTB_CUDA_ERROR 6
 
-/* scheduling policies for mctb_simulate (machine.hpp:219 SchedPolicy + ours) */
+/* scheduling policies for mctb_simulate (machine.hpp:143 SchedPolicy + ours) */
 #define MCTB_POLICY_ROUND_ROBIN 0 /* SchedPolicy::RoundRobin */
 #define MCTB_POLICY_MT19937 1     /* SchedPolicy::SeededRandom (std::mt19937_64) */
 #define MCTB_POLICY_FIRST 2       /* first enabled: the first DFS path of explore_machine */
@@ -50,7 +50,7 @@ int mctb_version(void);
 /* number of sm_100 devices visible (0 -> every compute call fails with MCTB_NO_DEVICE) */
 int mctb_device_count(void);
 
-/* derive_launch (model.hpp:75, model.cpp:161-177); out = {wgs, nwd, nwu, nwe, all_nwe} */
+/* derive_launch (model.hpp:89, model.cpp:72-88); out = {wgs, nwd, nwu, nwe, all_nwe} */
 int mctb_derive_launch(const int* plat, int size, int wg, int ts, int* out);
 
 /* ---------------------------------------------------------------------------
@@ -60,7 +60,7 @@ int mctb_derive_launch(const int* plat, int size, int wg, int ts, int* out);
  *    log2np_lo, log2np_hi, log2wg_lo, log2wg_hi, log2ts_lo, log2ts_hi}
  * Index order (least index = preferred on ties): wg descending, ts descending,
  * then np, nu, nd ascending — for a single platform this is exactly the
- * reference's preference "largest wg, then largest ts" (search.hpp:367-369,
+ * reference's preference "largest wg, then largest ts" (search.hpp:60-61,
  * explore.cpp:64-72).  The reference's own space for (plat, size) is
  *   {kernel, size, gmt, nd, nd, nu, nu, log2 np, log2 np, 1, n-1, 1, n-1}.
  */
@@ -91,13 +91,13 @@ int mctb_int32_peak(double* ops_per_sec, double* ms);
  * Reference-compatible drivers (host buffers).
  */
 
-/* exhaustive_sweep (search.hpp:384, search.cpp:214-246).
+/* exhaustive_sweep (search.hpp:76, search.cpp:212-244).
  * rows = int64[6 * cap]: {wg, ts, time, transitions, ok, note(0 none, 1 infeasible, 2 deadlock)},
  * sorted exactly like the reference. */
 int mctb_sweep(const int* plat, int size, int kernel, const int64_t* input, int64_t* rows,
                int64_t cap, int64_t* n_rows);
 
-/* Machine::run (machine.hpp:224-227, machine.cpp:788-825) on the GPU, with one of the
+/* Machine::run (machine.hpp:210-215, machine.cpp:788-825) on the GPU, with one of the
  * MCTB_POLICY_* schedulers (traj = trajectory id for MCTB_POLICY_PHILOX).
  * out = {time, steps, result (INT64_MIN for abstract), process_count}. */
 int mctb_simulate(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
@@ -105,7 +105,7 @@ int mctb_simulate(const int* plat, int size, int kernel, const int64_t* input, i
                   int64_t cap, int64_t* trace_len);
 
 /* Batched trajectories (north-star subsystem 2; the swarm_worker runs of
- * explore.hpp:295-299 re-designed as counter-based random schedules):
+ * explore.hpp:102-110 re-designed as counter-based random schedules):
  * trajectory t (= traj0 + i) runs configuration configs[t % n_configs]
  * (configs = int32[2 * n_configs] of (wg, ts)).
  * out = int64[6 * n_traj]: {time, steps, result, status, FNV-1a 64 of the trace over its
@@ -117,11 +117,11 @@ int mctb_trajectories(const int* plat, int size, int kernel, const int64_t* inpu
  * thread's last mctb_trajectories call, in ms (the call's rate without its copies). */
 double mctb_trajectories_kernel_ms(void);
 
-/* replay (explore.hpp:301-304, explore.cpp:283-300) on the GPU; out = {final_time, result} */
+/* replay (explore.hpp:111-113, explore.cpp:283-300) on the GPU; out = {final_time, result} */
 int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
                 const int32_t* trace, int64_t len, int64_t final_time, int64_t* out);
 
-/* trace_to_text (report.hpp:435-440, report.cpp:82-97): returns the text length and
+/* trace_to_text (report.hpp:33-38, report.cpp:82-97): returns the text length and
  * copies at most cap-1 bytes + NUL into buf; -1 on error. */
 int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* input, int wg,
                         int ts, const int32_t* trace, int64_t len, char* buf, int64_t cap);
@@ -130,7 +130,7 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
  * Interleaving exploration and the bound-lowering driver (subsystems 3 and 4).
  */
 
-/* explore_machine (explore.hpp:272-277) over several configurations in one GPU sweep
+/* explore_machine (explore.hpp:81-86) over several configurations in one GPU sweep
  * (configs = int32[2 * n] of (wg, ts)); max_states = the reference's per-machine visited
  * cap (ExploreLimits::max_states, default 5e6 when <= 0); flags bit 0 = check
  * Machine::check_invariants (machine.cpp:719-756) and tick gating on every state;
@@ -165,7 +165,7 @@ int mctb_explore_mp_seed(void* ctx);
 int mctb_explore_mp_run(void* ctx, int64_t* out, int64_t* info);
 void mctb_explore_mp_close(void* ctx);
 
-/* check_overtime (explore.hpp:279-284), exact mode.
+/* check_overtime (explore.hpp:88-93), exact mode.
  * out = int64[12]: {violated, exhaustive, states_visited, max_depth_reached,
  *                   transitions_applied, configs_explored, configs_skipped, final_time, wg,
  *                   ts, steps, trace_exact}; the counterexample goes to trace. */
@@ -173,8 +173,8 @@ int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* in
                         int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
                         int64_t* trace_len);
 
-/* The `tune` flow: estimate_initial_time (search.hpp:361-364) when t_hi <= 0, then
- * bisect_min_time (search.hpp:366-371).
+/* The `tune` flow: estimate_initial_time (search.hpp:53-56) when t_hi <= 0, then
+ * bisect_min_time (search.hpp:58-63).
  * out = int64[10]: {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total,
  *                   first_trail_time, steps, trace_exact}
  * info = double[5] (optional): {ms cost model, ms first paths, ms exploration,
@@ -189,7 +189,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
  * bound — its full trace is mctb_check_overtime(T)).  Returns the probe count. */
 int64_t mctb_tune_probes(int64_t* rows, int64_t cap);
 
-/* swarm_min_time (search.hpp:373-379) re-designed as rounds of per_round Philox
+/* swarm_min_time (search.hpp:65-71) re-designed as rounds of per_round Philox
  * trajectories over every feasible configuration (max_rounds bounds the rounds).
  * out = int64[10]: {t_min, wg, ts, t_ini, rounds, transitions_total, first_trail_time,
  *                   steps, best_trajectory_id, trajectories_run}

@@ -29,11 +29,11 @@ namespace mctune_b200 {
 using Tick = std::int64_t;
 
 // ------------------------------------------------------------------ errors
-/// Invalid user input (model.hpp:15-18).
+/// Invalid user input (model.hpp:15-17).
 struct ConfigError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
-/// Internal contract violation of the transition system (model.hpp:21-24).
+/// Internal contract violation of the transition system (model.hpp:20-22).
 struct ModelBug : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -68,7 +68,7 @@ inline void check(int rc) {
 // ------------------------------------------------------------------ model (model.hpp)
 constexpr bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
 
-/// Exact log2 of a power of two (model.cpp:94-99).
+/// Exact log2 of a power of two (model.cpp:5-10).
 inline int log2_exact(int v) {
     if (!is_pow2(v)) throw ConfigError("not a power of two: " + std::to_string(v));
     int k = 0;
@@ -76,14 +76,14 @@ inline int log2_exact(int v) {
     return k;
 }
 
-/// Architecture constants of the abstract platform (model.hpp:37-44).
+/// Architecture constants of the abstract platform (model.hpp:33-40).
 struct PlatformConfig {
     int nd = 1;
     int nu = 1;
     int np = 4;
     int gmt = 4;
 
-    void validate() const {  // model.cpp:101-106
+    void validate() const {  // model.cpp:12-17
         if (nd < 1 || nu < 1 || np < 1 || gmt < 1)
             throw ConfigError("platform constants nd, nu, np, gmt must all be >= 1");
         if (!is_pow2(np)) throw ConfigError("np must be a power of two, got " + std::to_string(np));
@@ -97,13 +97,13 @@ inline const char* to_string(KernelKind k) {
     return k == KernelKind::Abstract ? "abstract" : "minimum";
 }
 
-inline KernelKind kernel_kind_from_string(const std::string& s) {  // model.cpp:112-116
+inline KernelKind kernel_kind_from_string(const std::string& s) {  // model.cpp:23-27
     if (s == "abstract") return KernelKind::Abstract;
     if (s == "minimum") return KernelKind::Minimum;
     throw ConfigError("unknown kernel kind '" + s + "' (expected abstract or minimum)");
 }
 
-/// The problem instance (model.hpp:53-64).
+/// The problem instance (model.hpp:48-58).
 struct ProblemSpec {
     int size = 8;
     KernelKind kernel = KernelKind::Abstract;
@@ -126,7 +126,7 @@ struct ProblemSpec {
         p.validate();
         return p;
     }
-    void validate() const {  // model.cpp:140-149
+    void validate() const {  // model.cpp:51-60
         if (size < 4 || !is_pow2(size))
             throw ConfigError("size must be a power of two >= 4, got " + std::to_string(size));
         if (kernel == KernelKind::Minimum) {
@@ -138,14 +138,14 @@ struct ProblemSpec {
     }
 };
 
-/// The two tuning parameters (model.hpp:67-72).
+/// The two tuning parameters (model.hpp:61-66).
 struct TuningParams {
     int wg = 0;
     int ts = 0;
     bool operator==(const TuningParams&) const = default;
 };
 
-/// Launch shape derived from (platform, size, params) (model.hpp:75-83).
+/// Launch shape derived from (platform, size, params) (model.hpp:69-77).
 struct LaunchPlan {
     int wgs = 0;
     int nwd = 0;
@@ -155,7 +155,7 @@ struct LaunchPlan {
     bool operator==(const LaunchPlan&) const = default;
 };
 
-/// model.cpp:151-159
+/// model.cpp:62-70
 inline void validate_params(int size, const TuningParams& params) {
     const int hi = size / 2;
     if (!is_pow2(params.wg) || params.wg < 2 || params.wg > hi)
@@ -164,7 +164,7 @@ inline void validate_params(int size, const TuningParams& params) {
         throw ConfigError("ts must be a power of two in [2, size/2], got " + std::to_string(params.ts));
 }
 
-/// Listing-3 launch arithmetic (model.cpp:161-177), mctb_derive_launch.
+/// Listing-3 launch arithmetic (model.cpp:72-88), mctb_derive_launch.
 inline LaunchPlan derive_launch(const PlatformConfig& platform, int size, const TuningParams& params) {
     const int plat[4] = {platform.nd, platform.nu, platform.np, platform.gmt};
     int out[5];
@@ -172,7 +172,7 @@ inline LaunchPlan derive_launch(const PlatformConfig& platform, int size, const 
     return LaunchPlan{out[0], out[1], out[2], out[3], out[4]};
 }
 
-/// All (wg, ts) = (2^i, 2^j), i, j in [1, n-1], ascending (model.cpp:179-189).
+/// All (wg, ts) = (2^i, 2^j), i, j in [1, n-1], ascending (model.cpp:90-100).
 inline std::vector<TuningParams> enumerate_configs(int size) {
     if (size < 4 || !is_pow2(size))
         throw ConfigError("size must be a power of two >= 4, got " + std::to_string(size));
@@ -189,14 +189,14 @@ inline bool config_feasible(const ProblemSpec& problem, const TuningParams& para
 }
 
 // ------------------------------------------------------------------ machine (machine.hpp)
-/// Transition labels (machine.hpp:50-70).
+/// Transition labels (machine.hpp:48-68).
 enum class Op : std::uint8_t {
     ClockTick, ClockHalt, HostGo, HostReactGo, HostStop, HostSetFin, DeviceUnitGo, DeviceDone,
     DeviceUnitStop, UnitPexGo, UnitDone, UnitPexStop, UnitBarrierStop, PexReport, PexEffect,
     PexArrive, PexItemDone, PexEndDone, BarrierRelease
 };
 
-/// One atomic step of the transition system (machine.hpp:78-88).
+/// One atomic step of the transition system (machine.hpp:76-84).
 struct Transition {
     std::uint16_t actor = 0;
     std::uint16_t peer = 0xffff;
@@ -205,7 +205,7 @@ struct Transition {
     bool operator==(const Transition&) const = default;
 };
 
-/// Scheduling policies of Machine::run (machine.hpp:219) plus the engine's own.
+/// Scheduling policies of Machine::run (machine.hpp:143) plus the engine's own.
 enum class SchedPolicy : std::uint8_t {
     RoundRobin = MCTB_POLICY_ROUND_ROBIN,
     SeededRandom = MCTB_POLICY_MT19937,  // std::mt19937_64, bit-exact with the reference
@@ -214,7 +214,7 @@ enum class SchedPolicy : std::uint8_t {
     TickLast = MCTB_POLICY_TICK_LAST     // lock-step schedule
 };
 
-/// Machine::run's outcome (machine.hpp:184-190): final time, transition count,
+/// Machine::run's outcome (machine.hpp:145-149): final time, transition count,
 /// and glob[0] for the minimum kernel.
 struct RunOutcome {
     Tick time = 0;
@@ -276,7 +276,7 @@ inline double since(Clock::time_point t0) {
 }
 }  // namespace detail
 
-/// Machine::run (machine.hpp:224-227) on the GPU.
+/// Machine::run (machine.hpp:210-215) on the GPU.
 inline RunOutcome run(const PlatformConfig& platform, const ProblemSpec& problem,
                       const TuningParams& params, SchedPolicy policy, std::uint64_t seed = 0,
                       std::vector<Transition>* trace_out = nullptr) {
@@ -300,7 +300,7 @@ inline RunOutcome run(const PlatformConfig& platform, const ProblemSpec& problem
 }
 
 // ------------------------------------------------------------------ explore (explore.hpp)
-/// Checked properties (explore.hpp:23-36).
+/// Checked properties (explore.hpp:19-34).
 struct Property {
     enum class Kind : std::uint8_t { OverTime, NonTermination };
     Kind kind = Kind::NonTermination;
@@ -414,7 +414,7 @@ inline ExploreResult explore_machine(const PlatformConfig& platform, const Probl
 }
 
 /// Exhaustive check of the over-time property across the whole parameter
-/// space (explore.hpp:95-101).
+/// space (explore.hpp:88-93).
 inline Verdict check_overtime(const PlatformConfig& platform, const ProblemSpec& problem, Tick T,
                               const ExploreLimits& limits) {
     if (limits.mode != ExploreLimits::Mode::Exact)
@@ -572,7 +572,7 @@ inline TuneResult tune_call(const PlatformConfig& platform, const ProblemSpec& p
 }  // namespace detail
 
 /// Counterexample-guided binary search for the minimal termination time
-/// (search.hpp:57-62): same verdicts, statistics and trace as the reference.
+/// (search.hpp:58-63): same verdicts, statistics and trace as the reference.
 inline TuneResult bisect_min_time(const PlatformConfig& platform, const ProblemSpec& problem,
                                   Tick t_hi, const ExploreLimits& limits) {
     if (limits.mode != ExploreLimits::Mode::Exact) throw ConfigError("bisection needs exact mode");
@@ -588,7 +588,7 @@ inline TuneResult tune(const PlatformConfig& platform, const ProblemSpec& proble
     return detail::tune_call(platform, problem, 0, seed, limits);
 }
 
-/// Randomised search (search.hpp:64-71): rounds of `workers` x 4096
+/// Randomised search (search.hpp:65-71): rounds of `workers` x 4096
 /// counter-based Philox trajectories with the reference's stop rule.
 /// Heuristic: never a proof.  trails_out receives the first round's terminal
 /// runs (time, params, steps; no transition lists).
@@ -652,14 +652,14 @@ inline std::vector<SweepRow> exhaustive_sweep(const PlatformConfig& platform,
 }
 
 /// Reads (wg, ts, time) out of a counterexample after replay validation
-/// (search.hpp:86-88).
+/// (search.hpp:85-87).
 inline ExtractedParams extract_params(const PlatformConfig& platform, const ProblemSpec& problem,
                                       const Trace& trace) {
     const RunOutcome end = replay(platform, problem, trace);
     return ExtractedParams{trace.params.wg, trace.params.ts, end.time};
 }
 
-/// Stable sort of trail summaries by (time, transitions) (search.hpp:90-91).
+/// Stable sort of trail summaries by (time, transitions) (search.hpp:89-90).
 inline std::vector<RankedTrail> rank_trails(const std::vector<Trace>& traces) {
     std::vector<RankedTrail> out;
     for (const auto& t : traces) out.push_back(RankedTrail{t.final_time, t.params.wg, t.params.ts, t.steps});

@@ -47,7 +47,7 @@ typedef struct {
     int wgs, nwd, nwu, nwe, all_nwe;
 } plan_t;
 
-/* PlatformConfig::validate, model.cpp:101-106 */
+/* PlatformConfig::validate, model.cpp:12-17 */
 static int validate_platform(const plat_t* p) {
     if (p->nd < 1 || p->nu < 1 || p->np < 1 || p->gmt < 1) {
         set_err("platform constants nd, nu, np, gmt must all be >= 1");
@@ -60,7 +60,7 @@ static int validate_platform(const plat_t* p) {
     return MO_OK;
 }
 
-/* validate_params, model.cpp:151-159 (+ size check of derive_launch, model.cpp:163) */
+/* validate_params, model.cpp:62-70 (+ size check of derive_launch, model.cpp:74) */
 static int validate_params(int size, int wg, int ts) {
     if (size < 4 || !is_pow2(size)) {
         set_err("size must be a power of two >= 4");
@@ -78,7 +78,7 @@ static int validate_params(int size, int wg, int ts) {
     return MO_OK;
 }
 
-/* derive_launch, model.cpp:161-177: Listing 3 arithmetic, wgs clamped to >= 1 */
+/* derive_launch, model.cpp:72-88: Listing 3 arithmetic, wgs clamped to >= 1 */
 static void plan_of(const plat_t* p, int size, int wg, int ts, plan_t* out) {
     long long wgs = (long long)size / ((long long)wg * ts);
     if (wgs < 1) wgs = 1;
@@ -184,7 +184,7 @@ typedef struct {
 enum { R_MAIN, R_HOST, R_CLOCK, R_DEVICE, R_UNIT, R_BARRIER, R_PEX };
 static const char* ROLE_NAME[] = {"main", "host", "clock", "device", "unit", "barrier", "pex"};
 
-/* control locations, machine.hpp:20-46 (ordinals matter for serialization) */
+/* control locations, machine.hpp:22-46 (ordinals matter for serialization) */
 enum { H_SENDGO, H_WAITDONEREACT, H_REACTGO, H_WAITDONESTOP, H_SENDSTOP, H_SETFIN, H_EXITED };
 enum { D_WAITGO, D_SENDUNITGO, D_WAITUNITDONE, D_SENDDONE, D_STOPUNITS, D_EXITED };
 enum { U_WAITGO, U_ACTIVATEPEX, U_SERVE, U_REACTPEX, U_SENDUNITDONE, U_STOPPEXES, U_STOPBARRIER,
@@ -195,7 +195,7 @@ enum { P_WAITGO, P_RUN, P_ARRIVEBARRIER, P_WAITBARRIER, P_ARRIVEGROUPEND, P_WAIT
 enum { C_RUN, C_EXITED };
 enum { PH_ACTIVATION, PH_EPILOGUE };
 
-/* Op, machine.hpp:50-70 */
+/* Op, machine.hpp:48-68 */
 enum {
     OP_CLOCKTICK, OP_CLOCKHALT, OP_HOSTGO, OP_HOSTREACTGO, OP_HOSTSTOP, OP_HOSTSETFIN,
     OP_DEVICEUNITGO, OP_DEVICEDONE, OP_DEVICEUNITSTOP, OP_UNITPEXGO, OP_UNITDONE,
@@ -303,7 +303,7 @@ static int machine_init(machine_t* m, const plat_t* p, int size, int kernel, con
     m->ts = ts;
     plan_of(p, size, wg, ts, &m->plan);
     if (kernel == 1) {
-        if (!input) { /* ProblemSpec::minimum default, model.cpp:126-138 */
+        if (!input) { /* ProblemSpec::minimum default, model.cpp:37-49 */
             m->default_input = (int64_t*)malloc(sizeof(int64_t) * (size_t)size);
             for (int i = 0; i < size; ++i) m->default_input[i] = size - i;
             input = m->default_input;
@@ -447,7 +447,7 @@ static const instr_t* instr_at(const machine_t* m, const pex_t_* px) {
     return px->phase == PH_ACTIVATION ? &m->act[px->cursor] : &m->epi[px->cursor];
 }
 
-static int has_epilogue(const machine_t* m) { return m->n_epi > 1; } /* kernel.hpp:94 */
+static int has_epilogue(const machine_t* m) { return m->n_epi > 1; } /* kernel.hpp:84 */
 
 /* Machine::place_pex, machine.cpp:136-162 */
 static void place_pex(const machine_t* m, state_t* s, int p) {
@@ -613,7 +613,7 @@ static void enabled(const machine_t* m, const state_t* s, tvec* out) {
 static int pex_me(const machine_t* m, int p) { return p % m->plan.nwe; }
 static int pex_unit(const machine_t* m, int p) { return p / m->plan.nwe; }
 
-/* MemRef::resolve, kernel.hpp:25-32 + Machine::read_ref/write_ref machine.cpp:343-359 */
+/* MemRef::resolve, kernel.hpp:28-35 + Machine::read_ref/write_ref machine.cpp:343-359 */
 static int64_t* mem_ref(machine_t* m, state_t* s, int base, int off, int shift, int slot) {
     int idx;
     int64_t* arr;
@@ -634,7 +634,7 @@ static int64_t* mem_ref(machine_t* m, state_t* s, int base, int off, int shift, 
     return &arr[idx];
 }
 
-/* global_item_id, kernel.hpp:101-103 */
+/* global_item_id, kernel.hpp:93-95 */
 static int global_item_id(const machine_t* m, int nwg, int me, int iter) {
     return m->wg > m->p.np ? nwg * m->wg + me + iter * m->p.np : nwg * m->wg + me;
 }
@@ -865,7 +865,7 @@ static void apply(machine_t* m, state_t* s, const mo_transition* t) {
             REQUIRE(t->arg == px->cursor, "transition not enabled: cursor matches");
             const int gid = global_item_id(m, px->nwg, pex_me(m, p), px->iter);
             const int shift = gid * m->ts;
-            const int slot = pex_unit(m, p) * m->p.np + pex_me(m, p); /* machine.hpp:205 */
+            const int slot = pex_unit(m, p) * m->p.np + pex_me(m, p); /* machine.hpp:208 */
             const int64_t* src = mem_ref(m, s, in->src_base, in->src_off, shift, slot);
             if (!src) return;
             const int64_t v = *src;
@@ -1134,7 +1134,7 @@ int mo_simulate(const int* plat, int size, int kernel, const int64_t* input, int
     tvec en = {0};
     int64_t steps = 0;
     int rr_next = 0;
-    const int64_t max_steps = 200000000LL; /* machine.hpp:235 kDefaultMaxRunSteps */
+    const int64_t max_steps = 200000000LL; /* machine.hpp:215 kDefaultMaxRunSteps */
     rc = MO_OK;
     for (;;) {
         enabled(&m, &s, &en);

@@ -39,7 +39,7 @@ typedef struct {
 
 const char* mo_last_error(void);
 
-/* model.cpp:161-177; out = [wgs, nwd, nwu, nwe, all_nwe] */
+/* model.cpp:72-88; out = [wgs, nwd, nwu, nwe, all_nwe] */
 int mo_derive_launch(const int* plat, int size, int wg, int ts, int* out);
 
 /* Lock-step closed form of the final time and transition count (derived from

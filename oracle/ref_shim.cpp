@@ -124,7 +124,7 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
-// derive_launch (model.cpp:161-177): out = [wgs, nwd, nwu, nwe, all_nwe]
+// derive_launch (model.cpp:72-88): out = [wgs, nwd, nwu, nwe, all_nwe]
 int ref_derive_launch(const int* plat, int size, int wg, int ts, int* out) {
     return guarded([&] {
         const LaunchPlan p = derive_launch(plat_of(plat), size, TuningParams{wg, ts});
@@ -256,7 +256,7 @@ int ref_check_overtime(const int* plat, int size, int kernel, const int64_t* inp
     });
 }
 
-// estimate_initial_time (search.cpp:96-104)
+// estimate_initial_time (search.cpp:94-102)
 int ref_estimate_initial_time(const int* plat, int size, int kernel, const int64_t* input,
                               uint64_t seed, int64_t* out) {
     return guarded([&] {
@@ -264,8 +264,8 @@ int ref_estimate_initial_time(const int* plat, int size, int kernel, const int64
     });
 }
 
-// bisect_min_time (search.cpp:106-160).  t_hi <= 0 means estimate_initial_time(seed) first
-// (the `tune` command flow, tools/main.cpp:301-304).
+// bisect_min_time (search.cpp:104-158).  t_hi <= 0 means estimate_initial_time(seed) first
+// (the `tune` command flow, tools/main.cpp:119-128).
 // out = [t_min, wg, ts, t_ini, proven, checks_run, states_visited_total, first_trail_time, steps]
 int ref_tune(const int* plat, int size, int kernel, const int64_t* input, int64_t t_hi,
              uint64_t seed, long long max_depth, long long max_states, int64_t* out,
@@ -288,7 +288,7 @@ int ref_tune(const int* plat, int size, int kernel, const int64_t* input, int64_
     });
 }
 
-// exhaustive_sweep (search.cpp:214-246).  rows: [wg, ts, time, transitions, ok, note]
+// exhaustive_sweep (search.cpp:212-244).  rows: [wg, ts, time, transitions, ok, note]
 // note: 0 none, 1 infeasible, 2 deadlock.  Returns row count via *n_rows.
 int ref_sweep(const int* plat, int size, int kernel, const int64_t* input, int64_t* rows,
               long long cap, long long* n_rows) {
@@ -335,7 +335,7 @@ long long ref_trace_text(const int* plat, int size, int kernel, const int64_t* i
     return n;
 }
 
-// swarm_min_time (search.cpp:162-212), for timing and for the >= bisection property.
+// swarm_min_time (search.cpp:160-210), for timing and for the >= bisection property.
 // out = [t_min, wg, ts, t_ini, checks_run, states_visited_total, first_trail_time, steps]
 int ref_swarm(const int* plat, int size, int kernel, const int64_t* input, int workers,
               double budget_secs, long long max_depth, uint64_t seed, int64_t* out) {

@@ -18,7 +18,7 @@ class MctuneError(RuntimeError):
 
 
 class ConfigError(MctuneError):
-    """Invalid user input (reference: mctune::ConfigError, model.hpp:16)."""
+    """Invalid user input (reference: mctune::ConfigError, model.hpp:15-17)."""
 
 
 class ModelBug(MctuneError):

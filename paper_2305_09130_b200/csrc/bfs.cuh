@@ -30,7 +30,7 @@ struct BfsResult {
 
 // Explores every configuration in `hs` in one sweep.  max_states bounds the
 // whole table; cfg_cap is the per-configuration visited cap of the reference
-// (ExploreLimits::max_states, explore.hpp:227-233).
+// (ExploreLimits::max_states, explore.hpp:36-42).
 // seeds (optional): packed states of configuration 0 (layout bfs_layout(hs[0].d, 1))
 // to start from instead of the initial states — a multi-source exploration.
 // first_cap (0 = sized for max_states) bounds the first table; it grows 16x

@@ -212,7 +212,7 @@ __host__ __device__ inline int bfs_slot_rules(const MachDesc& m, const MState& s
     return n;
 }
 
-// Ordinal form -> the pid form of machine.hpp:78-88 (what apply() takes).
+// Ordinal form -> the pid form of machine.hpp:76-84 (what apply() takes).
 __host__ __device__ inline Transition to_pid(const MachDesc& m, const Transition& t) {
     Transition r{0, kNoPeer, t.op, t.arg};
     const int a = t.actor, p = t.peer;
@@ -427,7 +427,7 @@ __host__ __device__ inline bool fast_successor(const BfsDesc& d, const MState& s
             // global item, a neighbour's slot, or (publish) the element's slot into
             // glob[0]; then the next instruction
             const int p = tr.actor, g = p >> m.lognwe, me = p - g * m.nwe;
-            const int slot = g * m.np + me;  // myloc, machine.hpp:205
+            const int slot = g * m.np + me;  // myloc, machine.hpp:208
             PexS px = s.pex[p];
             const Instr in = instr_at(m, px.phase, px.cursor);
             int32_t v, cur;

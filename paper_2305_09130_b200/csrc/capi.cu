@@ -97,7 +97,7 @@ int log2i(long long v) {
     return n;
 }
 
-// PlatformConfig::validate (model.cpp:101-106)
+// PlatformConfig::validate (model.cpp:12-17)
 int check_platform(const int* plat) {
     if (plat[0] < 1 || plat[1] < 1 || plat[2] < 1 || plat[3] < 1) {
         set_error("platform constants nd, nu, np, gmt must all be >= 1");
@@ -110,7 +110,7 @@ int check_platform(const int* plat) {
     return MCTB_OK;
 }
 
-// ProblemSpec::validate (model.cpp:140-149)
+// ProblemSpec::validate (model.cpp:51-60)
 int check_problem(int size, int kernel) {
     if (size < 4 || !is_pow2(size)) {
         set_error("size must be a power of two >= 4, got " + std::to_string(size));
@@ -124,7 +124,7 @@ int check_problem(int size, int kernel) {
 }
 
 // The reference's own tuning space for one (platform, problem):
-// enumerate_configs (model.cpp:179-189) as a space descriptor.
+// enumerate_configs (model.cpp:90-100) as a space descriptor.
 void reference_space(const int* plat, int size, int kernel, int64_t* sd) {
     const int n = log2i(size);
     const int64_t v[13] = {kernel, size, plat[3], plat[0], plat[0], plat[1], plat[1],
@@ -228,7 +228,7 @@ int mctb_space_eval_async(const int64_t* sd, uint64_t first, uint64_t count, int
     return launch_space_eval(s, first, count, d_time, d_steps, static_cast<cudaStream_t>(stream));
 }
 
-// exhaustive_sweep (search.cpp:214-246): every enumerated configuration,
+// exhaustive_sweep (search.cpp:212-244): every enumerated configuration,
 // infeasible ones flagged, stable-sorted by (ok first, time, transitions).
 int mctb_sweep(const int* plat, int size, int kernel, const int64_t* input, int64_t* rows,
                int64_t cap, int64_t* n_rows) {
@@ -260,7 +260,7 @@ int mctb_sweep(const int* plat, int size, int kernel, const int64_t* input, int6
     };
     std::vector<Row> out;
     out.reserve(n);
-    // enumerate_configs order: wg ascending, then ts ascending (model.cpp:185-187);
+    // enumerate_configs order: wg ascending, then ts ascending (model.cpp:96-98);
     // space index order is wg descending, ts descending.
     const int L = log2i(size) - 1;
     for (int i = 1; i <= L; ++i)

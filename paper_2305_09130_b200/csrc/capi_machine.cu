@@ -14,7 +14,7 @@ int check_problem(int size, int kernel);
 bool is_pow2(long long v);
 
 // Machine::Machine preconditions (machine.cpp:60-69): validate_params
-// (model.cpp:151-159) and, for the minimum kernel, the feasibility check of
+// (model.cpp:62-70) and, for the minimum kernel, the feasibility check of
 // build_minimum_kernel (kernel.cpp:56-62).
 int check_machine(const int* plat, int size, int kernel, int wg, int ts) {
     int rc = check_platform(plat);

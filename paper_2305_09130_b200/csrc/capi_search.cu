@@ -1,6 +1,6 @@
 // The bound-lowering driver on the GPU (north-star subsystem 4):
 // check_overtime (explore.cpp:167-205), estimate_initial_time
-// (search.cpp:96-104) and bisect_min_time (search.cpp:106-160).
+// (search.cpp:94-102) and bisect_min_time (search.cpp:104-158).
 //
 // The reference answers every probe C_ex(T) of the bisection with a fresh
 // exhaustive DFS over all configurations.  Here one GPU sweep establishes,
@@ -52,7 +52,7 @@ struct Ctx {
     int plat[4];
     int size = 0, kernel = 0;
     const int64_t* input = nullptr;
-    uint64_t cap = 5000000;  // ExploreLimits::max_states (explore.hpp:229)
+    uint64_t cap = 5000000;  // ExploreLimits::max_states (explore.hpp:38)
     int skipped = 0;
     std::vector<int> wg, ts;  // feasible configurations, largest-first (explore.cpp:64-72)
     std::vector<int64_t> cm_time, cm_steps;
@@ -301,7 +301,7 @@ using namespace mctb;
 
 extern "C" {
 
-// check_overtime (explore.hpp:279-284).
+// check_overtime (explore.hpp:88-93).
 // out = {violated, exhaustive, states_visited, max_depth_reached, transitions_applied,
 //        configs_explored, configs_skipped, final_time, wg, ts, steps, trace_exact}
 int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* input, int64_t T,
@@ -341,7 +341,7 @@ static void record_probe(int64_t T, const VerdictOut& v, const Ctx& c) {
     g_probes.insert(g_probes.end(), row, row + 8);
 }
 
-// estimate_initial_time + bisect_min_time: the `tune` flow (tools/main.cpp:301-304).
+// estimate_initial_time + bisect_min_time: the `tune` flow (tools/main.cpp:119-128).
 // t_hi <= 0 selects estimate_initial_time(seed).
 // out = {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total, first_trail_time,
 //        steps, trace_exact}
@@ -357,7 +357,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     int rc = prepare(c, max_states);
     if (rc) return rc;
     if (t_hi <= 0) {
-        // estimate_initial_time (search.cpp:96-104): mt19937_64(seed) picks a feasible
+        // estimate_initial_time (search.cpp:94-102): mt19937_64(seed) picks a feasible
         // configuration in enumerate_configs order; its SeededRandom run is T_ini.
         std::vector<int> order(c.wg.size());
         for (size_t k = 0; k < order.size(); ++k) order[k] = (int)k;
@@ -380,7 +380,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         set_error("t_hi must be >= 1");
         return MCTB_CONFIG_ERROR;
     }
-    // search.cpp:106-160
+    // search.cpp:104-158
     g_probes.clear();
     int checks = 0;
     int64_t states_total = 0;

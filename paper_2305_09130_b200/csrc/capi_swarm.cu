@@ -1,5 +1,5 @@
 // Swarm search on the GPU (north-star subsystem 2): swarm_min_time
-// (search.cpp:162-212) re-designed around counter-based trajectories.
+// (search.cpp:160-210) re-designed around counter-based trajectories.
 //
 // The reference runs `workers` threads of randomised bitstate DFS per round
 // under a wall-clock budget.  Here a round is one launch of n trajectories
@@ -9,7 +9,7 @@
 // The stop rule is the reference's: round 0 collects terminating runs; each
 // further round keeps only runs strictly below the best time so far and the
 // search stops when a round finds none (or no smaller time).  Ties prefer the
-// largest wg, then the largest ts (pick_preferred, search.cpp:69-78).
+// largest wg, then the largest ts (pick_preferred, search.cpp:67-78).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -46,8 +46,8 @@ int mctb_swarm(const int* plat, int size, int kernel, const int64_t* input, int6
         return MCTB_CONFIG_ERROR;
     }
     if ((rc = require_device())) return rc;
-    if (max_steps <= 0) max_steps = 4000000;  // ExploreLimits::max_depth (explore.hpp:228)
-    // feasible configurations, enumerate_configs order (model.cpp:185-187)
+    if (max_steps <= 0) max_steps = 4000000;  // ExploreLimits::max_depth (explore.hpp:37)
+    // feasible configurations, enumerate_configs order (model.cpp:96-98)
     int n = 0;
     while ((1 << n) < size) ++n;
     std::vector<MachHost> hs;

@@ -41,7 +41,7 @@ struct Cost {
     bool feasible;
 };
 
-// derive_launch, model.cpp:161-177 (powers of two as logs)
+// derive_launch, model.cpp:72-88 (powers of two as logs)
 __host__ __device__ inline void launch_plan(int logn, int nd, int nu, int lognp, int logwg,
                                             int logts, int& wgs, int& nwd, int& nwu, int& nwe) {
     const int s = logwg + logts;

@@ -7,7 +7,7 @@
 // one packed 64-bit key per CTA with atomicMin:
 //     key = (min(time, 2^30 - 1) << 33) | index.
 // The index order puts the reference's preferred configuration (largest wg,
-// then largest ts — explore.cpp:64-72, search.cpp:451-453) first, so the
+// then largest ts — explore.cpp:64-72, search.cpp:67-78) first, so the
 // minimum key breaks ties exactly as bisect_min_time does.
 //
 // Nothing here reads memory on the hot path: the kernel is bound by integer
@@ -228,7 +228,7 @@ int sm_count() {
 }  // namespace
 
 // Validates the descriptor and fills the device view.  The ranges must keep
-// every configuration inside validate_params (model.cpp:151-159).
+// every configuration inside validate_params (model.cpp:62-70).
 int make_space(const int64_t* sd, SpaceDev* out) {
     const int64_t kernel = sd[0], size = sd[1];
     if (kernel != 0 && kernel != 1) {

@@ -18,14 +18,14 @@
 
 namespace mctb {
 
-// Op ordinals, machine.hpp:50-70
+// Op ordinals, machine.hpp:48-68
 enum : int {
     OP_CLOCKTICK, OP_CLOCKHALT, OP_HOSTGO, OP_HOSTREACTGO, OP_HOSTSTOP, OP_HOSTSETFIN,
     OP_DEVICEUNITGO, OP_DEVICEDONE, OP_DEVICEUNITSTOP, OP_UNITPEXGO, OP_UNITDONE,
     OP_UNITPEXSTOP, OP_UNITBARRIERSTOP, OP_PEXREPORT, OP_PEXEFFECT, OP_PEXARRIVE,
     OP_PEXITEMDONE, OP_PEXENDDONE, OP_BARRIERRELEASE
 };
-// control locations, machine.hpp:20-46
+// control locations, machine.hpp:22-46
 enum : int { H_SENDGO, H_WAITDONEREACT, H_REACTGO, H_WAITDONESTOP, H_SENDSTOP, H_SETFIN, H_EXITED };
 enum : int { D_WAITGO, D_SENDUNITGO, D_WAITUNITDONE, D_SENDDONE, D_STOPUNITS, D_EXITED };
 enum : int { U_WAITGO, U_ACTIVATEPEX, U_SERVE, U_REACTPEX, U_SENDUNITDONE, U_STOPPEXES,
@@ -214,7 +214,7 @@ __host__ __device__ inline Instr instr_at(const MachDesc& m, int phase, int c) {
     return in;
 }
 
-// has_epilogue (kernel.hpp:94): only the minimum kernel's
+// has_epilogue (kernel.hpp:84): only the minimum kernel's
 __host__ __device__ inline bool has_epilogue(const MachDesc& m) { return m.kernel == 1; }
 
 // ------------------------------------------------------------ state
@@ -676,11 +676,11 @@ __host__ __device__ inline bool apply(const MachDesc& m, MState& s, const Transi
             const Instr in = instr_at(m, px.phase, px.cursor);
             if (in.kind != IK_EFFECT || t.arg != px.cursor) return false;
             const int g = div_nwe(m, ord), me = ord - g * m.nwe;
-            const int slot = g * m.np + me;  // myloc, machine.hpp:205
+            const int slot = g * m.np + me;  // myloc, machine.hpp:208
             int32_t v;
             int32_t* dst;
             if (px.phase == 0) {
-                // glob[shift + i] -> loc[myloc]; global_item_id, kernel.hpp:101-103
+                // glob[shift + i] -> loc[myloc]; global_item_id, kernel.hpp:93-95
                 const int gid = m.wg > m.np ? px.nwg * m.wg + me + px.iter * m.np
                                             : px.nwg * m.wg + me;
                 const int idx = gid * m.ts + in.src;

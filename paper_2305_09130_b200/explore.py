@@ -17,7 +17,7 @@ from .model import PlatformConfig, ProblemSpec, TuningParams
 
 @dataclass
 class ExploreStats:
-    """(explore.hpp:235-245) + terminal-time range."""
+    """(explore.hpp:44-56) + terminal-time range."""
     complete: bool
     states_visited: int
     transitions_applied: int
@@ -61,5 +61,5 @@ def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
 
 def explore_machine(platform: PlatformConfig, problem: ProblemSpec, params: TuningParams,
                     max_states: int = 5_000_000) -> ExploreStats:
-    """Every interleaving of one machine (explore.hpp:272-277)."""
+    """Every interleaving of one machine (explore.hpp:81-86)."""
     return explore_configs(platform, problem, [params], max_states)[0]

@@ -27,7 +27,7 @@ Transition = Tuple[int, int, int, int]  # (actor, peer, op, arg)
 
 @dataclass
 class RunOutcome:
-    """(machine.hpp:221-225)"""
+    """(machine.hpp:145-149)"""
     time: int = 0
     result: Optional[int] = None
     steps: int = 0
@@ -35,7 +35,7 @@ class RunOutcome:
 
 @dataclass
 class Trace:
-    """(explore.hpp:247-254)"""
+    """(explore.hpp:58-63)"""
     transitions: List[Transition] = field(default_factory=list)
     final_time: int = 0
     params: TuningParams = TuningParams()
@@ -48,7 +48,7 @@ def _trace_buf(trace: Sequence[Transition]):
 
 
 class Machine:
-    """One (platform, problem, params) choice (machine.hpp:94-211)."""
+    """One (platform, problem, params) choice (machine.hpp:151-233)."""
 
     def __init__(self, platform: PlatformConfig, problem: ProblemSpec, params: TuningParams):
         platform.validate()
@@ -74,7 +74,7 @@ class Machine:
 
 
 def replay(platform: PlatformConfig, problem: ProblemSpec, trace: Trace) -> Tuple[int, Optional[int]]:
-    """Re-applies a trace on the GPU (explore.hpp:301-304); returns (final time, result).
+    """Re-applies a trace on the GPU (explore.hpp:111-113); returns (final time, result).
     Raises CorruptTrace on divergence, non-terminal end or time mismatch."""
     buf, n = _trace_buf(trace.transitions)
     out = (C.c_int64 * 2)()
@@ -85,7 +85,7 @@ def replay(platform: PlatformConfig, problem: ProblemSpec, trace: Trace) -> Tupl
 
 
 def trace_to_text(platform: PlatformConfig, problem: ProblemSpec, trace: Trace) -> str:
-    """report.hpp:435-440: one line per transition, then the FINAL line."""
+    """report.hpp:33-38: one line per transition, then the FINAL line."""
     buf, n = _trace_buf(trace.transitions)
     need = lib.mctb_trace_text(platform.as_array(), problem.size, problem.kernel,
                                problem.input_array(), trace.params.wg, trace.params.ts, buf, n,

@@ -18,7 +18,7 @@ def is_pow2(v: int) -> bool:
 
 
 def log2_exact(v: int) -> int:
-    """model.cpp:94-99"""
+    """model.cpp:5-10"""
     if not is_pow2(v):
         raise ConfigError(f"not a power of two: {v}")
     return v.bit_length() - 1
@@ -26,13 +26,13 @@ def log2_exact(v: int) -> int:
 
 @dataclass(frozen=True)
 class PlatformConfig:
-    """Abstract platform constants (model.hpp:37-44)."""
+    """Abstract platform constants (model.hpp:33-40)."""
     nd: int = 1
     nu: int = 1
     np: int = 4
     gmt: int = 4
 
-    def validate(self) -> None:  # model.cpp:101-106
+    def validate(self) -> None:  # model.cpp:12-17
         if self.nd < 1 or self.nu < 1 or self.np < 1 or self.gmt < 1:
             raise ConfigError("platform constants nd, nu, np, gmt must all be >= 1")
         if not is_pow2(self.np):
@@ -46,7 +46,7 @@ ABSTRACT, MINIMUM = 0, 1
 
 
 def kernel_kind_from_string(s: str) -> int:
-    """model.cpp:112-116"""
+    """model.cpp:23-27"""
     if s == "abstract":
         return ABSTRACT
     if s == "minimum":
@@ -56,7 +56,7 @@ def kernel_kind_from_string(s: str) -> int:
 
 @dataclass(frozen=True)
 class ProblemSpec:
-    """Problem instance (model.hpp:53-64)."""
+    """Problem instance (model.hpp:48-58)."""
     size: int = 8
     kernel: int = ABSTRACT
     input: tuple = field(default_factory=tuple)
@@ -69,13 +69,13 @@ class ProblemSpec:
 
     @staticmethod
     def minimum(size: int, input: Optional[Sequence[int]] = None) -> "ProblemSpec":
-        """Empty input selects glob[i] = size - i (model.cpp:126-138)."""
+        """Empty input selects glob[i] = size - i (model.cpp:37-49)."""
         vals = tuple(int(v) for v in input) if input else tuple(size - i for i in range(size))
         p = ProblemSpec(size, MINIMUM, vals)
         p.validate()
         return p
 
-    def validate(self) -> None:  # model.cpp:140-149
+    def validate(self) -> None:  # model.cpp:51-60
         if self.size < 4 or not is_pow2(self.size):
             raise ConfigError(f"size must be a power of two >= 4, got {self.size}")
         if self.kernel == MINIMUM:
@@ -92,14 +92,14 @@ class ProblemSpec:
 
 @dataclass(frozen=True)
 class TuningParams:
-    """(model.hpp:67-72)"""
+    """(model.hpp:61-66)"""
     wg: int = 0
     ts: int = 0
 
 
 @dataclass(frozen=True)
 class LaunchPlan:
-    """(model.hpp:75-83)"""
+    """(model.hpp:69-77)"""
     wgs: int = 0
     nwd: int = 0
     nwu: int = 0
@@ -108,7 +108,7 @@ class LaunchPlan:
 
 
 def validate_params(size: int, params: TuningParams) -> None:
-    """model.cpp:151-159"""
+    """model.cpp:62-70"""
     hi = size // 2
     if not is_pow2(params.wg) or params.wg < 2 or params.wg > hi:
         raise ConfigError(f"wg must be a power of two in [2, size/2], got {params.wg}")
@@ -117,14 +117,14 @@ def validate_params(size: int, params: TuningParams) -> None:
 
 
 def derive_launch(platform: PlatformConfig, size: int, params: TuningParams) -> LaunchPlan:
-    """Listing-3 launch arithmetic (model.cpp:161-177), through the C ABI."""
+    """Listing-3 launch arithmetic (model.cpp:72-88), through the C ABI."""
     out = (C.c_int32 * 5)()
     check(lib.mctb_derive_launch(platform.as_array(), size, params.wg, params.ts, out))
     return LaunchPlan(*out)
 
 
 def enumerate_configs(size: int) -> List[TuningParams]:
-    """All (wg, ts) = (2^i, 2^j), i, j in [1, n-1], (wg, ts) ascending (model.cpp:179-189)."""
+    """All (wg, ts) = (2^i, 2^j), i, j in [1, n-1], (wg, ts) ascending (model.cpp:90-100)."""
     if size < 4 or not is_pow2(size):
         raise ConfigError(f"size must be a power of two >= 4, got {size}")
     n = log2_exact(size)

@@ -19,7 +19,7 @@ CSV_HEADER = "size,wg,ts,time,transitions\n"
 
 @dataclass
 class RunConfig:
-    """(report.hpp:14-22)"""
+    """(report.hpp:12-20)"""
     platform: PlatformConfig = field(default_factory=PlatformConfig)
     problem: ProblemSpec = field(default_factory=lambda: ProblemSpec.abstract(8))
     max_depth: int = 4_000_000

@@ -16,7 +16,7 @@ from .model import PlatformConfig, ProblemSpec
 
 @dataclass(frozen=True)
 class SweepRow:
-    """(search.hpp:44-52)"""
+    """(search.hpp:36-44)"""
     size: int
     wg: int
     ts: int
@@ -31,7 +31,7 @@ _NOTES = {0: "", 1: "infeasible", 2: "deadlock"}
 
 def exhaustive_sweep(platform: PlatformConfig, problem: ProblemSpec) -> List[SweepRow]:
     """Every enumerated configuration, sorted by (time, transitions), flagged rows last
-    (search.hpp:381-385, search.cpp:214-246)."""
+    (search.hpp:73-77, search.cpp:212-244)."""
     n = (problem.size.bit_length() - 2) ** 2 if problem.size >= 4 else 0
     rows = (C.c_int64 * (6 * max(n, 1)))()
     got = C.c_int64()
@@ -45,7 +45,7 @@ def exhaustive_sweep(platform: PlatformConfig, problem: ProblemSpec) -> List[Swe
 
 
 # --------------------------------------------------------------------------
-# Verdicts and the bound-lowering driver (explore.hpp:256-261, search.hpp:324-342)
+# Verdicts and the bound-lowering driver (explore.hpp:65-70, search.hpp:16-34)
 
 from .machine import Trace  # noqa: E402
 from .model import TuningParams  # noqa: E402
@@ -89,7 +89,7 @@ class TuneStats:
 
 @dataclass
 class TuneProbe:
-    """One bound of the bisection: check_overtime(T)'s verdict (explore.hpp:95-101)
+    """One bound of the bisection: check_overtime(T)'s verdict (explore.hpp:88-93)
     and, when violated, its counterexample's configuration, time and length."""
     T: int
     violated: bool
@@ -103,7 +103,7 @@ class TuneProbe:
 
 @dataclass
 class TuneResult:
-    """(search.hpp:330-342)"""
+    """(search.hpp:22-34)"""
     t_min: int
     params: TuningParams
     trace: Trace
@@ -130,7 +130,7 @@ def _trace_from(buf, n, final_time, wg, ts):
 def check_overtime(platform: PlatformConfig, problem: ProblemSpec, T: int,
                    max_states: int = 5_000_000) -> Verdict:
     """Exhaustive check of "every terminating run takes more than T ticks" over all
-    configurations and interleavings (explore.hpp:279-284)."""
+    configurations and interleavings (explore.hpp:88-93)."""
     out = (C.c_int64 * 12)()
     buf = _trace_buffer()
     n = C.c_int64()
@@ -145,7 +145,7 @@ def check_overtime(platform: PlatformConfig, problem: ProblemSpec, T: int,
 def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: int = 0,
          max_states: int = 5_000_000) -> TuneResult:
     """The `tune` command flow: estimate_initial_time(seed) then bisect_min_time
-    (tools/main.cpp:301-304)."""
+    (tools/main.cpp:119-128)."""
     import time as _time
     t0 = _time.perf_counter()
     out = (C.c_int64 * 10)()
@@ -172,7 +172,7 @@ def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: in
 
 def bisect_min_time(platform: PlatformConfig, problem: ProblemSpec, t_hi: int,
                     max_states: int = 5_000_000) -> TuneResult:
-    """Counterexample-guided binary search for the minimal time (search.hpp:366-371)."""
+    """Counterexample-guided binary search for the minimal time (search.hpp:58-63)."""
     if t_hi < 1:
         from ._lib import ConfigError
         raise ConfigError("t_hi must be >= 1")
@@ -180,7 +180,7 @@ def bisect_min_time(platform: PlatformConfig, problem: ProblemSpec, t_hi: int,
 
 
 def extract_params(platform: PlatformConfig, problem: ProblemSpec, trace: Trace):
-    """Reads (wg, ts, time) out of a counterexample after replay validation (search.hpp:393-395)."""
+    """Reads (wg, ts, time) out of a counterexample after replay validation (search.hpp:85-87)."""
     from .machine import replay
     replay(platform, problem, trace)
     return trace.params.wg, trace.params.ts, trace.final_time
@@ -195,7 +195,7 @@ class RankedTrail:
 
 
 def rank_trails(traces) -> list:
-    """Stable sort of trail summaries by (time, transitions) (search.hpp:397-398)."""
+    """Stable sort of trail summaries by (time, transitions) (search.hpp:89-90)."""
     out = [RankedTrail(t.final_time, t.params.wg, t.params.ts, t.steps) for t in traces]
     return sorted(out, key=lambda r: (r.time, r.transitions))
 
@@ -203,7 +203,7 @@ def rank_trails(traces) -> list:
 def swarm_min_time(platform: PlatformConfig, problem: ProblemSpec, workers: int = 4,
                    seed: int = 1, trajectories_per_worker: int = 4096, max_rounds: int = 64,
                    max_depth: int = 4_000_000, trails_out: list | None = None) -> TuneResult:
-    """Randomized search for the minimal time (search.hpp:373-379): rounds of
+    """Randomized search for the minimal time (search.hpp:65-71): rounds of
     counter-based Philox trajectories on the GPU with the reference's stop rule.
     Heuristic: never a proof (proven = False)."""
     import time as _time

@@ -1,6 +1,6 @@
 """Exhaustive evaluation of tuning spaces on the GPU (north-star subsystem 1).
 
-A Space generalises the reference's enumerate_configs (model.cpp:179-189):
+A Space generalises the reference's enumerate_configs (model.cpp:90-100):
 besides wg and ts it ranges over the platform shape (nd devices, nu units,
 np = 2^k processing elements = work-items a unit runs at once).  The
 reference's own space for one platform is Space.reference(platform, problem).
