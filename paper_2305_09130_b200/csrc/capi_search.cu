@@ -170,7 +170,9 @@ int prepare(Ctx& c, int64_t max_states) {
     // first table from the cost model: the explored states ran at ~3x the lock-step
     // transitions summed over the configurations on the Table-1 platforms
     // (sizes 8-512); 4x that at load 1/4, clamped to [2^22, 2^29] slots.  Wider
-    // spaces outgrow it and restart 16x larger.
+    // spaces outgrow it and restart 16x larger.  (32x was measured: no restarts
+    // on Table-1 spaces either, but a first sweep then maps a 4x larger fresh
+    // buffer, ~28 ms per GB: size 256 1.40 -> 1.57 s.)
     uint64_t est = 0;
     for (int k = 0; k < nc; ++k) est += (uint64_t)std::max<int64_t>(c.cm_steps[k], 1);
     uint64_t first_cap = 1ull << 22;
@@ -354,8 +356,11 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     c.size = size;
     c.kernel = kernel;
     c.input = input;
+    const bool tt = getenv("MCTB_TUNE_TRACE") != nullptr;
+    const double tp0 = now_ms();
     int rc = prepare(c, max_states);
     if (rc) return rc;
+    const double tp1 = now_ms();
     if (t_hi <= 0) {
         // estimate_initial_time (search.cpp:94-102): mt19937_64(seed) picks a feasible
         // configuration in enumerate_configs order; its SeededRandom run is T_ini.
@@ -367,19 +372,28 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         Mt64 rng;
         rng.seed(seed);
         const int k = order[rng.next() % order.size()];
-        TrajOut o;
-        if ((rc = gpu_run(c.hs[k], MCTB_POLICY_MT19937, seed, 0, 200000000LL, &o, nullptr, 0)))
-            return rc;
-        if (o.status != MCTB_OK) {
-            set_error("model bug: deadlock in the initial-time simulation");
-            return MCTB_MODEL_BUG;
+        const BfsStats& b = c.bfs.stats[k];
+        if (!b.capped && b.terminals > 0 && b.min_time == b.max_time) {
+            // the sweep explored every run of this configuration and they all end at
+            // one time, so the seeded run ends there too: no serial simulation
+            // (a lone GPU thread steps ~2 us per transition; 124 ms at size 128)
+            t_hi = b.min_time;
+        } else {
+            TrajOut o;
+            if ((rc = gpu_run(c.hs[k], MCTB_POLICY_MT19937, seed, 0, 200000000LL, &o, nullptr, 0)))
+                return rc;
+            if (o.status != MCTB_OK) {
+                set_error("model bug: deadlock in the initial-time simulation");
+                return MCTB_MODEL_BUG;
+            }
+            t_hi = o.time;
         }
-        t_hi = o.time;
     }
     if (t_hi < 1) {
         set_error("t_hi must be >= 1");
         return MCTB_CONFIG_ERROR;
     }
+    const double tp2 = now_ms();
     // search.cpp:104-158
     g_probes.clear();
     int checks = 0;
@@ -439,7 +453,12 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         info[3] = (double)c.bfs.states;
         info[4] = c.bfs.ms;  // exploration kernel time (CUDA events)
     }
-    return emit_trace(c, best, trace, cap, trace_len);
+    const double tp3 = now_ms();
+    rc = emit_trace(c, best, trace, cap, trace_len);
+    if (tt)
+        fprintf(stderr, "[tune] prepare %.2f (cost %.2f, bfs %.2f) estimate %.2f bisect %.2f (first %.2f) trace %.2f ms\n",
+                tp1 - tp0, c.ms_cost, c.ms_bfs, tp2 - tp1, tp3 - tp2, c.ms_first, now_ms() - tp3);
+    return rc;
 }
 
 int64_t mctb_tune_probes(int64_t* rows, int64_t cap) {
