@@ -118,7 +118,8 @@ def verdict_to_json(v, T: int, trace_path: str = "") -> str:
     """report.cpp:140-155"""
     j = {"verdict": "violated" if v.violated else "holds", "exhaustive": v.exhaustive, "T": T,
          "states_visited": v.stats.states_visited,
-         "max_depth_reached": v.stats.max_depth_reached, "wall_seconds": 0.0}
+         "max_depth_reached": v.stats.max_depth_reached,
+         "wall_seconds": float(getattr(v.stats, "wall_seconds", 0.0))}
     if v.violated and v.trace is not None:
         j.update(final_time=v.trace.final_time, wg=v.trace.params.wg, ts=v.trace.params.ts)
     if trace_path:
