@@ -484,11 +484,11 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0):
 
 # Thread-level instructions executed per configuration by space_argmin_kernel<0>
 # on this workload: ncu smsp__inst_executed.sum x 32 / 1e9 configurations
-# (profiles/r01_argmin_v7_ncu.txt).  Re-measured after every kernel change.
-INT_OPS_PER_CONFIG = 12.16
+# (profiles/r01_argmin_v8_ncu.txt).  Re-measured after every kernel change.
+INT_OPS_PER_CONFIG = 11.80
 # the binding pipe of that kernel in the same capture:
 # sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active
-ALU_PIPE_FRAC_NCU = 0.832
+ALU_PIPE_FRAC_NCU = 0.814
 
 # configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
 # state (smsp__inst_executed.sum / states; DRAM read + write bytes / states),

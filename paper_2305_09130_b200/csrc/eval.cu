@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                         R += (int32_t)nd;
                     }
                 }
+#pragma unroll 8
                 for (; k < run; ++k) {
                     const uint32_t tf = max(Q + 1, w_hi) * D32;
                     if (tf < best_tf) {
