@@ -13,6 +13,7 @@
 #define MCTUNE_B200_HPP
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdint>
 #include <optional>
@@ -459,6 +460,78 @@ inline RunOutcome replay(const PlatformConfig& platform, const ProblemSpec& prob
     r.transitions = static_cast<long long>(trace.transitions.size());
     if (problem.kernel == KernelKind::Minimum) r.result = out[1];
     return r;
+}
+
+/// Randomised bounded worker (explore.hpp:102-110, explore.cpp:235-281),
+/// re-designed for the GPU.  The reference runs a seed-shuffled DFS with a
+/// fingerprint set per configuration; here every feasible configuration, in
+/// the same mt19937_64(seed) shuffle order, runs `trajectories_per_config`
+/// counter-based Philox schedules (trajectory id t -> configuration t mod n,
+/// one batched launch), and every run that violates `property` yields a trace,
+/// one per distinct (configuration, final time, result), re-run with capture
+/// from its trajectory id.  Same contract: bitstate mode only (ConfigError
+/// otherwise), deterministic per seed, every trace replays; never a proof.
+inline std::vector<Trace> swarm_worker(const PlatformConfig& platform, const ProblemSpec& problem,
+                                       const Property& property, std::uint64_t seed,
+                                       const ExploreLimits& limits,
+                                       ExploreStats* stats_out = nullptr,
+                                       int trajectories_per_config = 256) {
+    if (limits.mode != ExploreLimits::Mode::Bitstate)
+        throw ConfigError("swarm workers run in bitstate mode");
+    if (trajectories_per_config < 1) throw ConfigError("trajectories_per_config must be >= 1");
+    ExploreStats stats;
+    std::vector<TuningParams> configs;
+    for (const auto& c : enumerate_configs(problem.size)) {
+        if (config_feasible(problem, c)) configs.push_back(c);
+        else stats.configs_skipped += 1;
+    }
+    std::vector<Trace> traces;
+    if (configs.empty()) {
+        if (stats_out) stats_out->absorb(stats);
+        return traces;
+    }
+    std::mt19937_64 rng(seed);
+    std::shuffle(configs.begin(), configs.end(), rng);
+    const detail::Args a(platform, problem);
+    const int n = static_cast<int>(configs.size());
+    std::vector<std::int32_t> cfg(2 * static_cast<std::size_t>(n));
+    for (int k = 0; k < n; ++k) {
+        cfg[2 * k] = configs[static_cast<std::size_t>(k)].wg;
+        cfg[2 * k + 1] = configs[static_cast<std::size_t>(k)].ts;
+    }
+    const std::uint64_t n_traj = static_cast<std::uint64_t>(n) * trajectories_per_config;
+    std::vector<std::int64_t> out(6 * n_traj);
+    detail::check(mctb_trajectories(a.plat, a.size, a.kernel, a.input, cfg.data(), n,
+                                    MCTB_POLICY_PHILOX, seed, 0, n_traj, limits.max_depth,
+                                    out.data()));
+    stats.configs_explored = n;
+    std::vector<std::array<std::int64_t, 3>> seen;
+    for (std::uint64_t t = 0; t < n_traj; ++t) {
+        const std::int64_t* r = &out[6 * t];
+        stats.transitions_applied += r[1];
+        stats.states_visited += r[1] + 1;
+        stats.max_depth_reached = std::max<long long>(stats.max_depth_reached, r[1]);
+        if (r[3] == MCTB_LIMIT) {
+            stats.limit_hit = true;
+            continue;
+        }
+        detail::check(static_cast<int>(r[3]));
+        if (!property.violated_by(r[0])) continue;
+        const std::array<std::int64_t, 3> key{r[5], r[0], r[2]};
+        if (std::find(seen.begin(), seen.end(), key) != seen.end()) continue;
+        seen.push_back(key);
+        const TuningParams p = configs[static_cast<std::size_t>(r[5])];
+        std::int64_t o[4];
+        auto tr = detail::with_trace([&](std::int32_t* buf, std::int64_t cap, std::int64_t* len) {
+            return mctb_simulate(a.plat, a.size, a.kernel, a.input, p.wg, p.ts,
+                                 MCTB_POLICY_PHILOX, seed, t, o, buf, cap, len);
+        });
+        if (o[0] != r[0] || o[1] != r[1])
+            throw ModelBug("swarm trajectory " + std::to_string(t) + " did not re-run identically");
+        traces.push_back(Trace{std::move(tr), r[0], p, r[1]});
+    }
+    if (stats_out) stats_out->absorb(stats);
+    return traces;
 }
 
 /// trace_to_text (report.hpp, report.cpp:82-97).

@@ -125,3 +125,31 @@ TEST_CASE("tuning-space argmin: the reference's space and a generalised one") {
     CHECK(w.index == 92160000ull);
     CHECK(w.params == TuningParams{512, 512});
 }
+
+TEST_CASE("swarm workers are deterministic per seed and sound (test_explore.cpp:112-143)") {
+    const ProblemSpec problem = ProblemSpec::abstract(8);
+    ExploreLimits limits;
+    limits.mode = ExploreLimits::Mode::Bitstate;
+    CHECK_THROWS_AS(swarm_worker(kPlat, problem, Property::non_termination(), 1, ExploreLimits{}),
+                    ConfigError);
+    const auto a = swarm_worker(kPlat, problem, Property::non_termination(), 5, limits);
+    const auto b = swarm_worker(kPlat, problem, Property::non_termination(), 5, limits);
+    REQUIRE(a.size() == b.size());
+    CHECK(a.size() == 4);  // every feasible configuration ends at one time
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        CHECK(a[i].final_time == b[i].final_time);
+        CHECK(a[i].params == b[i].params);
+        CHECK(a[i].transitions == b[i].transitions);
+    }
+    for (std::uint64_t seed : {1ull, 2ull}) {
+        ExploreStats st;
+        const auto traces = swarm_worker(kPlat, problem, Property::over_time(44), seed, limits, &st);
+        REQUIRE(!traces.empty());
+        CHECK(st.configs_explored == 4);
+        for (const auto& t : traces) {
+            CHECK(t.final_time <= 44);
+            CHECK(t.params == TuningParams{4, 4});
+            CHECK(replay(kPlat, problem, t).time == t.final_time);
+        }
+    }
+}
