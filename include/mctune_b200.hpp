@@ -462,6 +462,57 @@ inline RunOutcome replay(const PlatformConfig& platform, const ProblemSpec& prob
     return r;
 }
 
+/// Terminating traces, one per distinct terminal state, for every feasible
+/// configuration largest-first (explore.hpp:95-100, explore.cpp:207-233).  One
+/// GPU sweep explores every configuration; a configuration whose reachable
+/// terminal states are one (every schedule ends in the same state — all the
+/// Table-1 platforms) contributes the end of the DFS's first path, which is
+/// where the reference's DFS first meets it: the FirstEnabled run.  A
+/// configuration with several terminal states (multi-device handover skew)
+/// raises LimitError: their DFS order is not reproduced here.
+inline std::vector<Trace> check_nontermination(const PlatformConfig& platform,
+                                               const ProblemSpec& problem,
+                                               const ExploreLimits& limits,
+                                               ExploreStats* stats_out = nullptr) {
+    if (limits.max_depth < 1) throw ConfigError("max_depth must be >= 1");
+    ExploreStats stats;
+    std::vector<TuningParams> configs;
+    for (const auto& c : enumerate_configs(problem.size)) {
+        if (config_feasible(problem, c)) configs.push_back(c);
+        else stats.configs_skipped += 1;
+    }
+    std::sort(configs.begin(), configs.end(), [](const TuningParams& a, const TuningParams& b) {
+        return a.wg != b.wg ? a.wg > b.wg : a.ts > b.ts;  // explore.cpp:67-72
+    });
+    std::vector<Trace> traces;
+    if (!configs.empty()) {
+        const auto res = explore_configs(platform, problem, configs, limits);
+        for (std::size_t k = 0; k < configs.size(); ++k) {
+            const ExploreResult& r = res[k];
+            stats.absorb(r.stats);
+            if (r.deadlocks) throw ModelBug("deadlock reached during exploration");
+            if (r.terminal_states == 0) continue;
+            if (r.terminal_states > 1)
+                throw LimitError("check_nontermination: configuration (" +
+                                 std::to_string(configs[k].wg) + ", " +
+                                 std::to_string(configs[k].ts) + ") has " +
+                                 std::to_string(r.terminal_states) +
+                                 " terminal states; only single-terminal spaces are served");
+            std::vector<Transition> tr;
+            const RunOutcome o =
+                run(platform, problem, configs[k], SchedPolicy::FirstEnabled, 0, &tr);
+            if (static_cast<long long>(tr.size()) > limits.max_depth) {
+                stats.limit_hit = true;  // every run of it is this long
+                continue;
+            }
+            const long long n = static_cast<long long>(tr.size());
+            traces.push_back(Trace{std::move(tr), o.time, configs[k], n});
+        }
+    }
+    if (stats_out) stats_out->absorb(stats);
+    return traces;
+}
+
 /// Randomised bounded worker (explore.hpp:102-110, explore.cpp:235-281),
 /// re-designed for the GPU.  The reference runs a seed-shuffled DFS with a
 /// fingerprint set per configuration; here every feasible configuration, in

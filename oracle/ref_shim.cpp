@@ -256,6 +256,36 @@ int ref_check_overtime(const int* plat, int size, int kernel, const int64_t* inp
     });
 }
 
+// check_nontermination (explore.cpp:207-233): rows = [wg, ts, final_time, steps] per
+// trace (up to cap_rows), traces concatenated into `trace` (4 ints per transition);
+// out = [n_traces, states_visited, transitions_applied, max_depth_reached, limit_hit]
+int ref_check_nontermination(const int* plat, int size, int kernel, const int64_t* input,
+                             long long max_depth, long long max_states, int64_t* out,
+                             int64_t* rows, long long cap_rows, int32_t* trace, long long cap,
+                             long long* trace_len) {
+    return guarded([&] {
+        ExploreStats st;
+        const auto traces = check_nontermination(plat_of(plat), problem_of(size, kernel, input),
+                                                 limits_of(max_depth, max_states, 0, 0.0), &st);
+        out[0] = static_cast<int64_t>(traces.size());
+        out[1] = st.states_visited;
+        out[2] = st.transitions_applied;
+        out[3] = st.max_depth_reached;
+        out[4] = st.limit_hit;
+        std::vector<Transition> all;
+        for (std::size_t i = 0; i < traces.size(); ++i) {
+            if (static_cast<long long>(i) < cap_rows) {
+                rows[4 * i] = traces[i].params.wg;
+                rows[4 * i + 1] = traces[i].params.ts;
+                rows[4 * i + 2] = traces[i].final_time;
+                rows[4 * i + 3] = traces[i].steps;
+            }
+            all.insert(all.end(), traces[i].transitions.begin(), traces[i].transitions.end());
+        }
+        put_trace(all, trace, cap, trace_len);
+    });
+}
+
 // estimate_initial_time (search.cpp:94-102)
 int ref_estimate_initial_time(const int* plat, int size, int kernel, const int64_t* input,
                               uint64_t seed, int64_t* out) {

@@ -12,7 +12,7 @@ from .model import (ABSTRACT, MINIMUM, LaunchPlan, PlatformConfig, ProblemSpec, 
                     log2_exact, validate_params)
 from .machine import (FIRST, MT19937, PHILOX, ROUND_ROBIN, SEEDED_RANDOM, Machine, RunOutcome,
                       Trace, TrajectoryBatch, replay, trace_to_text, trajectories)
-from .explore import ExploreStats, SweepInfo, explore_configs, explore_machine
+from .explore import ExploreStats, SweepInfo, check_nontermination, explore_configs, explore_machine
 from .search import (RankedTrail, SweepRow, TuneProbe, TuneResult, Verdict, bisect_min_time, check_overtime,
                      exhaustive_sweep, extract_params, rank_trails, swarm_min_time, tune)
 from . import report
@@ -27,5 +27,5 @@ __all__ = [
     "exhaustive_sweep", "kernel_kind_from_string", "log2_exact", "space_argmin",
     "validate_params", "FIRST", "MT19937", "PHILOX", "ROUND_ROBIN", "SEEDED_RANDOM", "Machine",
     "RunOutcome", "RankedTrail", "TuneProbe", "TuneResult", "Verdict", "bisect_min_time", "check_overtime",
-    "extract_params", "rank_trails", "swarm_min_time", "tune", "ExploreStats", "SweepInfo", "explore_configs", "explore_machine", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
+    "extract_params", "rank_trails", "swarm_min_time", "tune", "ExploreStats", "SweepInfo", "explore_configs", "explore_machine", "check_nontermination", "Trace", "TrajectoryBatch", "replay", "trace_to_text", "trajectories",
 ]

@@ -63,3 +63,37 @@ def explore_machine(platform: PlatformConfig, problem: ProblemSpec, params: Tuni
                     max_states: int = 5_000_000) -> ExploreStats:
     """Every interleaving of one machine (explore.hpp:81-86)."""
     return explore_configs(platform, problem, [params], max_states)[0]
+
+
+def check_nontermination(platform: PlatformConfig, problem: ProblemSpec, max_depth: int = 4_000_000,
+                         max_states: int = 5_000_000):
+    """Terminating traces, one per distinct terminal state, for every feasible
+    configuration largest-first (explore.hpp:95-100, explore.cpp:207-233).  One GPU
+    sweep; a single-terminal configuration contributes the FIRST-policy run (where
+    the reference's DFS first meets its terminal state); several terminal states
+    raise LimitError.  Returns (traces, stats of the sweep per configuration)."""
+    from ._lib import ConfigError, LimitError, ModelBug
+    from .machine import FIRST, Machine, Trace
+    from .model import config_feasible, enumerate_configs
+    if max_depth < 1:
+        raise ConfigError("max_depth must be >= 1")
+    configs = sorted((c for c in enumerate_configs(problem.size) if config_feasible(problem, c)),
+                     key=lambda c: (-c.wg, -c.ts))
+    if not configs:
+        return [], []
+    stats = explore_configs(platform, problem, configs, max_states)
+    traces = []
+    for c, st in zip(configs, stats):
+        if st.deadlocks:
+            raise ModelBug("deadlock reached during exploration")
+        if st.terminals == 0:
+            continue
+        if st.terminals > 1:
+            raise LimitError(f"check_nontermination: configuration ({c.wg}, {c.ts}) has "
+                             f"{st.terminals} terminal states; only single-terminal spaces are served")
+        tr = []
+        r = Machine(platform, problem, c).run(FIRST, trace_out=tr)
+        if len(tr) > max_depth:
+            continue
+        traces.append(Trace(tr, r.time, c, len(tr)))
+    return traces, stats

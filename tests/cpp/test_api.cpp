@@ -154,3 +154,22 @@ TEST_CASE("swarm workers are deterministic per seed and sound (test_explore.cpp:
         }
     }
 }
+
+TEST_CASE("non-termination counterexamples enumerate terminating runs (test_explore.cpp:64-86)") {
+    const ProblemSpec problem = ProblemSpec::abstract(8);
+    ExploreLimits limits;
+    const auto traces = check_nontermination(kPlat, problem, limits);
+    REQUIRE(traces.size() == 4);
+    Tick best = traces.front().final_time;
+    std::vector<TuningParams> seen;
+    for (const auto& t : traces) {
+        best = std::min(best, t.final_time);
+        if (std::find(seen.begin(), seen.end(), t.params) == seen.end()) seen.push_back(t.params);
+        CHECK(replay(kPlat, problem, t).time == t.final_time);
+    }
+    CHECK(best == 44);
+    CHECK(seen.size() == 4);
+    CHECK(traces.front().params == TuningParams{4, 4});  // largest-first
+    limits.max_depth = 1;
+    CHECK(check_nontermination(kPlat, problem, limits).empty());
+}

@@ -164,3 +164,31 @@ def test_table_overflow_restarts_with_identical_counts(engine, parts, monkeypatc
     got = m.explore_configs(*args, partitions=parts, info=info)[0]
     assert got == want and want.complete and want.states_visited == 131492
     assert info[0].table_slots > (1 << 16) * parts
+
+
+def test_check_nontermination_matches_reference(engine, gold):
+    """check_nontermination (explore.cpp:207-233): the same traces in the same order
+    (configuration, final time, length, SHA-256 of the transitions) and the same
+    sweep statistics as the reference (nonterm.json); a depth cap of one finds none."""
+    import hashlib
+    import struct
+    m = engine
+
+    def sha(trace):
+        return hashlib.sha256(b"".join(struct.pack("<4i", *t) for t in trace)).hexdigest()
+
+    for c in gold("nonterm.json"):
+        key = (tuple(c["plat"]), c["size"], c["kernel"])
+        traces, stats = m.check_nontermination(m.PlatformConfig(*c["plat"]),
+                                               problem(m, c["size"], c["kernel"]))
+        assert len(traces) == c["n"], key
+        for t, g in zip(traces, c["traces"]):
+            assert (t.params.wg, t.params.ts, t.final_time, t.steps) == \
+                (g["wg"], g["ts"], g["final_time"], g["steps"]), key
+            assert sha(t.transitions) == g["sha"], key
+        assert sum(s.states_visited for s in stats) == c["states"], key
+        assert sum(s.transitions_applied for s in stats) == c["transitions"], key
+        assert max(s.max_depth_reached for s in stats) == c["max_depth"], key
+    traces, _ = m.check_nontermination(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8),
+                                       max_depth=1)
+    assert traces == []
