@@ -28,7 +28,7 @@ def ref_nonterm(ref, plat, size, kernel, max_depth=0, max_states=0):
                                               out, rows, C.c_longlong(256), buf,
                                               C.c_longlong(TRACE_CAP), C.byref(n)))
     trs, pos, allt = [], 0, _untr(buf, n.value)
-    for i in range(out[0]):
+    for i in range(min(out[0], 256)):
         wg, ts, t, steps = rows[4 * i:4 * i + 4]
         trs.append({"wg": wg, "ts": ts, "final_time": t, "steps": steps,
                     "sha": trace_sha(allt[pos:pos + steps])})

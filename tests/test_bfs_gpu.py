@@ -192,3 +192,7 @@ def test_check_nontermination_matches_reference(engine, gold):
     traces, _ = m.check_nontermination(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8),
                                        max_depth=1)
     assert traces == []
+    # handover skew: the reference returns > 256 terminal states for this space;
+    # the engine refuses rather than return a different set
+    with pytest.raises(m.LimitError):
+        m.check_nontermination(m.PlatformConfig(3, 1, 1, 1), m.ProblemSpec.minimum(32))
