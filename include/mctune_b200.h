@@ -41,7 +41,11 @@ extern "C" {
 #define MCTB_POLICY_PHILOX 3      /* swarm trajectory: Philox4x32-10 counter-based choice */
 #define MCTB_POLICY_TICK_LAST 4   /* clock ticks only when nothing else is enabled (lock-step) */
 
-/* argmin key: (min(time, 2^30-1) << 33) | config index  (index < 2^33) */
+/* argmin key: (min(time, 2^30-1) << 33) | config index  (index < 2^33).
+ * The key is exact whenever its time field is below 2^30-1.  A saturated time
+ * field means every configuration of the range has time >= 2^30-1 (or is
+ * infeasible); mctb_space_argmin then resolves the winner exactly with
+ * mctb_space_exact_async's two passes, and so must a caller of the async call. */
 #define MCTB_KEY_TIME_BITS 30
 #define MCTB_KEY_INDEX_BITS 33
 
@@ -73,10 +77,18 @@ uint64_t mctb_space_count(const int64_t* sd);
 int mctb_space_argmin_async(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* d_key,
                             void* stream);
 
-/* Host-buffer argmin (end to end, including the host<->device copies).
+/* Host-buffer argmin (end to end, including the host<->device copies); exact for
+ * every space (a saturated key is resolved by the exact passes below).
  * out = {time, steps, nd, nu, np, gmt, wg, ts} of the winning configuration. */
 int mctb_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* key,
                       int64_t* out);
+
+/* Exact argmin of [first, first+count) in two plain passes, no packing: *d_time =
+ * the least 64-bit model time of the feasible configurations (UINT64_MAX: none),
+ * then *d_index = the least index with that time (device pointers; both are reset
+ * by the call).  The resolution of a saturated key (search.cpp:67-78 tie rule). */
+int mctb_space_exact_async(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* d_time,
+                           uint64_t* d_index, void* stream);
 
 /* Per-configuration table: d_time[i], d_steps[i] for index first+i (device
  * pointers; time = -1 for infeasible configurations). */
@@ -132,7 +144,10 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
 
 /* explore_machine (explore.hpp:81-86) over several configurations in one GPU sweep
  * (configs = int32[2 * n] of (wg, ts)); max_states = the reference's per-machine visited
- * cap (ExploreLimits::max_states, default 5e6 when <= 0); flags bit 0 = check
+ * cap (ExploreLimits::max_states, default 5e6 when <= 0); max_depth =
+ * ExploreLimits::max_depth (>= 1, else MCTB_CONFIG_ERROR as explore.cpp:91; the
+ * reference default is 4e6): states deeper than it are not explored
+ * (explore.cpp:124-127) and complete is 0 when one was cut; flags bit 0 = check
  * Machine::check_invariants (machine.cpp:719-756) and tick gating on every state;
  * bits 8-11 = P > 1 splits the visited set into P hash partitions on this device,
  * the exchange of the multi-GPU sweep (mctb_explore_mp_*) run on one GPU; bit 1 =
@@ -142,8 +157,8 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
  *                      invariant_violations}
  * info = int64[4]: {table slots, total states, packed key words, kernel microseconds} */
 int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
-                 const int32_t* configs, int n_configs, int64_t max_states, int flags,
-                 int64_t* out, int64_t* info);
+                 const int32_t* configs, int n_configs, int64_t max_states, int64_t max_depth,
+                 int flags, int64_t* out, int64_t* info);
 
 /* Multi-GPU explore_machine: one process per GPU (rank r of world <= 8), each
  * owning the hash partition r of the visited set; successors owned by another
@@ -165,23 +180,24 @@ int mctb_explore_mp_seed(void* ctx);
 int mctb_explore_mp_run(void* ctx, int64_t* out, int64_t* info);
 void mctb_explore_mp_close(void* ctx);
 
-/* check_overtime (explore.hpp:88-93), exact mode.
+/* check_overtime (explore.hpp:88-93), exact mode, within ExploreLimits' max_states and
+ * max_depth (>= 1; the DFS meets no state deeper than max_depth, explore.cpp:124-127).
  * out = int64[12]: {violated, exhaustive, states_visited, max_depth_reached,
  *                   transitions_applied, configs_explored, configs_skipped, final_time, wg,
  *                   ts, steps, trace_exact}; the counterexample goes to trace. */
 int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* input, int64_t T,
-                        int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
-                        int64_t* trace_len);
+                        int64_t max_states, int64_t max_depth, int64_t* out, int32_t* trace,
+                        int64_t cap, int64_t* trace_len);
 
 /* The `tune` flow: estimate_initial_time (search.hpp:53-56) when t_hi <= 0, then
- * bisect_min_time (search.hpp:58-63).
+ * bisect_min_time (search.hpp:58-63); every probe within max_states / max_depth.
  * out = int64[10]: {t_min, wg, ts, t_ini, proven, checks_run, states_visited_total,
  *                   first_trail_time, steps, trace_exact}
  * info = double[5] (optional): {ms cost model, ms first paths, ms exploration,
  *                               explored states, ms exploration kernel} */
 int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64_t t_hi,
-              uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
-              int64_t* trace_len, double* info);
+              uint64_t seed, int64_t max_states, int64_t max_depth, int64_t* out, int32_t* trace,
+              int64_t cap, int64_t* trace_len, double* info);
 
 /* The bound-lowering probes of the last mctb_tune on the calling thread, in
  * order: rows = int64[8 * cap] {T, violated, exhaustive, states_visited, wg, ts,

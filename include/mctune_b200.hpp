@@ -313,9 +313,11 @@ struct Property {
     }
 };
 
-/// explore.hpp:38-44.  max_states is the per-configuration visited cap; the
-/// engine's exploration is exact (Bitstate is rejected like the reference's
-/// bisection rejects it) and has no depth or wall-clock cut.
+/// explore.hpp:38-44.  max_states is the per-configuration visited cap and
+/// max_depth the DFS's depth cut (explore.cpp:124-127; the state graphs are
+/// graded, so the cut is order-independent and the GPU sweep reproduces it).
+/// The engine's exploration is exact (Bitstate is rejected like the
+/// reference's bisection rejects it); wall_budget_secs bounds nothing here.
 struct ExploreLimits {
     long long max_depth = 4'000'000;
     long long max_states = 5'000'000;
@@ -387,7 +389,7 @@ inline std::vector<ExploreResult> explore_configs(const PlatformConfig& platform
     const auto t0 = detail::Clock::now();
     detail::check(mctb_explore(a.plat, a.size, a.kernel, a.input, c.data(),
                                static_cast<int>(configs.size()), limits.max_states,
-                               check_invariants ? 1 : 0, out.data(), info));
+                               limits.max_depth, check_invariants ? 1 : 0, out.data(), info));
     const double wall = detail::since(t0);
     std::vector<ExploreResult> res(configs.size());
     for (std::size_t i = 0; i < configs.size(); ++i) {
@@ -424,7 +426,8 @@ inline Verdict check_overtime(const PlatformConfig& platform, const ProblemSpec&
     std::int64_t out[12];
     const auto t0 = detail::Clock::now();
     auto tr = detail::with_trace([&](std::int32_t* buf, std::int64_t cap, std::int64_t* len) {
-        return mctb_check_overtime(a.plat, a.size, a.kernel, a.input, T, limits.max_states, out,
+        return mctb_check_overtime(a.plat, a.size, a.kernel, a.input, T, limits.max_states,
+                                   limits.max_depth, out,
                                    buf, cap, len);
     });
     Verdict v;
@@ -677,7 +680,8 @@ inline TuneResult tune_call(const PlatformConfig& platform, const ProblemSpec& p
     std::int64_t out[10];
     const auto t0 = Clock::now();
     auto tr = with_trace([&](std::int32_t* buf, std::int64_t cap, std::int64_t* len) {
-        return mctb_tune(a.plat, a.size, a.kernel, a.input, t_hi, seed, limits.max_states, out,
+        return mctb_tune(a.plat, a.size, a.kernel, a.input, t_hi, seed, limits.max_states,
+                         limits.max_depth, out,
                          buf, cap, len, nullptr);
     });
     TuneResult r;

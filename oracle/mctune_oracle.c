@@ -1668,9 +1668,18 @@ int mo_space_decode(const int64_t* sd, uint64_t index, int* cfg) {
 #define MO_KEY_TIME_BITS 30
 #define MO_KEY_INDEX_BITS 33
 
+/* Exact argmin of [first, first+count): the least (time, index) over the feasible
+ * configurations — the reference's tie rule (search.cpp:67-78: least time, then
+ * the preferred configuration, which the index order puts first).  best_time = -1
+ * and best_index = UINT64_MAX when the range holds no feasible configuration.
+ * best_key is the GPU's packed key of the range, (min(time, 2^30-1) << 33) | index
+ * minimised over every configuration (infeasible ones carry the saturated time):
+ * exact only while its time field is below 2^30-1, which is why best_time and
+ * best_index are computed without it. */
 int mo_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* best_key,
                     int64_t* best_time, uint64_t* best_index) {
-    uint64_t best = UINT64_MAX;
+    uint64_t best = UINT64_MAX, bi = UINT64_MAX;
+    int64_t bt = -1;
     const uint64_t sat = (1ull << MO_KEY_TIME_BITS) - 1;
     for (uint64_t i = first; i < first + count; ++i) {
         int c[8];
@@ -1681,13 +1690,17 @@ int mo_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_t*
             int64_t t, st;
             cost_model(&p, c[4], c[5], c[6], c[7], &t, &st);
             tf = (uint64_t)t < sat ? (uint64_t)t : sat;
+            if (bt < 0 || t < bt) { /* ascending index: the first of equal times stays */
+                bt = t;
+                bi = i;
+            }
         }
         const uint64_t key = (tf << MO_KEY_INDEX_BITS) | i;
         if (key < best) best = key;
     }
     *best_key = best;
-    *best_index = best & ((1ull << MO_KEY_INDEX_BITS) - 1);
-    *best_time = (int64_t)(best >> MO_KEY_INDEX_BITS);
+    *best_time = bt;
+    *best_index = bi;
     return MO_OK;
 }
 

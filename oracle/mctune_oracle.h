@@ -80,7 +80,9 @@ int64_t mo_trace_text(const int* plat, int size, int kernel, const int64_t* inpu
                       int ts, const mo_transition* trace, int64_t len, char* buf, int64_t cap);
 
 /* Argmin of the cost model over a generalised tuning space (the exhaustive-evaluation
- * oracle for the GPU kernel).  Space layout in DESIGN.md §4 / include/mctune_b200.h. */
+ * oracle for the GPU kernel).  Space layout in DESIGN.md §4 / include/mctune_b200.h.
+ * best_time/best_index: the exact least (time, index) of the feasible configurations
+ * (-1 / UINT64_MAX: none); best_key: the GPU's packed, saturating key of the range. */
 int mo_space_argmin(const int64_t* space_desc, uint64_t first, uint64_t count,
                     uint64_t* best_key, int64_t* best_time, uint64_t* best_index);
 int mo_space_decode(const int64_t* space_desc, uint64_t index, int* cfg /* nd,nu,np,gmt,size,kernel,wg,ts */);

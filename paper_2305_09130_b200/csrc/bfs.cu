@@ -54,6 +54,7 @@ struct BfsPart {
     // discovered but not yet expanded move together in one atomic
     unsigned long long* tq;
     int* error;                // 1 table full, 2 queue full, 3 model bug, >= 5 watchdog
+    uint32_t* depth;           // [cap] depth | guard of each slot's state (depth cap only)
 };
 
 struct BfsArgs {
@@ -73,6 +74,8 @@ struct BfsArgs {
     int keep;         // continue with the first new successor (no queue round trip)
     unsigned long long* op_hist;  // generic successors per op (diagnostics)
     int check_inv;                // check Machine::check_invariants on every state
+    unsigned flush_states;        // publish a warp's state count once it holds this many
+    uint32_t depth_cap;           // ExploreLimits::max_depth (0: no state reaches it)
 };
 
 namespace {
@@ -335,6 +338,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     unsigned long long h_next = 0, h_end = 0, h_run = 0;
     unsigned claim = 1;
     uint32_t peek = kEmpty;  // lane j: entry h_run + j of the current run, as first read
+    uint32_t dep = 0;        // depth of the parent (tracked under a depth cap only)
     for (;;) {
         if (!local) {
             if (h_next == h_end) {
@@ -393,6 +397,21 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             }
             if (lane < SW - 2) pwords[lane] = w;
             H = warp_sum64(lane < a.words ? (uint64_t)w * hk[lane] : 0ull);
+            if (a.depth_cap) {
+                // written by the slot's claimer with its guard bit, like the key words
+                uint32_t dv = 0;
+                if (lane == 0)
+                    for (unsigned spins = 0;; ++spins) {
+                        dv = ld_relaxed32<SYS>(me.depth + slot);
+                        if (dv & kGuard) break;
+                        if (spins > (1u << 22)) {  // watchdog: a depth that never arrives
+                            set_error<SYS>(me.error, 6);
+                            break;
+                        }
+                        __nanosleep(64);
+                    }
+                dep = __shfl_sync(0xffffffffu, dv, 0) & ~kGuard;
+            }
             __syncwarp();
         }
         const int cfg = peek_cfg(pwords, a.cfg_bits);
@@ -401,7 +420,12 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             cur_cfg = cfg;
             since = 0;
         }
-        if ((since++ & 63) == 0) {
+        if ((since++ & 63) == 0 || n_states >= a.flush_states) {
+            // publish this warp's count first: the cap check below must see every
+            // warp's insertions, or each warp would stop only at its own local cap
+            // and max_states would bound neither work nor memory
+            flush();
+            __syncwarp();
             g_states = ld_relaxed64<false>(&a.stats[cfg].states);
             g_err = any_error<SYS>(a);
         }
@@ -452,6 +476,9 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
         } else if (g_states + n_states >= a.cfg_cap) {
             // explore.cpp:28: a full visited set inserts nothing more
             if (lane == 0) st.capped = 1;
+        } else if (a.depth_cap && dep >= a.depth_cap) {
+            // explore.cpp:124-127: a transition past max_depth is not applied
+            if (lane == 0) st.depth_cut = 1;
         } else {
             n_trans += (unsigned)ne;
             for (int base = 0; base < ne; base += 32) {
@@ -483,6 +510,8 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                     if (a.n_parts > 1) owner = owner_of(hh, a.n_parts);
                     ins = table_insert<SW, SYS>(a, a.part[owner], row, hh);
                     if (ins == -2) set_error<SYS>(me.error, 1);
+                    if (ins >= 0 && a.depth_cap)
+                        st_relaxed32<SYS>(a.part[owner].depth + ins, (dep + 1) | kGuard);
                 }
                 bool fresh = ins >= 0;
                 int keeper = -1;
@@ -513,6 +542,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
         if (local) {
             if (lane < SW - 2) pwords[lane] = kwords[lane];
             H = H_kept;
+            dep += 1;
             __syncwarp();
         } else if (lane == 0) {
             atom_add<SYS>(me.tq, ~0ull);  // this state is expanded: outstanding - 1
@@ -522,7 +552,8 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
 }
 
 template <int SW, bool SYS>
-__global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
+__global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds,
+                            const uint32_t* seed_dep) {
     // one initial state per configuration (explore.cpp:98-105), or the given
     // packed states of configuration 0 (a multi-source exploration), each into
     // its owner partition
@@ -550,7 +581,13 @@ __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds) {
         return;
     }
     atomicAdd(&a.stats[cfg].states, 1ull);
+    if (a.depth_cap)
+        st_relaxed32<SYS>(pt.depth + ins, (seeds && seed_dep ? seed_dep[c] : 0u) | kGuard);
     const unsigned long long pos = atom_add<SYS>(pt.tq, (1ull << 32) | 1ull) >> 32;
+    if (pos >= a.queue_cap) {  // as push_fresh: the queue sits before the counters
+        set_error<SYS>(pt.error, 2);
+        return;
+    }
     st_relaxed32<SYS>(&pt.queue[pos], (uint32_t)ins);
 }
 
@@ -563,6 +600,14 @@ Layout bfs_layout(const MachDesc& m, int n_cfg) {
     const int64_t per_item = m.kernel == 0 ? (int64_t)m.reps * (m.gmt * m.ts + m.ts) + m.gmt
                                            : (int64_t)m.ts * m.gmt + m.nwe + m.gmt;
     return make_layout(m, n_cfg, groups * m.wg * per_item + 1);
+}
+
+uint64_t depth_bound(const MachDesc& m, int64_t protocol_steps) {
+    // every tick consumes >= 1 busy tick of some element (bfs_layout's time bound)
+    const int64_t groups = (int64_t)m.device_rounds * m.nwu;
+    const int64_t per_item = m.kernel == 0 ? (int64_t)m.reps * (m.gmt * m.ts + m.ts) + m.gmt
+                                           : (int64_t)m.ts * m.gmt + m.nwe + m.gmt;
+    return (uint64_t)protocol_steps + (uint64_t)(groups * m.wg * per_item + 1);
 }
 
 // Descriptors, packed layouts and field tables of a sweep (bfs_plan) — shared by
@@ -605,7 +650,7 @@ static int bfs_plan(std::vector<MachHost>& hs, cudaStream_t st, BfsPlan* pl) {
 }
 
 using ExploreFn = void (*)(BfsArgs);
-using SeedFn = void (*)(BfsArgs, const uint32_t*, int);
+using SeedFn = void (*)(BfsArgs, const uint32_t*, int, const uint32_t*);
 
 static ExploreFn explore_fn(int sw, bool sys) {
     if (sw == 16) return sys ? explore_kernel<16, true> : explore_kernel<16, false>;
@@ -635,30 +680,32 @@ static int bfs_grid(ExploreFn kern, int sw, int* grid, size_t* dyn_smem) {
     return MCTB_OK;
 }
 
-// Bytes of one partition (table + queue + counters) and the counters' offset.
-static size_t part_bytes(uint64_t cap, int sw, size_t* misc_off) {
+// Bytes of one partition (table + queue + counters [+ depths]) and the counters'
+// offset.
+static size_t part_bytes(uint64_t cap, int sw, size_t* misc_off, bool depth = false) {
     const size_t sz_table = cap * 4 * (size_t)sw, sz_q = (cap / 2) * 4;
     *misc_off = sz_table + sz_q;
-    return sz_table + sz_q + 256;
+    return sz_table + sz_q + 256 + (depth ? cap * 4 : 0);
 }
 
-static void part_at(char* base, uint64_t cap, int sw, BfsPart* p) {
+static void part_at(char* base, uint64_t cap, int sw, BfsPart* p, bool depth = false) {
     size_t misc_off = 0;
-    part_bytes(cap, sw, &misc_off);
+    part_bytes(cap, sw, &misc_off, depth);
     p->table = (uint32_t*)base;
     p->queue = (uint32_t*)(base + cap * 4 * (size_t)sw);
     char* misc = base + misc_off;
     p->head = (unsigned long long*)misc;
     p->tq = (unsigned long long*)(misc + 8);
     p->error = (int*)(misc + 24);
+    p->depth = depth ? (uint32_t*)(misc + 256) : nullptr;
 }
 
-static int part_clear(char* base, uint64_t cap, int sw, cudaStream_t st) {
+static int part_clear(char* base, uint64_t cap, int sw, cudaStream_t st, bool depth = false) {
     size_t misc_off = 0;
-    part_bytes(cap, sw, &misc_off);
+    part_bytes(cap, sw, &misc_off, depth);
     MCTB_CUDA(cudaMemsetAsync(base, 0, cap * 4 * (size_t)sw, st));
     MCTB_CUDA(cudaMemsetAsync(base + cap * 4 * (size_t)sw, 0xff, (cap / 2) * 4, st));
-    MCTB_CUDA(cudaMemsetAsync(base + misc_off, 0, 256, st));
+    MCTB_CUDA(cudaMemsetAsync(base + misc_off, 0, 256 + (depth ? cap * 4 : 0), st));
     return MCTB_OK;
 }
 
@@ -681,7 +728,7 @@ static int shared_init(const BfsPlan& pl, char* blk, BfsArgs* a, cudaStream_t st
     MCTB_CUDA(cudaMemcpyAsync(d_ftab + pl.ftab.size(), pl.nfields.data(), pl.nfields.size() * 4,
                               cudaMemcpyHostToDevice, st));
     std::vector<BfsStats> init(pl.n_cfg);
-    for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0, 0};
+    for (auto& x : init) x = BfsStats{0, 0, 0, INT64_MAX, -1, 0, 0, 0, 0, 0};
     MCTB_CUDA(cudaMemcpyAsync(a->stats, init.data(), sizeof(BfsStats) * pl.n_cfg,
                               cudaMemcpyHostToDevice, st));
     MCTB_CUDA(cudaMemcpyAsync((void*)a->descs, pl.descs.data(), sizeof(BfsDesc) * pl.n_cfg,
@@ -693,17 +740,24 @@ static int shared_init(const BfsPlan& pl, char* blk, BfsArgs* a, cudaStream_t st
 }
 
 static int seed_launch(const BfsPlan& pl, const BfsArgs& a, bool sys, const std::vector<uint32_t>* seeds,
-                       cudaStream_t st) {
+                       cudaStream_t st, const std::vector<uint32_t>* seed_depths = nullptr) {
     uint32_t* d_seeds = nullptr;
+    uint32_t* d_dep = nullptr;
     int n_seeds = 0;
     if (seeds && !seeds->empty()) {
         n_seeds = (int)(seeds->size() / pl.words);
         MCTB_CUDA(cudaMallocAsync(&d_seeds, seeds->size() * 4, st));
         MCTB_CUDA(cudaMemcpyAsync(d_seeds, seeds->data(), seeds->size() * 4, cudaMemcpyHostToDevice, st));
+        if (seed_depths && (int)seed_depths->size() == n_seeds) {
+            MCTB_CUDA(cudaMallocAsync(&d_dep, n_seeds * 4, st));
+            MCTB_CUDA(cudaMemcpyAsync(d_dep, seed_depths->data(), n_seeds * 4,
+                                      cudaMemcpyHostToDevice, st));
+        }
     }
     const int n_first = seeds ? n_seeds : pl.n_cfg;
-    seed_fn(pl.sw, sys)<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds);
+    seed_fn(pl.sw, sys)<<<(n_first + 127) / 128 + 1, 128, 0, st>>>(a, d_seeds, n_seeds, d_dep);
     if (d_seeds) cudaFreeAsync(d_seeds, st);
+    if (d_dep) cudaFreeAsync(d_dep, st);
     MCTB_CUDA(cudaGetLastError());
     return MCTB_OK;
 }
@@ -800,7 +854,9 @@ struct AsyncFree {
 
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds, int n_parts,
-            bool sys_scope, uint64_t first_cap) {
+            bool sys_scope, uint64_t first_cap, uint32_t depth_cap,
+            const std::vector<uint32_t>* seed_depths) {
+    const bool dep = depth_cap > 0;
     if (n_parts < 1 || n_parts > kMaxParts) {
         set_error("partitions must be in [1, 8]");
         return MCTB_CONFIG_ERROR;
@@ -817,7 +873,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     size_t free_b = 0, total_b = 0;
     MCTB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     free_b += table_cached_bytes();  // the cached table buffer is ours to reuse
-    const double slot_bytes = 4.0 * sw + 2.0;  // slot line + queue (half the slots)
+    const double slot_bytes = 4.0 * sw + 2.0 + (dep ? 4.0 : 0.0);  // slot line + queue (+ depth)
     // capacity grows 16x on overflow; the sweep restarts (all counts are rebuilt)
     // first capacity: enough for the bound up to 2^29 slots (a restart loses the
     // work done, so large sweeps start large); then 16x per overflow.  Split over
@@ -850,21 +906,27 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
         a.check_inv = check_invariants ? 1 : 0;
+        // the visited cap must bound the sweep: every warp publishes its count at
+        // least every 64 expansions, and sooner under a small cap, so the states
+        // inserted past the cap stay below ~grid warps x 48 (cap <= table / 4)
+        a.flush_states = (unsigned)std::min<uint64_t>(
+            4096, std::max<uint64_t>(16, cfg_cap / (4ull * grid * (kBfsThreads / 32))));
         a.n_parts = n_parts;
         a.part0 = 0;
         a.n_here = n_parts;
+        a.depth_cap = depth_cap;
         size_t misc_off = 0;
-        const size_t pb = (part_bytes(cap, sw, &misc_off) + 255) & ~(size_t)255;
+        const size_t pb = (part_bytes(cap, sw, &misc_off, dep) + 255) & ~(size_t)255;
         TableLease lease;  // returned to the cache when this attempt ends
         lease.st = st;
         if ((rc = table_lease(pb * n_parts + shared_bytes(pl), &lease.p, &lease.bytes))) return rc;
         char* b = (char*)lease.p;
         for (int p = 0; p < n_parts; ++p) {
-            part_at(b + pb * p, cap, sw, &a.part[p]);
-            if ((rc = part_clear(b + pb * p, cap, sw, st))) return rc;
+            part_at(b + pb * p, cap, sw, &a.part[p], dep);
+            if ((rc = part_clear(b + pb * p, cap, sw, st, dep))) return rc;
         }
         if ((rc = shared_init(pl, b + pb * n_parts, &a, st))) return rc;
-        if ((rc = seed_launch(pl, a, sys_scope, seeds, st))) return rc;
+        if ((rc = seed_launch(pl, a, sys_scope, seeds, st, seed_depths))) return rc;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -982,11 +1044,15 @@ int check_machine(const int* plat, int size, int kernel, int wg, int ts);
 extern "C" {
 
 int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
-                 const int32_t* configs, int n_configs, int64_t max_states, int flags,
-                 int64_t* out, int64_t* info) {
+                 const int32_t* configs, int n_configs, int64_t max_states, int64_t max_depth,
+                 int flags, int64_t* out, int64_t* info) {
     int rc;
     if (n_configs < 1) {
         set_error("no configurations");
+        return MCTB_CONFIG_ERROR;
+    }
+    if (max_depth < 1) {  // explore.cpp:91
+        set_error("max_depth must be >= 1");
         return MCTB_CONFIG_ERROR;
     }
     std::vector<MachHost> hs(n_configs);
@@ -1003,8 +1069,23 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     // flags: bit 0 invariants; bits 8-11 hash partitions on this device (0 = 1);
     // bit 1 system-scope memory operations (the multi-GPU kernel variant)
     const int n_parts = std::max(1, (flags >> 8) & 15);
+    // protocol transitions of every run (steps - time of the cost model): a terminal
+    // state of time t sits at depth protocol + t
+    std::vector<int64_t> proto(n_configs);
+    uint32_t depth_cap = 0;
+    for (int c = 0; c < n_configs; ++c) {
+        int logn = 0, lw = 0, lt = 0, lp = 0;
+        while ((1 << logn) < size) ++logn;
+        while ((1 << lw) < configs[2 * c]) ++lw;
+        while ((1 << lt) < configs[2 * c + 1]) ++lt;
+        while ((1 << lp) < plat[2]) ++lp;
+        const Cost cm = lockstep_cost(kernel, logn, plat[3], Config{plat[0], plat[1], lp, lw, lt});
+        proto[c] = cm.steps - cm.time;
+        if (depth_bound(hs[c].d, proto[c]) > (uint64_t)max_depth)
+            depth_cap = (uint32_t)std::min<int64_t>(max_depth, 0x7fffffff);
+    }
     rc = run_bfs(hs, cap * (uint64_t)n_configs, cap, &r, st, (flags & 1) != 0, nullptr, n_parts,
-                 (flags & 2) != 0);
+                 (flags & 2) != 0, 0, depth_cap);
     cudaStreamDestroy(st);
     if (rc) return rc;
     if (r.error == 3) {
@@ -1019,18 +1100,13 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
         const BfsStats& s = r.stats[c];
         int64_t* o = out + 9 * c;
         o[8] = (int64_t)s.violations;
-        o[0] = !s.capped;
+        o[0] = !s.capped && !s.depth_cut;
         o[1] = (int64_t)std::min<uint64_t>(s.states, cap);
         o[2] = (int64_t)s.transitions;
         // DFS max depth = longest complete run = protocol transitions + max time
-        // (pinned against explore_machine in tests/test_bfs_gpu.py)
-        int logn = 0, lw = 0, lt = 0, lp = 0;
-        while ((1 << logn) < size) ++logn;
-        while ((1 << lw) < configs[2 * c]) ++lw;
-        while ((1 << lt) < configs[2 * c + 1]) ++lt;
-        while ((1 << lp) < plat[2]) ++lp;
-        const Cost cm = lockstep_cost(kernel, logn, plat[3], Config{plat[0], plat[1], lp, lw, lt});
-        o[3] = s.terminals ? cm.steps - cm.time + s.max_time : -1;
+        // (pinned against explore_machine in tests/test_bfs_gpu.py); under the depth
+        // cap the deepest visited states sit at max_depth
+        o[3] = s.depth_cut ? max_depth : s.terminals ? proto[c] + s.max_time : -1;
         o[4] = s.terminals ? s.min_time : -1;
         o[5] = s.terminals ? s.max_time : -1;
         o[6] = (int64_t)s.terminals;

@@ -18,6 +18,7 @@ struct BfsStats {
     unsigned long long capped;   // the per-configuration state cap was reached
     unsigned long long generic;  // successors built by the generic unpacked apply()
     unsigned long long violations;  // states breaking Machine::check_invariants
+    unsigned long long depth_cut;   // a non-terminal state at the depth cap (explore.cpp:124-127)
 };
 
 struct BfsResult {
@@ -38,17 +39,32 @@ struct BfsResult {
 // n_parts > 1 splits the visited set into hash partitions on this device (the
 // multi-GPU exchange path, exercised on one GPU); sys_scope selects the
 // system-scope memory operations of the multi-GPU kernel.
+// depth_cap > 0 applies ExploreLimits::max_depth (explore.cpp:124-127): a state at
+// depth >= depth_cap is visited but not expanded (depth_cut is set when it has
+// enabled transitions).  The state graphs are graded — every path from the
+// initial state to a state has the same length (tests/test_oracle.py) — so the
+// depth-limited DFS visits exactly the states of depth <= max_depth and the cap
+// is order-independent.  seed_depths gives the depth of each seed (0 when NULL).
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants = false,
             const std::vector<uint32_t>* seeds = nullptr, int n_parts = 1,
-            bool sys_scope = false, uint64_t first_cap = 0);
+            bool sys_scope = false, uint64_t first_cap = 0, uint32_t depth_cap = 0,
+            const std::vector<uint32_t>* seed_depths = nullptr);
+
+// Upper bound on the depth of any state of a configuration (protocol transitions
+// + the largest model time the packing admits): a sweep whose configurations
+// stay below max_depth needs no depth tracking.
+uint64_t depth_bound(const MachDesc& m, int64_t protocol_steps);
 
 // The packed layout the exploration uses for a configuration among n_cfg.
 Layout bfs_layout(const MachDesc& m, int n_cfg);
 
 // The reference DFS's counterexample for bound T (lexfirst.cu).
+// sibling_depths (optional): the depth of each abandoned sibling (its position on
+// the path + 1).
 int lexfirst_path(MachHost& h, int64_t T, int64_t max_len, const Layout& layout,
                   std::vector<int32_t>* path, int64_t* final_time, int64_t* sibling_applies,
-                  std::vector<uint32_t>* siblings, int* n_siblings);
+                  std::vector<uint32_t>* siblings, int* n_siblings,
+                  std::vector<uint32_t>* sibling_depths = nullptr);
 
 }  // namespace mctb

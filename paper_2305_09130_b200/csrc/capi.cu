@@ -21,6 +21,8 @@ int launch_space_eval(const SpaceDev& s, uint64_t first, uint64_t count, int64_t
 int launch_space_point(const SpaceDev& s, const uint64_t* d_key, int64_t* d_out,
                        cudaStream_t stream);
 int launch_fill_key(uint64_t* d_key, cudaStream_t stream);
+int launch_space_exact(const SpaceDev& s, uint64_t first, uint64_t count, uint64_t* d_time,
+                       uint64_t* d_index, cudaStream_t stream);
 
 namespace {
 thread_local std::string g_error;
@@ -66,6 +68,7 @@ int require_device() {
 // Per-device scratch: a few pinned/device words reused by the host-buffer calls.
 struct Scratch {
     uint64_t* d_key = nullptr;
+    uint64_t* d_exact = nullptr;  // {time, index} of the exact resolution
     int64_t* d_out = nullptr;
     uint64_t* h_key = nullptr;
     int64_t* h_out = nullptr;
@@ -81,6 +84,7 @@ int scratch(Scratch** out) {
     Scratch& s = per_dev[dev & 63];
     if (!s.d_key) {
         MCTB_CUDA(cudaMalloc(&s.d_key, sizeof(uint64_t)));
+        MCTB_CUDA(cudaMalloc(&s.d_exact, 2 * sizeof(uint64_t)));
         MCTB_CUDA(cudaMalloc(&s.d_out, 16 * sizeof(int64_t)));
         MCTB_CUDA(cudaMallocHost(&s.h_key, sizeof(uint64_t)));
         MCTB_CUDA(cudaMallocHost(&s.h_out, 16 * sizeof(int64_t)));
@@ -212,11 +216,41 @@ int mctb_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_
     MCTB_CUDA(cudaStreamSynchronize(sc->stream));
     *key = *sc->h_key;
     std::memcpy(out, sc->h_out, 8 * sizeof(int64_t));
+    if (*key != kKeyNone && (*key >> MCTB_KEY_INDEX_BITS) == kKeySat) {
+        // saturated time field: every configuration of the range has time >= 2^30 - 1
+        // (or is infeasible), so the key's index is not the winner — resolve exactly
+        if ((rc = launch_space_exact(s, first, count, sc->d_exact, sc->d_exact + 1, sc->stream)))
+            return rc;
+        uint64_t ex[2];
+        MCTB_CUDA(cudaMemcpyAsync(ex, sc->d_exact, sizeof ex, cudaMemcpyDeviceToHost, sc->stream));
+        MCTB_CUDA(cudaStreamSynchronize(sc->stream));
+        if (ex[0] == UINT64_MAX) {
+            *key = kKeyNone;
+        } else {
+            *key = ((uint64_t)kKeySat << MCTB_KEY_INDEX_BITS) | ex[1];
+            MCTB_CUDA(cudaMemcpyAsync(sc->d_key, key, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                      sc->stream));
+            if ((rc = launch_space_point(s, sc->d_key, sc->d_out, sc->stream))) return rc;
+            MCTB_CUDA(cudaMemcpyAsync(sc->h_out, sc->d_out, 8 * sizeof(int64_t),
+                                      cudaMemcpyDeviceToHost, sc->stream));
+            MCTB_CUDA(cudaStreamSynchronize(sc->stream));
+            std::memcpy(out, sc->h_out, 8 * sizeof(int64_t));
+        }
+    }
     if (*key == kKeyNone || out[0] < 0) {
         set_error("tuning space range holds no configuration");
         return MCTB_CONFIG_ERROR;
     }
     return MCTB_OK;
+}
+
+int mctb_space_exact_async(const int64_t* sd, uint64_t first, uint64_t count, uint64_t* d_time,
+                           uint64_t* d_index, void* stream) {
+    SpaceDev s;
+    int rc = make_space(sd, &s);
+    if (rc) return rc;
+    if ((rc = require_device())) return rc;
+    return launch_space_exact(s, first, count, d_time, d_index, static_cast<cudaStream_t>(stream));
 }
 
 int mctb_space_eval_async(const int64_t* sd, uint64_t first, uint64_t count, int64_t* d_time,

@@ -46,16 +46,20 @@ struct Walk {
     int64_t T = -1;
     std::vector<int32_t> path;
     int64_t final_time = -1, applies = 0, sib_states = 0, sib_transitions = 0;
+    int64_t sib_depth = 0;  // deepest state of the abandoned siblings' subtrees
 };
 
 struct Ctx {
     int plat[4];
     int size = 0, kernel = 0;
     const int64_t* input = nullptr;
-    uint64_t cap = 5000000;  // ExploreLimits::max_states (explore.hpp:38)
+    uint64_t cap = 5000000;  // ExploreLimits::max_states (explore.hpp:39)
+    int64_t max_depth = 4000000;  // ExploreLimits::max_depth (explore.hpp:38)
+    uint32_t depth_cap = 0;  // the sweeps' depth cap: max_depth when a state can reach it
     int skipped = 0;
     std::vector<int> wg, ts;  // feasible configurations, largest-first (explore.cpp:64-72)
     std::vector<int64_t> cm_time, cm_steps;
+    std::vector<int64_t> proto;  // protocol transitions: a terminal of time t is at depth proto + t
     std::vector<MachHost> hs;
     BfsResult bfs;
     std::vector<int64_t> first_time, first_steps;
@@ -72,26 +76,34 @@ int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
     Walk w;
     w.k = k;
     w.T = T;
-    std::vector<uint32_t> sib;
+    std::vector<uint32_t> sib, sib_dep;
     int n_sib = 0;
     const Layout lay = bfs_layout(c.hs[k].d, 1);
     int rc = lexfirst_path(c.hs[k], T, 4 * c.cm_steps[k] + 4096, lay, &w.path, &w.final_time,
-                           &w.applies, &sib, &n_sib);
+                           &w.applies, &sib, &n_sib, &sib_dep);
     if (rc) return rc;
     if (n_sib > 0) {
         std::vector<MachHost> one(1, c.hs[k]);
         BfsResult r;
         cudaStream_t st;
         MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib, 1, false, 1ull << 25);
+        // the siblings' subtrees under the same depth cap as the DFS (each sibling
+        // sits at its position on the path + 1)
+        rc = run_bfs(one, c.cap + 64, c.cap, &r, st, false, &sib, 1, false, 1ull << 25,
+                     c.depth_cap, &sib_dep);
         cudaStreamDestroy(st);
         if (rc) return rc;
         if (r.error) {
             set_error("model bug or capacity limit in the sibling exploration");
             return r.error == 3 ? MCTB_MODEL_BUG : MCTB_LIMIT;
         }
-        w.sib_states = (int64_t)std::min<uint64_t>(r.stats[0].states, c.cap);
-        w.sib_transitions = (int64_t)r.stats[0].transitions;
+        const BfsStats& b = r.stats[0];
+        w.sib_states = (int64_t)std::min<uint64_t>(b.states, c.cap);
+        w.sib_transitions = (int64_t)b.transitions;
+        // every sibling subtree state leads to a terminal: the deepest one is the
+        // latest terminal reached, or the cap
+        w.sib_depth = b.depth_cut ? c.max_depth
+                      : b.terminals ? c.proto[k] + b.max_time : 0;
     }
     c.walks.push_back(std::move(w));
     *out = &c.walks.back();
@@ -112,10 +124,15 @@ double now_ms() {
     return t.tv_sec * 1e3 + t.tv_nsec * 1e-6;
 }
 
-int prepare(Ctx& c, int64_t max_states) {
+int prepare(Ctx& c, int64_t max_states, int64_t max_depth) {
     int rc = check_platform(c.plat);
     if (rc) return rc;
     if ((rc = check_problem(c.size, c.kernel))) return rc;
+    if (max_depth < 1) {  // explore.cpp:91
+        set_error("max_depth must be >= 1");
+        return MCTB_CONFIG_ERROR;
+    }
+    c.max_depth = max_depth;
     if ((rc = require_device())) return rc;
     if (max_states > 0) c.cap = (uint64_t)max_states;
     int64_t sd[13];
@@ -159,11 +176,18 @@ int prepare(Ctx& c, int64_t max_states) {
     }
     const int nc = (int)c.wg.size();
     c.hs.resize(nc);
-    for (int k = 0; k < nc; ++k)
+    c.proto.resize(nc);
+    for (int k = 0; k < nc; ++k) {
         if ((rc = build_desc(c.plat, c.size, c.kernel, c.input, c.wg[k], c.ts[k], &c.hs[k]))) {
             cudaStreamDestroy(st);
             return rc;
         }
+        // explore.cpp:124-127: the sweep tracks depths only when some state of some
+        // configuration could lie deeper than max_depth
+        c.proto[k] = c.cm_steps[k] - c.cm_time[k];
+        if (depth_bound(c.hs[k].d, c.proto[k]) > (uint64_t)max_depth)
+            c.depth_cap = (uint32_t)std::min<int64_t>(max_depth, 0x7fffffff);
+    }
     // every interleaving of every configuration, one sweep.  The first DFS paths
     // (needed only for the configurations a probe finds violating) run lazily.
     const double t1 = now_ms();
@@ -178,7 +202,7 @@ int prepare(Ctx& c, int64_t max_states) {
     uint64_t first_cap = 1ull << 22;
     while (first_cap < 12 * est && first_cap < (1ull << 29)) first_cap <<= 1;
     rc = run_bfs(c.hs, c.cap * (uint64_t)nc + 64ull * nc, c.cap, &c.bfs, st, false, nullptr, 1,
-                 false, first_cap);
+                 false, first_cap, c.depth_cap);
     c.ms_bfs = now_ms() - t1;
     cudaStreamDestroy(st);
     if (rc) return rc;
@@ -194,7 +218,7 @@ int prepare(Ctx& c, int64_t max_states) {
     }
     for (int k = 0; k < nc; ++k) {
         const BfsStats& b = c.bfs.stats[k];
-        const bool complete = !b.capped;
+        const bool complete = !b.capped && !b.depth_cut;
         if (complete && (b.terminals == 0 || b.min_time != c.cm_time[k])) {
             set_error("model bug: explored minimum differs from the lock-step model time");
             return MCTB_MODEL_BUG;
@@ -207,7 +231,7 @@ int prepare(Ctx& c, int64_t max_states) {
 int ensure_first(Ctx& c, int k) {
     if (c.first_time[k] >= 0) return MCTB_OK;
     const BfsStats& b = c.bfs.stats[k];
-    if (!b.capped && b.terminals > 0 && b.min_time == b.max_time) {
+    if (!b.capped && !b.depth_cut && b.terminals > 0 && b.min_time == b.max_time) {
         // every run of this configuration was explored and ends at one time, so
         // every run has the same length (protocol transitions + time): the first
         // path is known without stepping it
@@ -237,13 +261,20 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
     for (int k = 0; k < nc; ++k) {
         const BfsStats& b = c.bfs.stats[k];
         v.explored += 1;
-        const bool complete = !b.capped;
-        const int64_t tmin = complete ? b.min_time : c.cm_time[k];
-        if (tmin <= T) {
+        const bool complete = !b.capped && !b.depth_cut;
+        // the DFS meets only terminals within max_depth, i.e. of time <= max_depth -
+        // protocol transitions (explore.cpp:124-127; every run of a configuration
+        // has protocol + time transitions)
+        const int64_t t_depth = c.max_depth - c.proto[k];
+        const int64_t Tk = std::min(T, t_depth);
+        // the sweep saw every terminal within the depth cap unless the visited cap cut it
+        const int64_t tmin = !b.capped ? b.min_time
+                             : c.cm_time[k] <= t_depth ? c.cm_time[k] : INT64_MAX;
+        if (tmin <= Tk) {
             v.violated = true;
             v.cfg = k;
             if ((*rc_out = ensure_first(c, k))) return v;
-            if (c.first_time[k] <= T) {
+            if (c.first_time[k] <= Tk) {
                 // DFS reaches a satisfying terminal on its first path
                 v.final_time = c.first_time[k];
                 v.steps = c.first_steps[k];
@@ -255,13 +286,14 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
                 // branches; its first satisfying path comes from the guided walk and
                 // its effort from the abandoned siblings' exploration
                 const Walk* w = nullptr;
-                if ((*rc_out = ensure_walk(c, k, T, &w))) return v;
+                if ((*rc_out = ensure_walk(c, k, Tk, &w))) return v;
                 v.path = &w->path;
                 v.final_time = w->final_time;
                 v.steps = (int64_t)(w->path.size() / 4);
                 v.states += 1 + v.steps + w->sib_states;
                 v.transitions += w->applies + w->sib_transitions;
-                v.max_depth = std::max(v.max_depth, v.steps);  // DFS depth of the path
+                // the path and the abandoned siblings' subtrees
+                v.max_depth = std::max(v.max_depth, std::max(v.steps, w->sib_depth));
             }
             v.exhaustive = false;
             return v;
@@ -269,9 +301,10 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
         v.states += (int64_t)std::min<uint64_t>(b.states, c.cap);
         v.transitions += (int64_t)b.transitions;
         if (complete)
-            v.max_depth = std::max<int64_t>(v.max_depth, c.cm_steps[k] - c.cm_time[k] + b.max_time);
+            v.max_depth = std::max<int64_t>(v.max_depth, c.proto[k] + b.max_time);
         else
             limit = true;
+        if (b.depth_cut && !b.capped) v.max_depth = std::max(v.max_depth, c.max_depth);
     }
     v.exhaustive = !limit;
     return v;
@@ -307,8 +340,8 @@ extern "C" {
 // out = {violated, exhaustive, states_visited, max_depth_reached, transitions_applied,
 //        configs_explored, configs_skipped, final_time, wg, ts, steps, trace_exact}
 int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* input, int64_t T,
-                        int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
-                        int64_t* trace_len) {
+                        int64_t max_states, int64_t max_depth, int64_t* out, int32_t* trace,
+                        int64_t cap, int64_t* trace_len) {
     if (T < 0) {
         set_error("over-time bound must be >= 0");
         return MCTB_CONFIG_ERROR;
@@ -318,7 +351,7 @@ int mctb_check_overtime(const int* plat, int size, int kernel, const int64_t* in
     c.size = size;
     c.kernel = kernel;
     c.input = input;
-    int rc = prepare(c, max_states);
+    int rc = prepare(c, max_states, max_depth);
     if (rc) return rc;
     const VerdictOut v = verdict(c, T, &rc);
     if (rc) return rc;
@@ -349,8 +382,8 @@ static void record_probe(int64_t T, const VerdictOut& v, const Ctx& c) {
 //        steps, trace_exact}
 // info = {ms_cost_model, ms_first_paths, ms_bfs, bfs_states, bfs_levels}  (optional)
 int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64_t t_hi,
-              uint64_t seed, int64_t max_states, int64_t* out, int32_t* trace, int64_t cap,
-              int64_t* trace_len, double* info) {
+              uint64_t seed, int64_t max_states, int64_t max_depth, int64_t* out, int32_t* trace,
+              int64_t cap, int64_t* trace_len, double* info) {
     Ctx c;
     std::memcpy(c.plat, plat, sizeof c.plat);
     c.size = size;
@@ -358,7 +391,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     c.input = input;
     const bool tt = getenv("MCTB_TUNE_TRACE") != nullptr;
     const double tp0 = now_ms();
-    int rc = prepare(c, max_states);
+    int rc = prepare(c, max_states, max_depth);
     if (rc) return rc;
     const double tp1 = now_ms();
     if (t_hi <= 0) {
@@ -373,7 +406,7 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
         rng.seed(seed);
         const int k = order[rng.next() % order.size()];
         const BfsStats& b = c.bfs.stats[k];
-        if (!b.capped && b.terminals > 0 && b.min_time == b.max_time) {
+        if (!b.capped && !b.depth_cut && b.terminals > 0 && b.min_time == b.max_time) {
             // the sweep explored every run of this configuration and they all end at
             // one time, so the seeded run ends there too: no serial simulation
             // (a lone GPU thread steps ~2 us per transition; 124 ms at size 128)

@@ -15,6 +15,8 @@
 // grid is a multiple of the 148 SMs and each thread amortises its index decode
 // over thousands of configurations (nd is the fastest digit; per-(wg, ts, np,
 // nu) quantities are hoisted out of the nd loop).
+#include <climits>
+
 #include "common.cuh"
 #include "cost_model.cuh"
 
@@ -215,6 +217,52 @@ __global__ void space_point_kernel(SpaceDev sd, int kernel, const unsigned long 
 
 __global__ void fill_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// ---- exact resolution of a saturated key ("Exactness").
+// The packed key saturates its time field at 2^30 - 1, so when every
+// configuration of the range has time >= 2^30 - 1 the key's index is only the
+// first saturated (or infeasible) index.  These two plain passes are the exact
+// argmin by construction: the least full 64-bit time of the feasible
+// configurations (make_space bounds every time and transition count below
+// 2^62), then the least index with that time (the reference's tie rule,
+// search.cpp:67-78).  Not on the hot path: they run only for saturated keys.
+__device__ __forceinline__ unsigned long long warp_min_ull(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+__global__ void space_min_time_kernel(SpaceDev sd, uint64_t first, uint64_t count,
+                                      unsigned long long* out_time) {
+    unsigned long long best = ULLONG_MAX;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const Cost c = lockstep_cost(sd.kernel, sd.logn, sd.gmt, decode(sd, first + i));
+        if (c.feasible && (unsigned long long)c.time < best) best = (unsigned long long)c.time;
+    }
+    best = warp_min_ull(best);
+    if ((threadIdx.x & 31) == 0 && best != ULLONG_MAX) atomicMin(out_time, best);
+}
+
+__global__ void space_first_at_kernel(SpaceDev sd, uint64_t first, uint64_t count,
+                                      const unsigned long long* time,
+                                      unsigned long long* out_index) {
+    const unsigned long long t = *time;
+    unsigned long long best = ULLONG_MAX;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const Cost c = lockstep_cost(sd.kernel, sd.logn, sd.gmt, decode(sd, first + i));
+        if (c.feasible && (unsigned long long)c.time == t) {
+            best = first + i;  // grid-stride order: a thread's first hit is its least index
+            break;
+        }
+    }
+    best = warp_min_ull(best);
+    if ((threadIdx.x & 31) == 0 && best != ULLONG_MAX) atomicMin(out_index, best);
+}
+
 int sm_count() {
     static int n = 0;
     if (!n) {
@@ -259,6 +307,19 @@ int make_space(const int64_t* sd, SpaceDev* out) {
         sd[12] > logn - 1) {
         set_error("log2 wg and log2 ts ranges must lie in [1, log2(size) - 1]");
         return MCTB_CONFIG_ERROR;
+    }
+    // every model time and transition count of the space must fit int64 (the
+    // reference's Tick, model.hpp): the abstract kernel's largest time is below
+    // (size/2)(size(gmt+1) + gmt) and its transition count below 3 size^2 (gmt+1)
+    // (cost_model.cuh), so 4 size^2 (gmt+1) <= 2^62 bounds both.  The minimum
+    // kernel's are below 16 size (gmt+1) <= 2^55 for every admitted size and gmt.
+    if (kernel == 0) {
+        int lg = 0;
+        while ((1ll << lg) < sd[2] + 1) ++lg;
+        if (2 * logn + lg + 2 > 62) {
+            set_error("size^2 * (gmt + 1) must be below 2^60 (model times fit int64)");
+            return MCTB_CONFIG_ERROR;
+        }
     }
     SpaceDev s;
     s.kernel = (int32_t)kernel;
@@ -337,6 +398,25 @@ int launch_space_point(const SpaceDev& s, const uint64_t* d_key, int64_t* d_out,
                                            reinterpret_cast<const unsigned long long*>(d_key),
                                            d_out);
     return cuda_check(cudaGetLastError(), "space_point_kernel");
+}
+
+int launch_space_exact(const SpaceDev& s, uint64_t first, uint64_t count, uint64_t* d_time,
+                       uint64_t* d_index, cudaStream_t stream) {
+    if (first + count > space_count(s)) {
+        set_error("index range outside the tuning space");
+        return MCTB_CONFIG_ERROR;
+    }
+    auto* t = reinterpret_cast<unsigned long long*>(d_time);
+    auto* x = reinterpret_cast<unsigned long long*>(d_index);
+    fill_u64_kernel<<<1, 1, 0, stream>>>(t, ULLONG_MAX);
+    fill_u64_kernel<<<1, 1, 0, stream>>>(x, ULLONG_MAX);
+    if (count == 0) return cuda_check(cudaGetLastError(), "fill_u64_kernel");
+    const uint64_t want = (count + 255) / 256;
+    const uint64_t cap = (uint64_t)sm_count() * 16;
+    const unsigned blocks = (unsigned)(want < cap ? want : cap);
+    space_min_time_kernel<<<blocks, 256, 0, stream>>>(s, first, count, t);
+    space_first_at_kernel<<<blocks, 256, 0, stream>>>(s, first, count, t, x);
+    return cuda_check(cudaGetLastError(), "space_exact_kernels");
 }
 
 int launch_fill_key(uint64_t* d_key, cudaStream_t stream) {

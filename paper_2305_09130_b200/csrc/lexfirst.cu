@@ -80,7 +80,8 @@ __global__ void walk_pack_kernel(BfsDesc d, const MState* cur, const Transition*
 // `layout`), or MCTB_LIMIT when the walk exceeds max_len transitions.
 int lexfirst_path(MachHost& h, int64_t T, int64_t max_len, const Layout& layout,
                   std::vector<int32_t>* path, int64_t* final_time, int64_t* sibling_applies,
-                  std::vector<uint32_t>* siblings, int* n_siblings) {
+                  std::vector<uint32_t>* siblings, int* n_siblings,
+                  std::vector<uint32_t>* sibling_depths) {
     cudaStream_t st;
     MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     int32_t* d_ids = nullptr;
@@ -111,6 +112,7 @@ int lexfirst_path(MachHost& h, int64_t T, int64_t max_len, const Layout& layout,
     path->clear();
     siblings->clear();
     *n_siblings = 0;
+    if (sibling_depths) sibling_depths->clear();
     *sibling_applies = 0;
     *final_time = -1;
     rc = MCTB_OK;
@@ -152,6 +154,7 @@ int lexfirst_path(MachHost& h, int64_t T, int64_t max_len, const Layout& layout,
             cudaMemcpyAsync(siblings->data() + old, d_pack, (size_t)pick * words * 4,
                             cudaMemcpyDeviceToHost, st);
             *n_siblings += pick;
+            if (sibling_depths) sibling_depths->insert(sibling_depths->end(), pick, (uint32_t)(step + 1));
         }
         *sibling_applies += pick + 1;
         walk_apply_kernel<<<1, 1, 0, st>>>(m, d_cur, d_en, pick, d_n + 1);

@@ -20,12 +20,13 @@ the GPU kernels and over gloo with CPU checkers in tests/test_distributed.py.
 """
 from __future__ import annotations
 
-from typing import Callable, Hashable, Iterable, List, Sequence, Tuple
+from typing import Callable, Hashable, Iterable, List, Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
 
 KEY_INDEX_BITS = 33
+KEY_SAT = (1 << 30) - 1
 
 
 def shard(total: int, rank: int, world: int) -> Tuple[int, int]:
@@ -36,9 +37,16 @@ def shard(total: int, rank: int, world: int) -> Tuple[int, int]:
 
 
 def sharded_space_argmin(total: int, local_argmin: Callable[[int, int], int],
-                         group=None, device: str = "cpu") -> Tuple[int, int, int]:
+                         group=None, device: str = "cpu",
+                         local_exact: Optional[Callable[[int, int], Tuple[int, int]]] = None
+                         ) -> Tuple[int, int, int]:
     """Global (key, time, index) of a space of `total` configurations.
-    local_argmin(first, count) -> packed key of the rank's shard (2^63 = none)."""
+    local_argmin(first, count) -> packed key of the rank's shard (2^63 = none).
+    The key's time field saturates at KEY_SAT; when the reduced key is saturated
+    every configuration has time >= KEY_SAT, and the winner is resolved exactly
+    with local_exact(first, count) -> (least time or -1, least index with it):
+    all-reduce(MIN) of the time, then all-reduce(MIN) of the index among the ranks
+    holding that time (search.cpp:67-78's tie rule across shards)."""
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     first, count = shard(total, rank, world)
@@ -47,7 +55,23 @@ def sharded_space_argmin(total: int, local_argmin: Callable[[int, int], int],
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
     k = int(t.item())
-    return k, k >> KEY_INDEX_BITS, k & ((1 << KEY_INDEX_BITS) - 1)
+    if k >= (1 << 63) - 1 or (k >> KEY_INDEX_BITS) < KEY_SAT:
+        return k, k >> KEY_INDEX_BITS, k & ((1 << KEY_INDEX_BITS) - 1)
+    if local_exact is None:
+        raise ValueError("saturated argmin key: pass local_exact to resolve it")
+    none = (1 << 63) - 1
+    et, ei = local_exact(first, count) if count else (-1, none)
+    v = torch.tensor([et if et >= 0 else none], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(v, op=dist.ReduceOp.MIN, group=group)
+    tmin = int(v.item())
+    if tmin == none:
+        return none, -1, none
+    w = torch.tensor([ei if et == tmin else none], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(w, op=dist.ReduceOp.MIN, group=group)
+    idx = int(w.item())
+    return (KEY_SAT << KEY_INDEX_BITS) | idx, tmin, idx
 
 
 def owner(fingerprint: int, world: int) -> int:

@@ -40,7 +40,8 @@ class SweepInfo:
 def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
                     configs: Sequence[TuningParams], max_states: int = 5_000_000,
                     info: list | None = None, check_invariants: bool = False,
-                    partitions: int = 1, system_scope: bool = False) -> List[ExploreStats]:
+                    partitions: int = 1, system_scope: bool = False,
+                    max_depth: int = 4_000_000) -> List[ExploreStats]:
     """partitions > 1 splits the visited set into hash partitions on this device:
     the successor exchange of the multi-GPU sweep, run on one GPU (same kernel,
     same results); system_scope selects the multi-GPU kernel variant."""
@@ -51,7 +52,7 @@ def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
     out = (C.c_int64 * (9 * len(configs)))()
     inf = (C.c_int64 * 4)()
     check(lib.mctb_explore(platform.as_array(), problem.size, problem.kernel,
-                           problem.input_array(), cfg, len(configs), max_states,
+                           problem.input_array(), cfg, len(configs), max_states, max_depth,
                            (1 if check_invariants else 0) | (2 if system_scope else 0)
                            | (partitions << 8 if partitions > 1 else 0), out, inf))
     if info is not None:
@@ -60,9 +61,10 @@ def explore_configs(platform: PlatformConfig, problem: ProblemSpec,
 
 
 def explore_machine(platform: PlatformConfig, problem: ProblemSpec, params: TuningParams,
-                    max_states: int = 5_000_000) -> ExploreStats:
-    """Every interleaving of one machine (explore.hpp:81-86)."""
-    return explore_configs(platform, problem, [params], max_states)[0]
+                    max_states: int = 5_000_000, max_depth: int = 4_000_000) -> ExploreStats:
+    """Every interleaving of one machine (explore.hpp:81-86) within ExploreLimits'
+    max_states / max_depth (explore.cpp:124-135)."""
+    return explore_configs(platform, problem, [params], max_states, max_depth=max_depth)[0]
 
 
 def check_nontermination(platform: PlatformConfig, problem: ProblemSpec, max_depth: int = 4_000_000,

@@ -128,14 +128,16 @@ def _trace_from(buf, n, final_time, wg, ts):
 
 
 def check_overtime(platform: PlatformConfig, problem: ProblemSpec, T: int,
-                   max_states: int = 5_000_000) -> Verdict:
+                   max_states: int = 5_000_000, max_depth: int = 4_000_000) -> Verdict:
     """Exhaustive check of "every terminating run takes more than T ticks" over all
-    configurations and interleavings (explore.hpp:88-93)."""
+    configurations and interleavings (explore.hpp:88-93), within ExploreLimits'
+    max_states and max_depth (explore.cpp:124-135)."""
     out = (C.c_int64 * 12)()
     buf = _trace_buffer()
     n = C.c_int64()
     check(lib.mctb_check_overtime(platform.as_array(), problem.size, problem.kernel,
-                                  problem.input_array(), T, max_states, out, buf, _TRACE_CAP,
+                                  problem.input_array(), T, max_states, max_depth, out, buf,
+                                  _TRACE_CAP,
                                   C.byref(n)))
     st = ExploreStatsSummary(out[2], out[4], out[3], out[5], out[6])
     trace = _trace_from(buf, n.value, out[7], out[8], out[9]) if out[0] else None
@@ -143,7 +145,7 @@ def check_overtime(platform: PlatformConfig, problem: ProblemSpec, T: int,
 
 
 def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: int = 0,
-         max_states: int = 5_000_000) -> TuneResult:
+         max_states: int = 5_000_000, max_depth: int = 4_000_000) -> TuneResult:
     """The `tune` command flow: estimate_initial_time(seed) then bisect_min_time
     (tools/main.cpp:119-128)."""
     import time as _time
@@ -153,7 +155,8 @@ def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: in
     n = C.c_int64()
     info = (C.c_double * 5)()
     check(lib.mctb_tune(platform.as_array(), problem.size, problem.kernel, problem.input_array(),
-                        t_hi, C.c_uint64(seed), max_states, out, buf, _TRACE_CAP, C.byref(n),
+                        t_hi, C.c_uint64(seed), max_states, max_depth, out, buf, _TRACE_CAP,
+                        C.byref(n),
                         info))
     wall = _time.perf_counter() - t0
     trace = _trace_from(buf, n.value, out[0], out[1], out[2])
@@ -171,12 +174,12 @@ def tune(platform: PlatformConfig, problem: ProblemSpec, seed: int = 1, t_hi: in
 
 
 def bisect_min_time(platform: PlatformConfig, problem: ProblemSpec, t_hi: int,
-                    max_states: int = 5_000_000) -> TuneResult:
+                    max_states: int = 5_000_000, max_depth: int = 4_000_000) -> TuneResult:
     """Counterexample-guided binary search for the minimal time (search.hpp:58-63)."""
     if t_hi < 1:
         from ._lib import ConfigError
         raise ConfigError("t_hi must be >= 1")
-    return tune(platform, problem, 0, t_hi, max_states)
+    return tune(platform, problem, 0, t_hi, max_states, max_depth)
 
 
 def extract_params(platform: PlatformConfig, problem: ProblemSpec, trace: Trace):

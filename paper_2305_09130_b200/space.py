@@ -79,7 +79,9 @@ class SpaceResult:
 
 
 def space_argmin(space: Space, first: int = 0, count: Optional[int] = None) -> SpaceResult:
-    """Minimal-time configuration of [first, first+count) (host buffers in, host result out)."""
+    """Minimal-time configuration of [first, first+count) (host buffers in, host result out).
+    Exact for every space: when the packed key's time field saturates, the C ABI
+    resolves the winner with the exact two-pass evaluation (include/mctune_b200.h)."""
     if count is None:
         count = space.count - first
     key = C.c_uint64()
@@ -94,6 +96,17 @@ def space_argmin_async(space: Space, first: int, count: int, d_key_ptr: int, str
     """Device-resident argmin into a uint64 device word (no sync, no allocation)."""
     check(lib.mctb_space_argmin_async(desc if desc is not None else space.desc(), first, count,
                                       C.c_void_p(d_key_ptr), C.c_void_p(stream)))
+
+
+def space_exact_async(space: Space, first: int, count: int, d_time_ptr: int, d_index_ptr: int,
+                      stream: int = 0, desc=None) -> None:
+    """Exact argmin of [first, first+count) without the packed key (two plain passes):
+    uint64 device words *time = least model time of the feasible configurations
+    (2^64-1: none), *index = least index with that time.  Resolves a key whose time
+    field saturated (key >> KEY_INDEX_BITS == KEY_SAT)."""
+    check(lib.mctb_space_exact_async(desc if desc is not None else space.desc(), first, count,
+                                     C.c_void_p(d_time_ptr), C.c_void_p(d_index_ptr),
+                                     C.c_void_p(stream)))
 
 
 def space_eval_async(space: Space, first: int, count: int, d_time_ptr: int, d_steps_ptr: int,

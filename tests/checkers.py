@@ -150,6 +150,23 @@ class Oracle(_Base):
                                                wg, ts, t, C.c_int64(n), out))
         return list(out)
 
+    def successors(self, plat, size, kernel, wg, ts, ser=None, cap=256):
+        """[(fingerprint, serialized state)] of the initial state (ser None) or of a
+        serialized state's successors, in the reference's enabled() order."""
+        self.lib.mo_successors.restype = C.c_int64
+        rec = C.c_int64()
+        if getattr(self, "_succ_cap", 0) < cap:
+            self._succ_buf = C.create_string_buffer(cap * 4096)
+            self._succ_fps = (C.c_uint64 * cap)()
+            self._succ_cap = cap
+        buf, fps = self._succ_buf, self._succ_fps
+        n = self.lib.mo_successors(_plat(plat), size, kernel, None, wg, ts, ser, buf, cap, fps,
+                                   C.byref(rec))
+        if n < 0:
+            raise CheckerError(int(n), self.err().decode(errors="replace"))
+        L = rec.value
+        return [(fps[i], bytes(buf.raw[i * L:(i + 1) * L])) for i in range(n)]
+
     def space_argmin(self, sd, first, count):
         key, idx = C.c_uint64(), C.c_uint64()
         t = C.c_int64()

@@ -57,6 +57,20 @@ def test_state_limit_is_reported(engine):
     assert not r.complete
 
 
+def test_state_limit_bounds_the_sweep(engine):
+    """max_states much smaller than the reachable space (1.37e8 states): the sweep
+    stops near the cap in its first table (no 16x restart), reports the
+    reference's capped count (explore.cpp:28) and is not complete."""
+    m = engine
+    info = []
+    r = m.explore_configs(m.PlatformConfig(1, 1, 16, 4), m.ProblemSpec.abstract(64),
+                          [m.TuningParams(16, 2)], max_states=100_000, info=info)[0]
+    assert not r.complete
+    assert r.states_visited == 100_000
+    assert info[0].table_slots == 1 << 20  # the first table: 4 x max_states, no restart
+    assert info[0].states < 1_000_000      # inserted past the cap: bounded by the flush
+
+
 def test_acceptance_7_interleaving_invariants(engine):
     """Every reachable state of every size-8 configuration (both kernels) keeps
     Machine::check_invariants and tick gating; no deadlock; the final time is

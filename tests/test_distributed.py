@@ -53,6 +53,16 @@ def _worker(rank, world, port, q):
     def local(first, count):
         return o.space_argmin(sd, first, count)[0]
     key, t, idx = D.sharded_space_argmin(total, local)
+    # 1b) a space whose every time saturates the key: the exact resolution across ranks
+    sd2 = [0, 1 << 24, 100, 1, 3, 1, 2, 0, 2, 1, 23, 1, 23]
+
+    def local2(first, count, sd2=sd2):
+        return o.space_argmin(sd2, first, count)[0]
+
+    def exact2(first, count, sd2=sd2):
+        r = o.space_argmin(sd2, first, count)
+        return r[1], r[2]
+    sat = D.sharded_space_argmin(3 * 2 * 3 * 23 * 23, local2, local_exact=exact2)
     # 2) hash-partitioned exploration of real model state spaces (reference fingerprints)
     counts = []
     for plat, size, kernel, wg, ts in CASES:
@@ -69,7 +79,7 @@ def _worker(rank, world, port, q):
 
         mine, tot = D.partitioned_explore(init, expand, encode, decode, (L + 3) // 4)
         counts.append((mine, tot))
-    q.put((rank, key, t, idx, counts))
+    q.put((rank, key, t, idx, counts, sat))
     dist.destroy_process_group()
 
 
@@ -84,10 +94,12 @@ def test_two_rank_argmin_and_partitioned_exploration(oracle):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (_, k0, t0, i0, c0), (_, k1, t1, i1, c1) = res
+    (_, k0, t0, i0, c0, s0), (_, k1, t1, i1, c1, s1) = res
     sd = [0, 1 << 12, 3, 1, 40, 1, 9, 0, 4, 1, 11, 1, 11]
     key, t, idx = oracle.space_argmin(sd, 0, 40 * 9 * 5 * 11 * 11)
     assert (k0, t0, i0) == (k1, t1, i1) == (key, t, idx)
+    # saturated key resolved exactly across the two shards (index 8706 lies in rank 1's)
+    assert s0 == s1 == (((1 << 30) - 1) << 33 | 8706, 1694498916, 8706)
     # reference state counts of these configurations (tests/golden/explore.json / oracle)
     want = [oracle.explore(p, s, k, wg, ts)["states"] for p, s, k, wg, ts in CASES]
     for (m0, tot0), (m1, tot1), w in zip(c0, c1, want):

@@ -107,3 +107,57 @@ def test_oracle_against_reference_directly(oracle, ref):
         a = ref.simulate(plat, size, kernel, wg, ts, 1, seed, inp, trace=True)
         b = oracle.simulate(plat, size, kernel, wg, ts, 1, seed, inp, trace=True)
         assert a == b
+
+
+GRADED = [((1, 1, 4, 4), 8, 0, 4, 4), ((2, 1, 2, 4), 8, 0, 2, 2), ((1, 1, 4, 4), 8, 1, 4, 2),
+          ((3, 1, 1, 1), 16, 0, 2, 2), ((2, 1, 4, 2), 16, 1, 2, 2), ((3, 1, 1, 4), 16, 1, 2, 2),
+          ((2, 2, 2, 2), 16, 0, 2, 4)]
+
+
+@pytest.mark.parametrize("case", GRADED)
+def test_state_graphs_are_graded(oracle, case):
+    """Every path from the initial state to a state has the same length (each
+    transition advances one process's fixed amount of protocol, and every run of
+    a configuration has protocol + time transitions).  The GPU's depth cap relies
+    on it: the depth-limited DFS (explore.cpp:124-127) then visits exactly the
+    states of depth <= max_depth, whatever its order."""
+    plat, size, kernel, wg, ts = case
+    init = oracle.successors(plat, size, kernel, wg, ts)
+    depth = {s: 0 for _, s in init}
+    frontier = [s for _, s in init]
+    d = 0
+    while frontier:
+        nxt = []
+        for s in frontier:
+            for _, t in oracle.successors(plat, size, kernel, wg, ts, s):
+                if t in depth:
+                    assert depth[t] == d + 1, (case, d)
+                else:
+                    depth[t] = d + 1
+                    nxt.append(t)
+        frontier = nxt
+        d += 1
+    # the deepest state is the end of the longest run: protocol transitions + max time
+    t, steps, _ = oracle.cost_model(plat, size, kernel, wg, ts)
+    r = oracle.explore(plat, size, kernel, wg, ts)
+    assert d - 1 == r["max_depth"] == steps - t + r["max_time"]
+
+
+def test_depth_cap_against_reference(oracle, gold):
+    """The oracle's depth-limited DFS against the reference's (tests/golden/depth.json)."""
+    g = gold("depth.json")
+    for c in g["explores"]:
+        r = oracle.explore(c["plat"], c["size"], c["kernel"], c["wg"], c["ts"],
+                           max_depth=c["depth_cap"])
+        for k in ("complete", "states", "transitions", "max_depth", "min_time", "max_time",
+                  "n_terminal"):
+            assert r[k] == c[k], (k, c)
+    for c in g["checks"]:
+        if c["plat"] == [2, 1, 2, 4] and not c["violated"]:
+            continue  # 4e5-state sweeps: the GPU tests cover them
+        r = oracle.check_overtime(c["plat"], c["size"], c["kernel"], c["T"],
+                                  max_depth=c["depth_cap"])
+        for k in ("violated", "exhaustive", "states", "max_depth", "transitions",
+                  "configs_explored", "configs_skipped", "final_time", "wg", "ts", "steps"):
+            assert r[k] == c[k], (k, c["plat"], c["size"], c["T"], c["depth_cap"])
+        assert sha(r["trace"]) == c["trace_sha"]

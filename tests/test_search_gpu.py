@@ -136,6 +136,8 @@ def test_schedule_dependent_counterexamples(engine, gold):
         assert sha(v.trace.transitions) == c["trace_sha"], key
         assert (v.stats.states_visited, v.stats.transitions_applied) == (
             c["states"], c["transitions"]), key
+        # the deepest state the DFS met: the path or the abandoned siblings' subtrees
+        assert v.stats.max_depth_reached == c["max_depth"], key
     for c in g["tunes"]:
         _tune_matches(m, c)
 
@@ -160,3 +162,49 @@ def test_tune_probes_are_the_per_bound_checks(engine, gold):
             if v.violated:
                 assert (p.wg, p.ts, p.final_time, p.steps) == (
                     v.trace.params.wg, v.trace.params.ts, v.trace.final_time, v.trace.steps)
+
+
+def test_depth_cap_matches_reference(engine, gold):
+    """ExploreLimits::max_depth (explore.cpp:124-127) against the reference: the
+    DFS applies no transition past the cap, so some configurations' runs are cut
+    (limit_hit, not exhaustive) and their terminals are unreachable — explore,
+    check_overtime (single-device and schedule-dependent spaces, violated and
+    not) and tune, whose optimum moves when the cap hides the best runs."""
+    m = engine
+    g = gold("depth.json")
+    for c in g["explores"]:
+        r = m.explore_machine(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]),
+                              m.TuningParams(c["wg"], c["ts"]), max_depth=c["depth_cap"])
+        key = (c["plat"], c["size"], c["wg"], c["ts"], c["depth_cap"])
+        assert (r.complete, r.states_visited, r.transitions_applied, r.max_depth_reached) == (
+            bool(c["complete"]), c["states"], c["transitions"], c["max_depth"]), key
+        assert (r.terminals, r.min_time, r.max_time) == (c["n_terminal"], c["min_time"],
+                                                         c["max_time"]), key
+    for c in g["checks"]:
+        plat, prob = m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"])
+        key = (c["plat"], c["size"], c["kernel"], c["T"], c["depth_cap"])
+        v = m.check_overtime(plat, prob, c["T"], max_depth=c["depth_cap"])
+        assert (v.violated, v.exhaustive) == (bool(c["violated"]), bool(c["exhaustive"])), key
+        assert (v.stats.states_visited, v.stats.transitions_applied, v.stats.max_depth_reached) == (
+            c["states"], c["transitions"], c["max_depth"]), key
+        assert (v.stats.configs_explored, v.stats.configs_skipped) == (
+            c["configs_explored"], c["configs_skipped"]), key
+        if v.violated:
+            assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
+                c["final_time"], c["wg"], c["ts"], c["steps"]), key
+            assert sha(v.trace.transitions) == c["trace_sha"], key
+    for c in g["tunes"]:
+        plat, prob = m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"])
+        if "error" in c:
+            with pytest.raises(m.ConfigError):
+                m.tune(plat, prob, seed=c["seed"], max_depth=c["depth_cap"])
+            continue
+        r = m.tune(plat, prob, seed=c["seed"], max_depth=c["depth_cap"])
+        key = (c["plat"], c["size"], c["kernel"], c["depth_cap"])
+        assert (r.t_min, r.params.wg, r.params.ts, r.t_ini, r.proven) == (
+            c["t_min"], c["wg"], c["ts"], c["t_ini"], bool(c["proven"])), key
+        assert (r.stats.checks_run, r.stats.states_visited_total, r.first_trail_time) == (
+            c["checks_run"], c["states_visited_total"], c["first_trail_time"]), key
+        assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
+    with pytest.raises(m.ConfigError):
+        m.check_overtime(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8), 44, max_depth=0)

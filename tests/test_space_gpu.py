@@ -43,8 +43,12 @@ def test_generalised_space_argmin_matches_oracle(engine, oracle, seed):
     n = min(count - first, 400000)
     r = m.space_argmin(sp, first, n)
     key, t, idx = oracle.space_argmin(list(sp.desc()), first, n)
-    assert r.key == key
-    assert r.index == idx
+    # the oracle's (t, idx) is the exact least (time, index); its key is the packed one
+    assert r.index == idx and r.time == t
+    if (key >> m.KEY_INDEX_BITS) < m.KEY_SAT:
+        assert r.key == key
+    else:
+        assert r.key == (m.KEY_SAT << m.KEY_INDEX_BITS) | idx
     plat, params = sp.decode(idx)
     t2, steps, ok = oracle.cost_model((plat.nd, plat.nu, plat.np, plat.gmt), sp.size, kernel,
                                       params.wg, params.ts)
@@ -100,3 +104,69 @@ def test_argmin_windows_match_oracle(engine, oracle, space_id):
         space_argmin_async(sp, first, count, d_key.data_ptr(), stream)
         key, t, idx = oracle.space_argmin(list(sp.desc()), first, count)
         assert int(d_key.item()) == key, (space_id, first, count)
+
+
+def _brute_force(sp, first, count):
+    """Exact argmin from the per-configuration time table (no packed key): the least
+    time of the feasible configurations, then the least index with that time."""
+    import torch
+    from paper_2305_09130_b200.space import space_eval_async
+    t = torch.empty(count, dtype=torch.int64, device="cuda")
+    s = torch.empty(count, dtype=torch.int64, device="cuda")
+    space_eval_async(sp, first, count, t.data_ptr(), s.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream)
+    t = torch.where(t < 0, torch.full_like(t, (1 << 63) - 1), t)
+    tmin = int(t.min().item())
+    idx = int(torch.nonzero(t == tmin)[0].item())
+    return tmin, first + idx, int(s[idx].item())
+
+
+SATURATING = [
+    # the round-1 counterexample: every time >= 2^30 - 1, winner index 8706
+    ((0, 1 << 24, 100, (1, 3), (1, 2), (0, 2)), 0, None, (1694498916, 8706)),
+    # minimum kernel, every feasible time saturated, infeasible indices first
+    ((1, 1 << 26, 1 << 14, (1, 2), (1, 2), (0, 1), (13, 25), (12, 25)), 0, None, None),
+    # mixed: saturated and unsaturated configurations, windows in both regions
+    ((0, 1 << 20, 1000, (1, 4000), (1, 3), (0, 2), (1, 19), (1, 19)), 0, 3_000_000, None),
+    ((0, 1 << 20, 1000, (1, 4000), (1, 3), (0, 2), (1, 19), (1, 19)), 17, 500_000, None),
+    ((1, 1 << 22, 3, (1, 200), (1, 7), (0, 5), (1, 21), (1, 21)), 0, None, None),
+]
+
+
+@pytest.mark.parametrize("case", range(len(SATURATING)))
+def test_space_argmin_exact_against_brute_force(engine, oracle, case):
+    """mctb_space_argmin against a brute-force exact-time argmin (not the packed key),
+    including spaces whose least time saturates the key's 30-bit time field."""
+    m = engine
+    args, first, count, want = SATURATING[case]
+    sp = m.Space(*args)
+    if count is None:
+        count = sp.count - first
+    t, idx, steps = _brute_force(sp, first, count)
+    r = m.space_argmin(sp, first, count)
+    assert (r.time, r.index, r.steps) == (t, idx, steps)
+    plat, params = sp.decode(idx)
+    assert (r.platform, r.params) == (plat, params)
+    if want is not None:
+        assert (r.time, r.index) == want
+    if count <= 400_000:
+        _, ot, oi = oracle.space_argmin(list(sp.desc()), first, count)
+        assert (ot, oi) == (t, idx)
+
+
+def test_space_exact_async_matches_brute_force(engine):
+    import torch
+    from paper_2305_09130_b200.space import space_exact_async
+    m = engine
+    sp = m.Space(0, 1 << 24, 100, (1, 3), (1, 2), (0, 2))
+    d = torch.empty(2, dtype=torch.int64, device="cuda")
+    space_exact_async(sp, 0, sp.count, d.data_ptr(), d.data_ptr() + 8,
+                      torch.cuda.current_stream().cuda_stream)
+    assert d.tolist() == [1694498916, 8706]
+    # a range with no feasible configuration: time = 2^64 - 1 (int64 -1)
+    sp2 = m.Space(1, 1 << 8, 2, (1, 1), (1, 1), (0, 0), (7, 7), (7, 7))
+    space_exact_async(sp2, 0, 1, d.data_ptr(), d.data_ptr() + 8,
+                      torch.cuda.current_stream().cuda_stream)
+    assert d.tolist() == [-1, -1]
+    with pytest.raises(m.ConfigError):
+        m.space_argmin(sp2)
