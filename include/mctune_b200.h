@@ -95,9 +95,13 @@ int mctb_space_exact_async(const int64_t* sd, uint64_t first, uint64_t count, ui
 int mctb_space_eval_async(const int64_t* sd, uint64_t first, uint64_t count, int64_t* d_time,
                           int64_t* d_steps, void* stream);
 
-/* Measured INT32 issue rate of the current device (integer ops/s over the chip;
- * IMAD + IADD3 chains) — the roofline denominator of the cost-model kernel. */
+/* Measured integer issue rate of the current device (thread operations/s over the
+ * chip, the best of mctb_issue_probe's integer variants 0-2) — the roofline
+ * denominator of the cost-model kernel. */
 int mctb_int32_peak(double* ops_per_sec, double* ms);
+/* One issue-rate probe (8 independent chains per thread, 64 warps per SM):
+ * 0 IMAD + LOP3, 1 IADD3, 2 IADD3 + LOP3 + IMAD + SHF, 3 FFMA (fp32 issue). */
+int mctb_issue_probe(int variant, double* ops_per_sec, double* ms);
 
 /* ---------------------------------------------------------------------------
  * Reference-compatible drivers (host buffers).

@@ -67,6 +67,7 @@ lib.mctb_space_argmin.argtypes = [i64p, C.c_uint64, C.c_uint64, u64p, i64p]
 lib.mctb_space_eval_async.argtypes = [i64p, C.c_uint64, C.c_uint64, vp, vp, vp]
 lib.mctb_space_exact_async.argtypes = [i64p, C.c_uint64, C.c_uint64, vp, vp, vp]
 lib.mctb_int32_peak.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
+lib.mctb_issue_probe.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 lib.mctb_sweep.argtypes = [i32p, C.c_int, C.c_int, i64p, i64p, C.c_int64, i64p]
 lib.mctb_simulate.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_int,
                               C.c_uint64, C.c_uint64, i64p, i32p, C.c_int64, i64p]
@@ -83,7 +84,7 @@ lib.mctb_trace_text.restype = C.c_int64
 EXPORTED = [
     "mctb_last_error", "mctb_version", "mctb_device_count", "mctb_derive_launch",
     "mctb_space_count", "mctb_space_argmin_async", "mctb_space_argmin",
-    "mctb_space_eval_async", "mctb_space_exact_async", "mctb_sweep", "mctb_int32_peak", "mctb_simulate",
+    "mctb_space_eval_async", "mctb_space_exact_async", "mctb_sweep", "mctb_int32_peak", "mctb_issue_probe", "mctb_simulate",
     "mctb_trajectories", "mctb_trajectories_kernel_ms", "mctb_replay", "mctb_trace_text",
 ]
 

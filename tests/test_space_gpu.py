@@ -76,7 +76,7 @@ def test_eval_table_matches_oracle(engine, oracle):
             assert t[i] == -1
 
 
-@pytest.mark.parametrize("space_id", range(3))
+@pytest.mark.parametrize("space_id", range(5))
 def test_argmin_windows_match_oracle(engine, oracle, space_id):
     """Many short windows [first, first+count) of large spaces, each against the
     oracle's argmin: every window exercises one thread's run logic (the exact
@@ -84,7 +84,9 @@ def test_argmin_windows_match_oracle(engine, oracle, space_id):
     index tie-break) instead of only the global winner."""
     m = engine
     spaces = [
-        m.Space(0, 1 << 10, 4, (1, 160000), (1, 64), (0, 9), (1, 9), (1, 9)),  # bench space
+        m.Space(1, 1 << 14, 4, (1, 166830), (1, 2048), (0, 5), (1, 2), (1, 2)),  # bench space
+        m.Space(1, 1 << 24, 4, (1, 2670000), (1, 128), (0, 5), (4, 5), (1, 2)),  # rich space
+        m.Space(0, 1 << 10, 4, (1, 160000), (1, 64), (0, 9), (1, 9), (1, 9)),  # round-1 bench
         m.Space(1, 1 << 20, 7, (1, 5000), (1, 13), (0, 4), (1, 19), (1, 19)),  # saturating
         m.Space(0, 1 << 6, 2, (3, 700), (2, 9), (0, 3)),
     ]
