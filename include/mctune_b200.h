@@ -184,6 +184,19 @@ int mctb_explore_mp_seed(void* ctx);
 int mctb_explore_mp_run(void* ctx, int64_t* out, int64_t* info);
 void mctb_explore_mp_close(void* ctx);
 
+/* check_nontermination's traces for ONE configuration (explore.hpp:95-100,
+ * explore.cpp:207-233): one trace per distinct terminal state, in the order the
+ * reference's DFS meets them, each the path that DFS followed to it (lexrank.cu:
+ * level-synchronous ranking of least paths).  rows = int64[2 * rows_cap]
+ * {final_time, steps}; trace = the traces' transitions concatenated (int32[4 *
+ * trace_cap]); *n_traces / *trace_len get the full sizes (MCTB_LIMIT when a
+ * buffer is too small, or when the exploration exceeds max_states: the
+ * reference's visited set then truncates in traversal order). */
+int mctb_nonterm_traces(const int* plat, int size, int kernel, const int64_t* input, int wg,
+                        int ts, int64_t max_depth, int64_t max_states, int64_t* n_traces,
+                        int64_t* rows, int64_t rows_cap, int32_t* trace, int64_t trace_cap,
+                        int64_t* trace_len);
+
 /* check_overtime (explore.hpp:88-93), exact mode, within ExploreLimits' max_states and
  * max_depth (>= 1; the DFS meets no state deeper than max_depth, explore.cpp:124-127).
  * out = int64[12]: {violated, exhaustive, states_visited, max_depth_reached,

@@ -494,13 +494,37 @@ inline std::vector<Trace> check_nontermination(const PlatformConfig& platform,
             const ExploreResult& r = res[k];
             stats.absorb(r.stats);
             if (r.deadlocks) throw ModelBug("deadlock reached during exploration");
+            if (r.stats.states_visited >= limits.max_states)
+                throw LimitError("check_nontermination: the visited set fills up, where "
+                                 "the reference's DFS truncates in traversal order");
             if (r.terminal_states == 0) continue;
-            if (r.terminal_states > 1)
-                throw LimitError("check_nontermination: configuration (" +
-                                 std::to_string(configs[k].wg) + ", " +
-                                 std::to_string(configs[k].ts) + ") has " +
-                                 std::to_string(r.terminal_states) +
-                                 " terminal states; only single-terminal spaces are served");
+            if (r.terminal_states > 1 || !r.complete) {
+                // every terminal state with its DFS path, in DFS order (lexrank.cu)
+                const detail::Args a(platform, problem);
+                std::int64_t n = 0, len = 0;
+                std::vector<std::int64_t> rows(2 * static_cast<std::size_t>(r.terminal_states));
+                std::vector<std::int32_t> buf(4 * static_cast<std::size_t>(r.terminal_states) *
+                                              static_cast<std::size_t>(r.stats.max_depth_reached + 1));
+                detail::check(mctb_nonterm_traces(
+                    a.plat, a.size, a.kernel, a.input, configs[k].wg, configs[k].ts,
+                    limits.max_depth, std::min(limits.max_states, r.stats.states_visited + 1), &n,
+                    rows.data(), static_cast<std::int64_t>(rows.size() / 2), buf.data(),
+                    static_cast<std::int64_t>(buf.size() / 4), &len));
+                std::size_t pos = 0;
+                for (std::int64_t i = 0; i < n; ++i) {
+                    Trace t;
+                    t.final_time = rows[2 * i];
+                    t.steps = rows[2 * i + 1];
+                    t.params = configs[k];
+                    for (std::int64_t s = 0; s < t.steps; ++s, ++pos)
+                        t.transitions.push_back(Transition{
+                            static_cast<std::uint16_t>(buf[4 * pos]),
+                            static_cast<std::uint16_t>(buf[4 * pos + 1]),
+                            static_cast<Op>(buf[4 * pos + 2]), buf[4 * pos + 3]});
+                    traces.push_back(std::move(t));
+                }
+                continue;
+            }
             std::vector<Transition> tr;
             const RunOutcome o =
                 run(platform, problem, configs[k], SchedPolicy::FirstEnabled, 0, &tr);

@@ -131,3 +131,6 @@ EXPORTED += ["mctb_explore_mp_open", "mctb_explore_mp_connect", "mctb_explore_mp
 lib.mctb_tune_probes.argtypes = [i64p, C.c_int64]
 lib.mctb_tune_probes.restype = C.c_int64
 EXPORTED.append("mctb_tune_probes")
+lib.mctb_nonterm_traces.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_int64,
+                                    C.c_int64, i64p, i64p, C.c_int64, i32p, C.c_int64, i64p]
+EXPORTED.append("mctb_nonterm_traces")

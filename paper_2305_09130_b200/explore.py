@@ -67,13 +67,44 @@ def explore_machine(platform: PlatformConfig, problem: ProblemSpec, params: Tuni
     return explore_configs(platform, problem, [params], max_states, max_depth=max_depth)[0]
 
 
+def nonterm_traces(platform: PlatformConfig, problem: ProblemSpec, params: TuningParams,
+                   max_depth: int = 4_000_000, max_states: int = 5_000_000,
+                   n_hint: int = 0, len_hint: int = 0):
+    """Every distinct terminal state of one configuration in the reference DFS's order,
+    each with the path that DFS follows to it (mctb_nonterm_traces, lexrank.cu).
+    Returns [(final_time, transitions)]."""
+    from ._lib import LimitError
+    rows_cap, trace_cap = max(n_hint, 16), max(len_hint, 4096)
+    for _ in range(2):
+        rows = (C.c_int64 * (2 * rows_cap))()
+        buf = (C.c_int32 * (4 * trace_cap))()
+        n, tl = C.c_int64(), C.c_int64()
+        rc = lib.mctb_nonterm_traces(platform.as_array(), problem.size, problem.kernel,
+                                     problem.input_array(), params.wg, params.ts, max_depth,
+                                     max_states, C.byref(n), rows, rows_cap, buf, trace_cap,
+                                     C.byref(tl))
+        if rc == 4 and (n.value > rows_cap or tl.value > trace_cap):
+            rows_cap, trace_cap = max(rows_cap, n.value), max(trace_cap, tl.value)
+            continue
+        check(rc)
+        out, pos = [], 0
+        for i in range(n.value):
+            t, steps = rows[2 * i], rows[2 * i + 1]
+            out.append((t, [tuple(buf[4 * k:4 * k + 4]) for k in range(pos, pos + steps)]))
+            pos += steps
+        return out
+    raise LimitError("check_nontermination: trace buffers")
+
+
 def check_nontermination(platform: PlatformConfig, problem: ProblemSpec, max_depth: int = 4_000_000,
                          max_states: int = 5_000_000):
     """Terminating traces, one per distinct terminal state, for every feasible
     configuration largest-first (explore.hpp:95-100, explore.cpp:207-233).  One GPU
-    sweep; a single-terminal configuration contributes the FIRST-policy run (where
-    the reference's DFS first meets its terminal state); several terminal states
-    raise LimitError.  Returns (traces, stats of the sweep per configuration)."""
+    sweep gives the statistics and each configuration's terminal count; a
+    configuration with one terminal state contributes its FIRST-policy run (where
+    the reference's DFS first meets it); one with several gets every terminal with
+    its DFS path in DFS order from the level-synchronous least-path ranking
+    (nonterm_traces).  Returns (traces, stats of the sweep per configuration)."""
     from ._lib import ConfigError, LimitError, ModelBug
     from .machine import FIRST, Machine, Trace
     from .model import config_feasible, enumerate_configs
@@ -83,19 +114,23 @@ def check_nontermination(platform: PlatformConfig, problem: ProblemSpec, max_dep
                      key=lambda c: (-c.wg, -c.ts))
     if not configs:
         return [], []
-    stats = explore_configs(platform, problem, configs, max_states)
+    stats = explore_configs(platform, problem, configs, max_states, max_depth=max_depth)
     traces = []
     for c, st in zip(configs, stats):
         if st.deadlocks:
             raise ModelBug("deadlock reached during exploration")
+        if st.states_visited >= max_states:
+            raise LimitError("check_nontermination: the visited set fills up, where the "
+                             "reference's DFS truncates in traversal order")
         if st.terminals == 0:
             continue
-        if st.terminals > 1:
-            raise LimitError(f"check_nontermination: configuration ({c.wg}, {c.ts}) has "
-                             f"{st.terminals} terminal states; only single-terminal spaces are served")
-        tr = []
-        r = Machine(platform, problem, c).run(FIRST, trace_out=tr)
-        if len(tr) > max_depth:
+        if st.terminals == 1 and st.complete:
+            tr = []
+            r = Machine(platform, problem, c).run(FIRST, trace_out=tr)
+            traces.append(Trace(tr, r.time, c, len(tr)))
             continue
-        traces.append(Trace(tr, r.time, c, len(tr)))
+        for t, tr in nonterm_traces(platform, problem, c, max_depth,
+                                    min(max_states, st.states_visited + 1), st.terminals,
+                                    st.terminals * (st.max_depth_reached + 1)):
+            traces.append(Trace(tr, t, c, len(tr)))
     return traces, stats

@@ -18,17 +18,17 @@ CASES = [((1, 1, 4, 4), s, k) for s in (8, 16, 32) for k in (0, 1)] + \
         [((1, 2, 4, 4), 16, 0), ((1, 1, 8, 2), 16, 1), ((2, 1, 4, 4), 8, 0), ((1, 2, 2, 3), 16, 0)]
 
 
-def ref_nonterm(ref, plat, size, kernel, max_depth=0, max_states=0):
+def ref_nonterm(ref, plat, size, kernel, max_depth=0, max_states=0, rows_cap=256):
     out = (C.c_int64 * 5)()
-    rows = (C.c_int64 * (4 * 256))()
+    rows = (C.c_int64 * (4 * rows_cap))()
     buf = (C.c_int32 * (4 * TRACE_CAP))()
     n = C.c_longlong()
     ref._chk(ref.lib.ref_check_nontermination(_plat(plat), size, kernel, _inp(size, kernel, None),
                                               C.c_longlong(max_depth), C.c_longlong(max_states),
-                                              out, rows, C.c_longlong(256), buf,
+                                              out, rows, C.c_longlong(rows_cap), buf,
                                               C.c_longlong(TRACE_CAP), C.byref(n)))
     trs, pos, allt = [], 0, _untr(buf, n.value)
-    for i in range(min(out[0], 256)):
+    for i in range(min(out[0], rows_cap)):
         wg, ts, t, steps = rows[4 * i:4 * i + 4]
         trs.append({"wg": wg, "ts": ts, "final_time": t, "steps": steps,
                     "sha": trace_sha(allt[pos:pos + steps])})

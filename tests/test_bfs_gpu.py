@@ -206,7 +206,24 @@ def test_check_nontermination_matches_reference(engine, gold):
     traces, _ = m.check_nontermination(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8),
                                        max_depth=1)
     assert traces == []
-    # handover skew: the reference returns > 256 terminal states for this space;
-    # the engine refuses rather than return a different set
+    # several terminal states per configuration (host re-arming on 2-3 devices), with
+    # and without a depth cap: every terminal's DFS path, in DFS order (lexrank.cu)
+    for c in gold("nonterm_multi.json"):
+        key = (tuple(c["plat"]), c["size"], c["kernel"], c["depth_cap"])
+        traces, stats = m.check_nontermination(m.PlatformConfig(*c["plat"]),
+                                               problem(m, c["size"], c["kernel"]),
+                                               max_depth=c["depth_cap"] or 4_000_000)
+        assert len(traces) == c["n"], key
+        for t, g in zip(traces, c["traces"]):
+            assert (t.params.wg, t.params.ts, t.final_time, t.steps) == \
+                (g["wg"], g["ts"], g["final_time"], g["steps"]), key
+            assert sha(t.transitions) == g["sha"], key
+        assert sum(s.states_visited for s in stats) == c["states"], key
+        assert sum(s.transitions_applied for s in stats) == c["transitions"], key
+        assert max(s.max_depth_reached for s in stats) == c["max_depth"], key
+        assert any(not s.complete for s in stats) == bool(c["limit_hit"]), key
+    # a visited set that fills up: the reference's truncation follows its traversal
+    # order, which the engine refuses to guess
     with pytest.raises(m.LimitError):
-        m.check_nontermination(m.PlatformConfig(3, 1, 1, 1), m.ProblemSpec.minimum(32))
+        m.check_nontermination(m.PlatformConfig(3, 1, 1, 1), m.ProblemSpec.minimum(32),
+                               max_states=100_000)
