@@ -15,11 +15,9 @@ from .machine import (FIRST, MT19937, PHILOX, ROUND_ROBIN, SEEDED_RANDOM, Machin
 from .explore import ExploreStats, SweepInfo, check_nontermination, explore_configs, explore_machine
 from .search import (RankedTrail, SweepRow, TuneProbe, TuneResult, Verdict, bisect_min_time, check_overtime,
                      exhaustive_sweep, extract_params, rank_trails, swarm_min_time, tune)
-from . import report
 from .space import KEY_INDEX_BITS, KEY_SAT, KEY_TIME_BITS, Space, SpaceResult, space_argmin
 
 __all__ = [
-    "report",
     "ABSTRACT", "MINIMUM", "ConfigError", "CorruptTrace", "CudaError", "LimitError",
     "MctuneError", "ModelBug", "NoDeviceError", "LaunchPlan", "PlatformConfig", "ProblemSpec",
     "TuningParams", "SweepRow", "Space", "SpaceResult", "KEY_INDEX_BITS", "KEY_SAT",
