@@ -723,12 +723,12 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
 # Thread-level instructions executed per configuration by space_argmin_kernel<1>
 # on the headline workload (and on the rich space): ncu smsp__inst_executed.sum x 32
 # / 1e9 configurations.  Re-measured after every kernel change.
-INT_OPS_PER_CONFIG = 11.83  # 3.697e8 warp inst / 1e9 (profiles/r02_argmin_headline_ncu.txt)
-RICH_INST_PER_CONFIG = 11.83
+INT_OPS_PER_CONFIG = 9.69  # 3.029e8 warp inst / 1e9 (profiles/r02_argmin_v9_ncu.txt)
+RICH_INST_PER_CONFIG = 9.38  # 2.931e8 warp inst / 1e9 (profiles/r02_argmin_v9_rich_ncu.csv)
 INT_OPS_SOURCE = "ncu smsp__inst_executed.sum x 32 / configurations (profiles/r02_argmin_*)"
 # the binding pipe of that kernel in the same capture:
 # sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active
-ALU_PIPE_FRAC_NCU = 0.805
+ALU_PIPE_FRAC_NCU = 0.787
 # thread instructions per trajectory of traj_kernel on the swarm workload (ncu)
 SWARM_INST_PER_TRAJ = 397295.0  # 1.2415e10 warp inst / 1e6 trajectories
 SWARM_INST_SOURCE = "ncu smsp__inst_executed.sum x 32 / trajectories (profiles/r02_swarm_traj_ncu.csv)"

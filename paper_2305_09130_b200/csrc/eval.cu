@@ -15,7 +15,9 @@
 // grid is a multiple of the 148 SMs and each thread amortises its index decode
 // over thousands of configurations (nd is the fastest digit; per-(wg, ts, np,
 // nu) quantities are hoisted out of the nd loop).
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "cost_model.cuh"
@@ -148,21 +150,36 @@ __global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uin
                         R += (int32_t)nd;
                     }
                 }
-#pragma unroll 8
-                for (; k < run; ++k) {
-                    const uint32_t tf = max(Q + 1, w_hi) * D32;
+                // Every configuration's waves is evaluated and compared.  Within the run
+                // the batch duration D32 is fixed and waves is non-increasing, so the
+                // run's least (time, index) is its last waves at the first index that
+                // reached it: compare each waves with its predecessor (one ISETP and a
+                // predicated move; no product, no running min) and form the time once
+                // at the end of the run.
+                // (waves - 1 = max(Q, w_hi - 1) is compared: the same order, one VIMNMX)
+                if (k < run) {
+                    const uint32_t w_hm1 = w_hi - 1;  // w_hi >= 1
+                    uint32_t prev = 0xffffffffu, run_k = k;
+#pragma unroll 16
+                    for (; k < run; ++k) {
+                        const uint32_t w = max(Q, w_hm1);
+                        run_k = w < prev ? k : run_k;
+                        prev = w;
+                        // nd -> nd + 1: dm = Q (nd+1) + (R - Q), at most one correction,
+                        // applied as c * nd with c = (R < 0) in {0, 1}: one IMAD (FMA
+                        // pipe) in place of a mask and an add on the saturated ALU pipe
+                        ++nd;
+                        R -= (int32_t)Q;
+                        const uint32_t c = (uint32_t)R >> 31;
+                        Q -= c;
+                        R = (int32_t)mad_u32(c, nd, (uint32_t)R);
+                    }
+                    // strict: an equal time from the prefix loops keeps its smaller index
+                    const uint32_t tf = (prev + 1) * D32;
                     if (tf < best_tf) {
                         best_tf = tf;
-                        best_k = k;
+                        best_k = run_k;
                     }
-                    // nd -> nd + 1: dm = Q (nd+1) + (R - Q), at most one correction,
-                    // applied as c * nd with c = (R < 0) in {0, 1}: one IMAD (FMA pipe)
-                    // in place of a mask and an add on the saturated ALU pipe
-                    ++nd;
-                    R -= (int32_t)Q;
-                    const uint32_t c = (uint32_t)R >> 31;
-                    Q -= c;
-                    R = (int32_t)mad_u32(c, nd, (uint32_t)R);
                 }
                 if (best_k != 0xffffffffu) best_idx = base + best_k;
             }
@@ -366,7 +383,10 @@ int launch_space_argmin(const SpaceDev& s, uint64_t first, uint64_t count, uint6
     // warps idle at the tail; the hardware CTA scheduler balances the finer grid.
     // configs[4] per step (1e9): 8 CTAs/SM 0.50 ms, 16 0.44, 32 0.40, 64 0.385,
     // 128 0.40, 256 0.45
-    constexpr int kCtasPerSm = 64;
+    static const int kCtasPerSm = [] {
+        const char* e = getenv("MCTB_ARGMIN_CTAS_PER_SM");  // experiments only
+        return e ? std::max(1, atoi(e)) : 64;
+    }();
     const uint64_t max_threads = (uint64_t)sm_count() * kCtasPerSm * kThreads;
     uint64_t per_thread = (count + max_threads - 1) / max_threads;
     if (per_thread < 16) per_thread = 16;
