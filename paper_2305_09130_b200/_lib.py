@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmctune_b200.so")
+# MCTB_LIB: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("MCTB_LIB") or os.path.join(HERE, "libmctune_b200.so")
 
 
 class MctuneError(RuntimeError):

@@ -27,6 +27,9 @@ namespace mctb {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef MCTB_ARGMIN_MINB
+#define MCTB_ARGMIN_MINB 1  // resident CTAs per SM the register allocation targets
+#endif
 
 // a << sh, saturating at INT64_MAX (a >= 0)
 __device__ __forceinline__ int64_t shl_sat(int64_t a, int sh) {
@@ -63,7 +66,7 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
 }
 
 template <int KERNEL>
-__global__ void __launch_bounds__(kThreads) space_argmin_kernel(SpaceDev sd, uint64_t first,
+__global__ void __launch_bounds__(kThreads, MCTB_ARGMIN_MINB) space_argmin_kernel(SpaceDev sd, uint64_t first,
                                                                 uint64_t count,
                                                                 uint64_t per_thread,
                                                                 unsigned long long* out_key) {
@@ -388,7 +391,8 @@ int launch_space_argmin(const SpaceDev& s, uint64_t first, uint64_t count, uint6
         return e ? std::max(1, atoi(e)) : 64;
     }();
     const uint64_t max_threads = (uint64_t)sm_count() * kCtasPerSm * kThreads;
-    uint64_t per_thread = (count + max_threads - 1) / max_threads;
+    // a multiple of the 16x-unrolled loop: whole runs need no remainder iterations
+    uint64_t per_thread = ((count + max_threads - 1) / max_threads + 15) & ~15ull;
     if (per_thread < 16) per_thread = 16;
     const uint64_t threads = (count + per_thread - 1) / per_thread;
     const unsigned blocks = (unsigned)((threads + kThreads - 1) / kThreads);
