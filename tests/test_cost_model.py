@@ -61,3 +61,33 @@ def test_cost_model_against_reference_exploration_grid(oracle, ref):
                         x = ref.explore(plat, size, kernel, wg, ts)
                         t, _, _ = oracle.cost_model(plat, size, kernel, wg, ts)
                         assert x["complete"] and x["min_time"] == t, (plat, size, kernel, wg, ts)
+
+
+@pytest.mark.slow
+def test_cost_model_against_reference_runs_at_bench_scale(oracle, ref):
+    """Size 1024 (Table 1's largest) and the bench space's size 16384: the closed
+    form's (time, transitions) against the reference's Machine::run (RoundRobin)
+    on random configurations with nd / nu / np drawn from the bench ranges, both
+    kernels, multi-device plans included (runs of up to ~3e5 transitions)."""
+    rng = random.Random(2024)
+    checked = multi = 0
+    while checked < 72:
+        size = rng.choice((1024, 1024, 16384))
+        kernel = rng.randint(0, 1)
+        n = size.bit_length() - 1
+        wg, ts = 1 << rng.randint(1, n - 1), 1 << rng.randint(1, n - 1)
+        if rng.random() < 0.3:  # the bench ranges
+            plat = (rng.randint(1, 4096), rng.randint(1, 2048), 1 << rng.randint(0, 5), 4)
+        else:  # few units per device: several devices share the workgroups
+            plat = (rng.randint(2, 64), rng.randint(1, 8), 1 << rng.randint(0, 5), 4)
+        t, steps, ok = oracle.cost_model(plat, size, kernel, wg, ts)
+        if not ok or steps > 300_000:
+            continue
+        plan = oracle.derive_launch(plat, size, wg, ts)  # wgs, nwd, nwu, nwe, all_nwe
+        if plan[4] + 2 * plan[1] * plan[2] + plan[1] > 6000:
+            continue  # keep the reference's O(processes) steps cheap
+        r = ref.simulate(plat, size, kernel, wg, ts, policy=0)
+        assert (r["time"], r["steps"]) == (t, steps), (plat, size, kernel, wg, ts)
+        checked += 1
+        multi += plan[1] > 1
+    assert multi >= 10
