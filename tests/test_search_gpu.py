@@ -208,3 +208,18 @@ def test_depth_cap_matches_reference(engine, gold):
         assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
     with pytest.raises(m.ConfigError):
         m.check_overtime(m.PlatformConfig(1, 1, 4, 4), m.ProblemSpec.abstract(8), 44, max_depth=0)
+
+
+def test_tune_at_large_sizes_matches_reference(engine, gold):
+    """configs[1]: `tune` on the paper's platform at size 512 (and 1024 when its
+    reference run is recorded) against the reference's own run (~66 min on one
+    core at 512): every result field and the counterexample trace."""
+    m = engine
+    for c in gold("tune_large.json"):
+        r = m.tune(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]), seed=c["seed"])
+        key = c["size"]
+        assert (r.t_min, r.params.wg, r.params.ts, r.t_ini, r.proven) == (
+            c["t_min"], c["wg"], c["ts"], c["t_ini"], bool(c["proven"])), key
+        assert (r.stats.checks_run, r.stats.states_visited_total, r.first_trail_time) == (
+            c["checks_run"], c["states_visited_total"], c["first_trail_time"]), key
+        assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
