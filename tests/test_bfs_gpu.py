@@ -227,3 +227,15 @@ def test_check_nontermination_matches_reference(engine, gold):
     with pytest.raises(m.LimitError):
         m.check_nontermination(m.PlatformConfig(3, 1, 1, 1), m.ProblemSpec.minimum(32),
                                max_states=100_000)
+
+
+def test_large_explorations_match_independent_counts(engine, gold):
+    """The wide exploration workloads (5.6e7 and configs[3]'s 1.37e8 states) against
+    the independent CPU counter's states and transitions (tests/golden/large_counts.json)."""
+    m = engine
+    for c in gold("large_counts.json"):
+        x = m.explore_configs(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]),
+                              [m.TuningParams(c["wg"], c["ts"])], max_states=400_000_000)[0]
+        assert x.complete and (x.states_visited, x.transitions_applied, x.terminals) == (
+            c["states"], c["transitions"], c["terminals"]), c
+        assert x.max_depth_reached == c["levels"] - 1, c
