@@ -516,10 +516,11 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                 bool fresh = ins >= 0;
                 int keeper = -1;
                 if (!kept && a.keep) {
-                    // keep the first new successor of this warp's partition: no queue
-                    // round trip on the chain; it inherits the parent's place in
-                    // `outstanding`
-                    const unsigned m = __ballot_sync(0xffffffffu, fresh && owner == mp);
+                    // keep the first new successor, whichever partition owns its slot:
+                    // no queue round trip on the chain (also none to another
+                    // partition's queue); it inherits the parent's place in this
+                    // partition's `outstanding`, which the chain's end releases
+                    const unsigned m = __ballot_sync(0xffffffffu, fresh);
                     if (m) {
                         keeper = __ffs(m) - 1;
                         if (lane == keeper) fresh = false;
