@@ -738,7 +738,7 @@ SWARM_INST_SOURCE = "ncu smsp__inst_executed.sum x 32 / trajectories (profiles/r
 # re-measured after every change of explore_kernel (profiles/).
 EXPLORE_SIZE = 64
 EXPLORE_PARAMS = (16, 2)
-EXPLORE_STATES = 137_145_999  # the state count, pinned (GPU P = 1..8 partitions agree)
+EXPLORE_STATES = 137_145_999  # pinned by the independent CPU count (tests/golden/large_counts.json)
 EXPLORE_INST_PER_STATE = 1071.9  # profiles/r01_explore_v8_ncu.txt
 EXPLORE_DRAM_BYTES_PER_STATE = 1038.8
 
