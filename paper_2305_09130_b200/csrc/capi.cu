@@ -83,11 +83,12 @@ int scratch(Scratch** out) {
     std::lock_guard<std::mutex> lock(mu);
     Scratch& s = per_dev[dev & 63];
     if (!s.d_key) {
-        MCTB_CUDA(cudaMalloc(&s.d_key, sizeof(uint64_t)));
+        // [key, out[0..15]] contiguous on both sides: one copy brings the result back
+        MCTB_CUDA(cudaMalloc(&s.d_key, 17 * sizeof(uint64_t)));
+        s.d_out = reinterpret_cast<int64_t*>(s.d_key + 1);
         MCTB_CUDA(cudaMalloc(&s.d_exact, 2 * sizeof(uint64_t)));
-        MCTB_CUDA(cudaMalloc(&s.d_out, 16 * sizeof(int64_t)));
-        MCTB_CUDA(cudaMallocHost(&s.h_key, sizeof(uint64_t)));
-        MCTB_CUDA(cudaMallocHost(&s.h_out, 16 * sizeof(int64_t)));
+        MCTB_CUDA(cudaMallocHost(&s.h_key, 17 * sizeof(uint64_t)));
+        s.h_out = reinterpret_cast<int64_t*>(s.h_key + 1);
         MCTB_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     }
     *out = &s;
@@ -209,9 +210,7 @@ int mctb_space_argmin(const int64_t* sd, uint64_t first, uint64_t count, uint64_
     if ((rc = launch_fill_key(sc->d_key, sc->stream))) return rc;
     if ((rc = launch_space_argmin(s, first, count, sc->d_key, sc->stream))) return rc;
     if ((rc = launch_space_point(s, sc->d_key, sc->d_out, sc->stream))) return rc;
-    MCTB_CUDA(cudaMemcpyAsync(sc->h_key, sc->d_key, sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                              sc->stream));
-    MCTB_CUDA(cudaMemcpyAsync(sc->h_out, sc->d_out, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost,
+    MCTB_CUDA(cudaMemcpyAsync(sc->h_key, sc->d_key, 9 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                               sc->stream));
     MCTB_CUDA(cudaStreamSynchronize(sc->stream));
     *key = *sc->h_key;
