@@ -1182,6 +1182,9 @@ int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* i
     a.cfg_cap = c->cfg_cap;
     a.keep = 1;
     a.check_inv = (flags & 1) ? 1 : 0;
+    // as run_bfs: publish warp counts often enough for the visited cap to bind
+    a.flush_states = (unsigned)std::min<uint64_t>(
+        4096, std::max<uint64_t>(16, c->cfg_cap / (4ull * c->grid * (kBfsThreads / 32) * world)));
     a.n_parts = world;
     a.part0 = rank;
     a.n_here = 1;
