@@ -223,7 +223,8 @@ class ReferencePool:
 
     def __init__(self, hi, seed=1, workers=None):
         self.workers = workers or os.cpu_count() or 1
-        ctx = mp.get_context("fork")
+        # spawn, not fork: the GPU arm has CUDA and torch's threads running
+        ctx = mp.get_context("spawn")
         self.q = ctx.Queue()
         self.procs = [ctx.Process(target=_ref_worker, args=(w, seed, hi, self.q), daemon=True)
                       for w in range(self.workers)]
