@@ -46,6 +46,7 @@ struct Walk {
     int64_t T = -1;
     std::vector<int32_t> path;
     int64_t final_time = -1, applies = 0, sib_states = 0, sib_transitions = 0;
+    bool sib_capped = false;  // the siblings' subtrees alone fill the visited set
     int64_t sib_depth = 0;  // deepest state of the abandoned siblings' subtrees
 };
 
@@ -99,6 +100,7 @@ int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
         }
         const BfsStats& b = r.stats[0];
         w.sib_states = (int64_t)std::min<uint64_t>(b.states, c.cap);
+        w.sib_capped = b.capped != 0;
         w.sib_transitions = (int64_t)b.transitions;
         // every sibling subtree state leads to a terminal: the deepest one is the
         // latest terminal reached, or the cap
@@ -271,32 +273,55 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
         const int64_t tmin = !b.capped ? b.min_time
                              : c.cm_time[k] <= t_depth ? c.cm_time[k] : INT64_MAX;
         if (tmin <= Tk) {
-            v.violated = true;
-            v.cfg = k;
             if ((*rc_out = ensure_first(c, k))) return v;
+            // The DFS inserts the states it meets, in order, until the visited set
+            // holds max_states (explore.cpp:28-31): it finds the terminal only if
+            // every state before it in DFS order fits — the first path's, or the
+            // guided walk's path with the abandoned siblings' subtrees before each
+            // step.  Otherwise this configuration ends capped, with no verdict.
+            bool found;
             if (c.first_time[k] <= Tk) {
                 // DFS reaches a satisfying terminal on its first path
-                v.final_time = c.first_time[k];
-                v.steps = c.first_steps[k];
-                v.states += v.steps + 1;
-                v.transitions += v.steps;
-                v.max_depth = std::max(v.max_depth, v.steps);
+                found = (uint64_t)c.first_steps[k] + 1 <= c.cap;
+                if (found) {
+                    v.final_time = c.first_time[k];
+                    v.steps = c.first_steps[k];
+                    v.states += v.steps + 1;
+                    v.transitions += v.steps;
+                    v.max_depth = std::max(v.max_depth, v.steps);
+                    v.path = nullptr;
+                }
             } else {
                 // schedule-dependent configuration: the DFS backtracks into later
                 // branches; its first satisfying path comes from the guided walk and
                 // its effort from the abandoned siblings' exploration
                 const Walk* w = nullptr;
                 if ((*rc_out = ensure_walk(c, k, Tk, &w))) return v;
-                v.path = &w->path;
-                v.final_time = w->final_time;
-                v.steps = (int64_t)(w->path.size() / 4);
-                v.states += 1 + v.steps + w->sib_states;
-                v.transitions += w->applies + w->sib_transitions;
-                // the path and the abandoned siblings' subtrees
-                v.max_depth = std::max(v.max_depth, std::max(v.steps, w->sib_depth));
+                const int64_t steps = (int64_t)(w->path.size() / 4);
+                found = !w->sib_capped && (uint64_t)(1 + steps + w->sib_states) <= c.cap;
+                if (found) {
+                    v.path = &w->path;
+                    v.final_time = w->final_time;
+                    v.steps = steps;
+                    v.states += 1 + v.steps + w->sib_states;
+                    v.transitions += w->applies + w->sib_transitions;
+                    // the path and the abandoned siblings' subtrees
+                    v.max_depth = std::max(v.max_depth, std::max(v.steps, w->sib_depth));
+                }
             }
-            v.exhaustive = false;
-            return v;
+            if (found) {
+                v.violated = true;
+                v.cfg = k;
+                v.exhaustive = false;
+                return v;
+            }
+            // the visited set filled before the satisfying terminal: the reference
+            // goes on to the next configuration with limit_hit (its transitions_applied
+            // here depends on its DFS order; the sweep's count stands in)
+            v.states += (int64_t)c.cap;
+            v.transitions += (int64_t)b.transitions;
+            limit = true;
+            continue;
         }
         v.states += (int64_t)std::min<uint64_t>(b.states, c.cap);
         v.transitions += (int64_t)b.transitions;

@@ -223,3 +223,34 @@ def test_tune_at_large_sizes_matches_reference(engine, gold):
         assert (r.stats.checks_run, r.stats.states_visited_total, r.first_trail_time) == (
             c["checks_run"], c["states_visited_total"], c["first_trail_time"]), key
         assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
+
+
+def test_visited_cap_matches_reference(engine, gold):
+    """A small max_states (explore.cpp:28-31): a configuration whose satisfying
+    terminal lies beyond the visited set's capacity in the DFS's order (its first
+    path, or the guided walk's path behind the abandoned siblings' subtrees) ends
+    capped with no verdict and the check moves on, as the reference does.  The
+    verdicts, states_visited, counterexamples and tune results match;
+    transitions_applied under a binding cap depends on the DFS order and is not
+    compared."""
+    m = engine
+    g = gold("cap.json")
+    for c in g["checks"]:
+        key = (c["plat"], c["size"], c["T"], c["max_states"])
+        v = m.check_overtime(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]),
+                             c["T"], max_states=c["max_states"])
+        assert (v.violated, v.exhaustive, v.stats.states_visited) == (
+            bool(c["violated"]), bool(c["exhaustive"]), c["states"]), key
+        if v.violated:
+            assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
+                c["final_time"], c["wg"], c["ts"], c["steps"]), key
+            assert sha(v.trace.transitions) == c["trace_sha"], key
+    for c in g["tunes"]:
+        key = (c["plat"], c["size"], c["max_states"])
+        r = m.tune(m.PlatformConfig(*c["plat"]), problem(m, c["size"], c["kernel"]), seed=1,
+                   max_states=c["max_states"])
+        assert (r.t_min, r.params.wg, r.params.ts, r.t_ini, r.proven) == (
+            c["t_min"], c["wg"], c["ts"], c["t_ini"], bool(c["proven"])), key
+        assert (r.stats.checks_run, r.stats.states_visited_total) == (
+            c["checks_run"], c["states_visited_total"]), key
+        assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
