@@ -317,11 +317,12 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     MState t;
     // warp-local statistics of the current configuration, flushed on change/exit
     int cur_cfg = -1;
-    unsigned long long n_states = 0, n_trans = 0;
+    // (32-bit: flushed at least every 64 expansions; registers are the kernel's limit)
+    unsigned n_states = 0, n_trans = 0;
     auto flush = [&]() {
         if (lane == 0 && cur_cfg >= 0) {
-            if (n_states) atomicAdd(&a.stats[cur_cfg].states, n_states);
-            if (n_trans) atomicAdd(&a.stats[cur_cfg].transitions, n_trans);
+            if (n_states) atomicAdd(&a.stats[cur_cfg].states, (unsigned long long)n_states);
+            if (n_trans) atomicAdd(&a.stats[cur_cfg].transitions, (unsigned long long)n_trans);
         }
         n_states = n_trans = 0;
     };
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     uint64_t H = 0;      // hash of the parent (known for a kept successor)
     // queue entries are claimed in runs: a warp that finds its entries already
     // filled doubles its next claim (up to 8), one that has to wait claims one
-    unsigned long long h_next = 0, h_end = 0, h_run = 0;
+    // queue positions (< queue_cap <= 2^28, plus the idle warps' last claims)
+    uint32_t h_next = 0, h_end = 0, h_run = 0;
     unsigned claim = 1;
     uint32_t peek = kEmpty;  // lane j: entry h_run + j of the current run, as first read
     uint32_t dep = 0;        // depth of the parent (tracked under a depth cap only)
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             if (h_next == h_end) {
                 unsigned long long h0 = 0;
                 if (lane == 0) h0 = atomicAdd(me.head, (unsigned long long)claim);
-                h_run = h_next = __shfl_sync(0xffffffffu, h0, 0);
+                h_run = h_next = (uint32_t)__shfl_sync(0xffffffffu, h0, 0);
                 h_end = h_next + claim;
                 // read the whole run at once and start the filled entries' slot lines
                 // on their way to L2; a later pop of a filled entry needs no poll
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                 if (peek != kEmpty)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(me.table + (uint64_t)peek * SW));
             }
-            const unsigned long long h = h_next++;
+            const uint32_t h = h_next++;
             if (h >= a.queue_cap) break;
             uint32_t slot = __shfl_sync(0xffffffffu, peek, (int)(h - h_run));
             bool waited = false;
