@@ -173,3 +173,54 @@ TEST_CASE("non-termination counterexamples enumerate terminating runs (test_expl
     limits.max_depth = 1;
     CHECK(check_nontermination(kPlat, problem, limits).empty());
 }
+
+TEST_CASE("check_nontermination with several terminal states per configuration") {
+    // (3,1,1,1) minimum size 16: host re-arming on three devices; the reference's
+    // traces in DFS order (tests/golden/nonterm_multi.json)
+    const PlatformConfig plat{3, 1, 1, 1};
+    const ProblemSpec problem = ProblemSpec::minimum(16);
+    ExploreStats stats;
+    const auto traces = check_nontermination(plat, problem, ExploreLimits{}, &stats);
+    REQUIRE(traces.size() == 25);
+    CHECK(traces[0].params == TuningParams{8, 2});
+    CHECK(traces[0].final_time == 17);
+    CHECK(traces[0].steps == 79);
+    CHECK(traces[1].params == TuningParams{4, 4});
+    CHECK(traces[1].steps == 71);
+    CHECK(traces[2].final_time == 9);
+    CHECK(traces[3].steps == 83);
+    CHECK(stats.states_visited == 32778);
+    CHECK(stats.transitions_applied == 85370);
+    CHECK(stats.max_depth_reached == 104);
+    for (const auto& t : traces) CHECK(replay(plat, problem, t).time == t.final_time);
+}
+
+TEST_CASE("ExploreLimits::max_depth cuts the DFS") {
+    const PlatformConfig plat{3, 1, 1, 1};
+    const ProblemSpec problem = ProblemSpec::minimum(16);
+    ExploreLimits limits;
+    limits.max_depth = 67;
+    const Verdict v = check_overtime(plat, problem, 17, limits);
+    CHECK(v.violated);
+    CHECK_FALSE(v.exhaustive);
+    CHECK(v.stats.states_visited == 540);
+    REQUIRE(v.trace.has_value());
+    CHECK(v.trace->params == TuningParams{2, 8});
+    CHECK(v.trace->steps == 67);
+    const TuneResult r = tune(plat, problem, 1, limits);
+    CHECK(r.t_min == 17);  // 9 without the cap
+    CHECK(r.params == TuningParams{2, 8});
+    CHECK_FALSE(r.proven);
+    CHECK(r.stats.states_visited_total == 30165);
+    limits.max_depth = 0;
+    CHECK_THROWS_AS(check_overtime(plat, problem, 17, limits), ConfigError);
+}
+
+TEST_CASE("a binding visited cap moves the counterexample") {
+    ExploreLimits limits;
+    limits.max_states = 300;
+    const TuneResult r = tune(kPlat, ProblemSpec::abstract(16), 1, limits);
+    CHECK(r.t_min == 84);
+    CHECK(r.params == TuningParams{2, 8});  // (4, 8) without the cap
+    CHECK(r.stats.states_visited_total == 20980);
+}
