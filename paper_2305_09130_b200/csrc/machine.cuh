@@ -386,10 +386,10 @@ __host__ __device__ inline int device_rules(const MachDesc& m, const MState& s, 
     return n;
 }
 
-__host__ __device__ inline int unit_rules(const MachDesc& m, const MState& s, int g,
-                                          Transition* out, int n) {
+// (the _at forms take the process ids the serial enumeration already has)
+__host__ __device__ inline int unit_rules_at(const MachDesc& m, const MState& s, int g, int upid,
+                                             int d, Transition* out, int n) {
     const UnitS& un = s.unit[g];
-    const int upid = unit_pid(m, g);
     switch (un.pc) {
         case U_ACTIVATEPEX:
         case U_REACTPEX:
@@ -401,8 +401,7 @@ __host__ __device__ inline int unit_rules(const MachDesc& m, const MState& s, in
             break;
         }
         case U_SENDUNITDONE:
-            if (s.dev[div_nwu(m, g)].pc == D_WAITUNITDONE)
-                MCTB_PUSH(upid, device_pid(m, div_nwu(m, g)), OP_UNITDONE, un.nwg);
+            if (s.dev[d].pc == D_WAITUNITDONE) MCTB_PUSH(upid, device_pid(m, d), OP_UNITDONE, un.nwg);
             break;
         case U_STOPBARRIER:
             if (s.bar[g].pc == B_COUNTING && s.bar[g].count == 0)
@@ -413,19 +412,27 @@ __host__ __device__ inline int unit_rules(const MachDesc& m, const MState& s, in
     return n;
 }
 
-__host__ __device__ inline int barrier_rules(const MachDesc& m, const MState& s, int g,
-                                             Transition* out, int n) {
+__host__ __device__ inline int unit_rules(const MachDesc& m, const MState& s, int g,
+                                          Transition* out, int n) {
+    return unit_rules_at(m, s, g, unit_pid(m, g), div_nwu(m, g), out, n);
+}
+
+__host__ __device__ inline int barrier_rules_at(const MachDesc& m, const MState& s, int g,
+                                                int bpid, Transition* out, int n) {
     const BarS& b = s.bar[g];
-    if (b.pc == B_COUNTING && b.count == m.nwe) MCTB_PUSH(barrier_pid(m, g), kNoPeer, OP_BARRIERRELEASE, 0);
+    if (b.pc == B_COUNTING && b.count == m.nwe) MCTB_PUSH(bpid, kNoPeer, OP_BARRIERRELEASE, 0);
     return n;
 }
 
-__host__ __device__ inline int pex_rules(const MachDesc& m, const MState& s, int p,
-                                         Transition* out, int n) {
-    const int g = div_nwe(m, p);
+__host__ __device__ inline int barrier_rules(const MachDesc& m, const MState& s, int g,
+                                             Transition* out, int n) {
+    return barrier_rules_at(m, s, g, barrier_pid(m, g), out, n);
+}
+
+// element p = g * nwe + e of unit g (process ids upid, upid + 2 + e)
+__host__ __device__ inline int pex_rules_at(const MachDesc& m, const MState& s, int p, int g,
+                                            int upid, int ppid, Transition* out, int n) {
     const PexS& px = s.pex[p];
-    const int upid = unit_pid(m, g);
-    const int ppid = upid + 2 + (p - g * m.nwe);
     switch (px.pc) {
         case P_RUN: {
             const Instr in = instr_at(m, px.phase, px.cursor);
@@ -450,6 +457,13 @@ __host__ __device__ inline int pex_rules(const MachDesc& m, const MState& s, int
         default: break;
     }
     return n;
+}
+
+__host__ __device__ inline int pex_rules(const MachDesc& m, const MState& s, int p,
+                                         Transition* out, int n) {
+    const int g = div_nwe(m, p);
+    const int upid = unit_pid(m, g);
+    return pex_rules_at(m, s, p, g, upid, upid + 2 + (p - g * m.nwe), out, n);
 }
 #undef MCTB_PUSH
 
@@ -481,18 +495,22 @@ __host__ __device__ inline int enabled(const MachDesc& m, const MState& s, Trans
     if (n >= max_out) return n;
     n = clock_rules(m, s, out, n);
     if (n >= max_out) return n;
-    int g = 0;
+    // process ids advance with the enumeration (device_pid / unit_pid without divisions)
+    int g = 0, p = 0, pid = 3;
     for (int d = 0; d < m.nwd; ++d) {
         n = device_rules(m, s, d, out, n);
         if (n >= max_out) return n;
+        ++pid;
         for (int u = 0; u < m.nwu; ++u, ++g) {
-            n = unit_rules(m, s, g, out, n);
-            n = barrier_rules(m, s, g, out, n);
+            const int upid = pid;
+            n = unit_rules_at(m, s, g, upid, d, out, n);
+            n = barrier_rules_at(m, s, g, upid + 1, out, n);
             if (n >= max_out) return n;
-            for (int e = 0; e < m.nwe; ++e) {
-                n = pex_rules(m, s, g * m.nwe + e, out, n);
+            for (int e = 0; e < m.nwe; ++e, ++p) {
+                n = pex_rules_at(m, s, p, g, upid, upid + 2 + e, out, n);
                 if (n >= max_out) return n;
             }
+            pid += 2 + m.nwe;
         }
     }
     return n;
