@@ -731,7 +731,7 @@ INT_OPS_SOURCE = "ncu smsp__inst_executed.sum x 32 / configurations (profiles/r0
 # sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active
 ALU_PIPE_FRAC_NCU = 0.787
 # thread instructions per trajectory of traj_kernel on the swarm workload (ncu)
-SWARM_INST_PER_TRAJ = 397295.0  # 1.2415e10 warp inst / 1e6 trajectories
+SWARM_INST_PER_TRAJ = 372337.0  # 1.1636e10 warp inst / 1e6 trajectories
 SWARM_INST_SOURCE = "ncu smsp__inst_executed.sum x 32 / trajectories (profiles/r02_swarm_traj_ncu.csv)"
 
 # configs[3]: the exploration workload (1.37e8 states) and its ncu figures per
