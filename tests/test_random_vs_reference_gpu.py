@@ -1,0 +1,93 @@
+"""Randomised GPU-against-reference checks (the reference core oracle/_ref, built
+here and shipped with the snapshot): explore_machine, check_overtime and
+check_nontermination on random small platforms, problems and ExploreLimits
+(depth and visited caps included), every compared field equal."""
+import hashlib
+import random
+import struct
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(trace):
+    return hashlib.sha256(b"".join(struct.pack("<4i", *t) for t in trace)).hexdigest()
+
+
+def problem(m, size, kernel, inp=None):
+    return m.ProblemSpec.abstract(size) if kernel == 0 else m.ProblemSpec.minimum(size, inp)
+
+
+def _case(rng):
+    plat = (rng.randint(1, 3), rng.randint(1, 2), 1 << rng.randint(0, 2), rng.randint(1, 4))
+    size = rng.choice((4, 8, 8, 16))
+    kernel = rng.randint(0, 1)
+    inp = [rng.randint(-99, 99) for _ in range(size)] if kernel and rng.random() < 0.5 else None
+    return plat, size, kernel, inp
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_explorations(engine, ref, seed):
+    m = engine
+    rng = random.Random(1000 + seed)
+    for _ in range(10):
+        plat, size, kernel, inp = _case(rng)
+        cfgs = [c for c in m.enumerate_configs(size) if kernel == 0 or c.wg * c.ts <= size]
+        c = rng.choice(cfgs)
+        depth = rng.choice((0, 0, rng.randint(1, 300)))
+        states = rng.choice((0, 0, rng.randint(1, 5000)))
+        x = ref.explore(plat, size, kernel, c.wg, c.ts, inp, max_depth=depth, max_states=states)
+        g = m.explore_machine(m.PlatformConfig(*plat), problem(m, size, kernel, inp), c,
+                              max_states=states or 5_000_000, max_depth=depth or 4_000_000)
+        key = (plat, size, kernel, c, depth, states)
+        assert (g.complete, g.states_visited) == (bool(x["complete"]), x["states"]), key
+        if x["states"] < (states or 5_000_000):  # the cap did not bind: order-independent
+            assert (g.transitions_applied, g.max_depth_reached, g.terminals) == (
+                x["transitions"], x["max_depth"], x["n_terminal"]), key
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_checks(engine, ref, seed):
+    m = engine
+    rng = random.Random(2000 + seed)
+    for _ in range(6):
+        plat, size, kernel, inp = _case(rng)
+        t = m.tune(m.PlatformConfig(*plat), problem(m, size, kernel, inp))
+        T = rng.choice((t.t_min, t.t_min - 1, t.t_min + rng.randint(0, 50), t.t_ini))
+        depth = rng.choice((0, 0, rng.randint(20, 400)))
+        states = rng.choice((0, 0, rng.randint(50, 5000)))
+        r = ref.check_overtime(plat, size, kernel, T, inp, max_depth=depth, max_states=states)
+        v = m.check_overtime(m.PlatformConfig(*plat), problem(m, size, kernel, inp), T,
+                             max_states=states or 5_000_000, max_depth=depth or 4_000_000)
+        key = (plat, size, kernel, T, depth, states)
+        assert (v.violated, v.exhaustive, v.stats.states_visited) == (
+            bool(r["violated"]), bool(r["exhaustive"]), r["states"]), key
+        if v.violated:
+            assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
+                r["final_time"], r["wg"], r["ts"], r["steps"]), key
+            assert sha(v.trace.transitions) == sha(r["trace"]), key
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_nontermination(engine, ref, seed):
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_golden_nonterm import ref_nonterm
+    m = engine
+    rng = random.Random(3000 + seed)
+    for _ in range(3):
+        plat, size, kernel, _ = _case(rng)
+        depth = rng.choice((0, 0, rng.randint(20, 300)))
+        r = ref_nonterm(ref, plat, size, kernel, max_depth=depth, rows_cap=4096)
+        traces, stats = m.check_nontermination(m.PlatformConfig(*plat), problem(m, size, kernel),
+                                               max_depth=depth or 4_000_000)
+        key = (plat, size, kernel, depth)
+        assert len(traces) == r["n"], key
+        for t, g in zip(traces, r["traces"]):
+            assert (t.params.wg, t.params.ts, t.final_time, t.steps) == (
+                g["wg"], g["ts"], g["final_time"], g["steps"]), key
+            assert sha(t.transitions) == g["sha"], key
+        assert sum(s.states_visited for s in stats) == r["states"], key
+        assert sum(s.transitions_applied for s in stats) == r["transitions"], key
