@@ -91,3 +91,29 @@ def test_random_nontermination(engine, ref, seed):
             assert sha(t.transitions) == g["sha"], key
         assert sum(s.states_visited for s in stats) == r["states"], key
         assert sum(s.transitions_applied for s in stats) == r["transitions"], key
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_tunes(engine, ref, seed):
+    m = engine
+    rng = random.Random(4000 + seed)
+    for _ in range(3):
+        plat, size, kernel, inp = _case(rng)
+        depth = rng.choice((0, 0, rng.randint(60, 400)))
+        states = rng.choice((0, 0, rng.randint(200, 5000)))
+        s = rng.randint(1, 9)
+        try:
+            r = ref.tune(plat, size, kernel, seed=s, inp=inp, max_depth=depth, max_states=states)
+        except Exception:
+            with pytest.raises(m.MctuneError):
+                m.tune(m.PlatformConfig(*plat), problem(m, size, kernel, inp), seed=s,
+                       max_states=states or 5_000_000, max_depth=depth or 4_000_000)
+            continue
+        g = m.tune(m.PlatformConfig(*plat), problem(m, size, kernel, inp), seed=s,
+                   max_states=states or 5_000_000, max_depth=depth or 4_000_000)
+        key = (plat, size, kernel, s, depth, states)
+        assert (g.t_min, g.params.wg, g.params.ts, g.t_ini, g.proven) == (
+            r["t_min"], r["wg"], r["ts"], r["t_ini"], bool(r["proven"])), key
+        assert (g.stats.checks_run, g.stats.states_visited_total, g.first_trail_time) == (
+            r["checks_run"], r["states_visited_total"], r["first_trail_time"]), key
+        assert g.trace.steps == r["steps"] and sha(g.trace.transitions) == sha(r["trace"]), key
