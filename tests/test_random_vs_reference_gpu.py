@@ -117,3 +117,30 @@ def test_random_tunes(engine, ref, seed):
         assert (g.stats.checks_run, g.stats.states_visited_total, g.first_trail_time) == (
             r["checks_run"], r["states_visited_total"], r["first_trail_time"]), key
         assert g.trace.steps == r["steps"] and sha(g.trace.transitions) == sha(r["trace"]), key
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_sweeps_and_runs(engine, ref, seed):
+    """exhaustive_sweep rows and Machine::run (RoundRobin / SeededRandom, with the
+    trace) on random platforms, sizes up to 64 and random inputs."""
+    m = engine
+    rng = random.Random(5000 + seed)
+    for _ in range(4):
+        plat = (rng.randint(1, 6), rng.randint(1, 5), 1 << rng.randint(0, 4), rng.randint(1, 6))
+        size = rng.choice((8, 16, 32, 64))
+        kernel = rng.randint(0, 1)
+        inp = [rng.randint(-999, 999) for _ in range(size)] if kernel else None
+        prob = problem(m, size, kernel, inp)
+        got = [(r.wg, r.ts, r.time, r.transitions, int(r.ok)) for r in
+               m.exhaustive_sweep(m.PlatformConfig(*plat), prob)]
+        want = [tuple(r[:5]) for r in ref.sweep(plat, size, kernel, inp)]
+        assert got == want, (plat, size, kernel)
+        cfgs = [c for c in m.enumerate_configs(size) if kernel == 0 or c.wg * c.ts <= size]
+        for _ in range(3):
+            c = rng.choice(cfgs)
+            policy, s = rng.choice((0, 1)), rng.randint(0, 1 << 40)
+            tr = []
+            g = m.Machine(m.PlatformConfig(*plat), prob, c).run(policy, s, trace_out=tr)
+            r = ref.simulate(plat, size, kernel, c.wg, c.ts, policy, s, inp, trace=True)
+            assert (g.time, g.steps, g.result) == (r["time"], r["steps"], r["result"]), (plat, c)
+            assert sha(tr) == sha(r["trace"]), (plat, c)
