@@ -645,6 +645,17 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
                         "frac": EXPLORE_INST_PER_STATE * rate / issue_peak,
                         "warp_inst_per_state": EXPLORE_INST_PER_STATE,
                         "peak_source": f"{sms} SMs x 4 SMSPs x 1 issue/cycle x {clk:.0f} MHz"}}}
+    # the same sweep through the multi-GPU exchange path, its 8 hash partitions on
+    # this one device (system-scope variant): the exchange's cost, counts equal
+    info8 = []
+    x8 = m.explore_configs(plat16, m.ProblemSpec.abstract(EXPLORE_SIZE),
+                           [m.TuningParams(*EXPLORE_PARAMS)], max_states=400_000_000, info=info8,
+                           partitions=8, system_scope=True)[0]
+    ex["partitioned_8"] = {"states_per_s": x8.states_visited / (info8[0].kernel_us * 1e-6),
+                           "same_counts": (x8.states_visited, x8.transitions_applied)
+                           == (x.states_visited, x.transitions_applied),
+                           "how": "8 hash partitions on one GPU, system-scope memory operations "
+                                  "(the multi-GPU kernel variant)"}
     if ref is not None:
         t0 = time.perf_counter()
         rx = ref.explore((1, 1, 8, 4), 32, 0, 8, 2)
