@@ -133,6 +133,16 @@ int mctb_trajectories(const int* plat, int size, int kernel, const int64_t* inpu
  * thread's last mctb_trajectories call, in ms (the call's rate without its copies). */
 double mctb_trajectories_kernel_ms(void);
 
+/* The cost-and-effect programs of build_abstract_kernel / build_minimum_kernel
+ * (kernel.hpp:92-118, kernel.cpp:26-82) as the engine runs them (host-side model
+ * description, no device needed): out = int32[3 * cap] rows {kind (0 busy,
+ * 1 local barrier, 2 effect, 3 end), ticks, operand}, the per-activation sequence
+ * (*n_act rows) then the epilogue (*n_epi rows, 0 for the abstract kernel); an
+ * effect's operand is its source offset (activation: glob[shift + operand] into
+ * loc[me]; epilogue: loc[me + operand] into loc[me], or -1: loc[me] into glob[0]). */
+int mctb_kernel_program(const int* plat, int size, int kernel, int wg, int ts, int32_t* out,
+                        int cap, int* n_act, int* n_epi);
+
 /* replay (explore.hpp:111-113, explore.cpp:283-300) on the GPU; out = {final_time, result} */
 int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
                 const int32_t* trace, int64_t len, int64_t final_time, int64_t* out);

@@ -189,6 +189,123 @@ inline bool config_feasible(const ProblemSpec& problem, const TuningParams& para
     return problem.kernel == KernelKind::Abstract || params.wg * params.ts <= problem.size;
 }
 
+// ------------------------------------------------------------------ kernel (kernel.hpp)
+/// kernel.hpp:11-46: memory spaces and the symbolic operands of effects.
+enum class MemSpace : std::uint8_t { Global, Local };
+
+struct MemRef {
+    enum class Base : std::uint8_t { GlobalAt, GlobalShifted, LocalSlot };
+    Base base = Base::GlobalAt;
+    int offset = 0;
+    MemSpace space() const { return base == Base::LocalSlot ? MemSpace::Local : MemSpace::Global; }
+    int resolve(int shift, int myloc) const {
+        return base == Base::GlobalAt ? offset
+               : base == Base::GlobalShifted ? shift + offset
+                                             : myloc + offset;
+    }
+};
+
+/// kernel.hpp:48-78: one instruction of a cost-and-effect program.
+struct CostInstr {
+    enum class Kind : std::uint8_t { Busy, LocalBarrier, Effect, ActivationEnd };
+    Kind kind = Kind::ActivationEnd;
+    Tick ticks = 0;
+    MemSpace tag = MemSpace::Global;
+    MemRef dst, src;
+};
+
+/// kernel.hpp:79-90: a kernel compiled to its per-activation and epilogue
+/// sequences, as the engine runs them (mctb_kernel_program).
+struct KernelProgram {
+    KernelKind kind = KernelKind::Abstract;
+    std::vector<CostInstr> per_activation;
+    std::vector<CostInstr> epilogue;
+
+    bool has_epilogue() const { return epilogue.size() > 1; }
+    Tick activation_busy_ticks() const { return busy(per_activation); }
+    Tick epilogue_busy_ticks() const { return busy(epilogue); }
+    int barriers_per_activation() const {
+        int n = 0;
+        for (const auto& c : per_activation) n += c.kind == CostInstr::Kind::LocalBarrier;
+        return n;
+    }
+
+private:
+    static Tick busy(const std::vector<CostInstr>& v) {
+        Tick t = 0;
+        for (const auto& c : v)
+            if (c.kind == CostInstr::Kind::Busy) t += c.ticks;
+        return t;
+    }
+};
+
+/// kernel.hpp:92-95.
+inline int global_item_id(const TuningParams& params, int np, int nwg, int me, int iter) {
+    return params.wg > np ? nwg * params.wg + me + iter * np : nwg * params.wg + me;
+}
+
+namespace detail {
+// The engine's program rows (include/mctune_b200.h mctb_kernel_program) as
+// CostInstr sequences: the abstract kernel's busy phases alternate a global tile
+// load (gmt * ts ticks) and a local compute (ts ticks), its last busy is the
+// global result write; the minimum kernel's map effects read the shifted global
+// tile into the item's slot, its epilogue folds the group's slots and publishes
+// glob[0].
+inline KernelProgram kernel_program(const PlatformConfig& platform, int size, int kernel,
+                                    const TuningParams& params) {
+    const int plat[4] = {platform.nd, platform.nu, platform.np, platform.gmt};
+    std::vector<std::int32_t> rows(3 * 4096);
+    int n_act = 0, n_epi = 0;
+    check(mctb_kernel_program(plat, size, kernel, params.wg, params.ts, rows.data(), 4096, &n_act,
+                              &n_epi));
+    KernelProgram prog;
+    prog.kind = kernel ? KernelKind::Minimum : KernelKind::Abstract;
+    for (int i = 0; i < n_act + n_epi; ++i) {
+        const bool epi = i >= n_act;
+        CostInstr c;
+        const std::int32_t* r = rows.data() + 3 * i;
+        c.kind = static_cast<CostInstr::Kind>(r[0]);
+        if (c.kind == CostInstr::Kind::Busy) {
+            c.ticks = r[1];
+            // abstract: the local compute phases tick ts; minimum: the epilogue's folds
+            const int j = i - (epi ? n_act : 0);
+            c.tag = kernel == 0 ? (j % 4 == 2 ? MemSpace::Local : MemSpace::Global)
+                                : (epi && r[1] == 1 && j + 1 < n_epi - 2 ? MemSpace::Local
+                                                                         : MemSpace::Global);
+        } else if (c.kind == CostInstr::Kind::Effect) {
+            if (!epi) {
+                c.dst = MemRef{MemRef::Base::LocalSlot, 0};
+                c.src = MemRef{MemRef::Base::GlobalShifted, r[2]};
+            } else if (r[2] >= 0) {
+                c.dst = MemRef{MemRef::Base::LocalSlot, 0};
+                c.src = MemRef{MemRef::Base::LocalSlot, r[2]};
+            } else {
+                c.dst = MemRef{MemRef::Base::GlobalAt, 0};
+                c.src = MemRef{MemRef::Base::LocalSlot, 0};
+            }
+        }
+        (epi ? prog.epilogue : prog.per_activation).push_back(c);
+    }
+    return prog;
+}
+}  // namespace detail
+
+/// kernel.hpp:97-101.
+inline KernelProgram build_abstract_kernel(int size, const TuningParams& params,
+                                           const PlatformConfig& platform) {
+    return detail::kernel_program(platform, size, 0, params);
+}
+
+/// kernel.hpp:103-112: ConfigError for an input of the wrong length or an
+/// infeasible (wg, ts).
+inline KernelProgram build_minimum_kernel(int size, const TuningParams& params,
+                                          const PlatformConfig& platform,
+                                          const std::vector<std::int64_t>& input) {
+    if (input.size() != static_cast<std::size_t>(size))
+        throw ConfigError("minimum kernel input length must equal size");
+    return detail::kernel_program(platform, size, 1, params);
+}
+
 // ------------------------------------------------------------------ machine (machine.hpp)
 /// Transition labels (machine.hpp:48-68).
 enum class Op : std::uint8_t {

@@ -135,3 +135,6 @@ EXPORTED.append("mctb_tune_probes")
 lib.mctb_nonterm_traces.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_int64,
                                     C.c_int64, i64p, i64p, C.c_int64, i32p, C.c_int64, i64p]
 EXPORTED.append("mctb_nonterm_traces")
+lib.mctb_kernel_program.argtypes = [i32p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, C.c_int,
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]
+EXPORTED.append("mctb_kernel_program")

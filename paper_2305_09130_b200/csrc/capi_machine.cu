@@ -42,6 +42,48 @@ int check_machine(const int* plat, int size, int kernel, int wg, int ts) {
     return MCTB_OK;
 }
 
+// The cost-and-effect programs the machine runs (kernel.cpp build_abstract_kernel /
+// build_minimum_kernel), materialised from the instruction view the GPU kernels
+// compute arithmetically (machine.cuh instr_at): out = int32[3 * cap] rows {kind
+// (0 busy, 1 barrier, 2 effect, 3 end), ticks, operand} — the per-activation
+// sequence, then the epilogue; operand = the effect's source offset (phase 0:
+// glob[shift + operand] into loc[me]; epilogue: loc[me + operand] into loc[me],
+// or -1: loc[me] into glob[0]).
+int kernel_program(const int* plat, int size, int kernel, int wg, int ts, int32_t* out,
+                   int cap, int* n_act, int* n_epi) {
+    int rc = check_machine(plat, size, kernel, wg, ts);
+    if (rc) return rc;
+    MachHost h;
+    if ((rc = build_desc(plat, size, kernel, nullptr, wg, ts, &h))) return rc;
+    int n = 0;
+    for (int phase = 0; phase < 2; ++phase) {
+        int len = 0;
+        if (phase == 1 && !has_epilogue(h.d)) {
+            *n_epi = 0;
+            break;
+        }
+        for (int c = 0;; ++c) {
+            const Instr in = instr_at(h.d, phase, c);
+            const int kind = in.kind == IK_BUSY ? 0 : in.kind == IK_BARRIER ? 1
+                             : in.kind == IK_EFFECT ? 2 : 3;
+            if (n < cap) {
+                out[3 * n] = kind;
+                out[3 * n + 1] = in.kind == IK_BUSY ? (int32_t)in.ticks : 0;
+                out[3 * n + 2] = in.kind == IK_EFFECT ? in.src : 0;
+            }
+            ++n;
+            ++len;
+            if (kind == 3) break;
+        }
+        (phase == 0 ? *n_act : *n_epi) = len;
+    }
+    if (n > cap) {
+        set_error("kernel program buffer too small");
+        return MCTB_LIMIT;
+    }
+    return MCTB_OK;
+}
+
 namespace {
 
 struct DevBuf {
@@ -306,6 +348,12 @@ int64_t mctb_trace_text(const int* plat, int size, int kernel, const int64_t* in
         buf[n] = 0;
     }
     return (int64_t)s.size();
+}
+
+// the programs of build_abstract_kernel / build_minimum_kernel (kernel.hpp:92-118)
+int mctb_kernel_program(const int* plat, int size, int kernel, int wg, int ts, int32_t* out,
+                        int cap, int* n_act, int* n_epi) {
+    return kernel_program(plat, size, kernel, wg, ts, out, cap, n_act, n_epi);
 }
 
 }  // extern "C"
