@@ -1,5 +1,5 @@
-// Drop-in for the reference's <mctune/machine.hpp>: the same names in namespace
-// mctune, served by the B200 engine (include/mctune_b200.hpp).
+// Drop-in for the reference's <mctune/machine.hpp>: Machine, MachineState,
+// Transition and run over the B200 engine, in namespace mctune.
 #pragma once
 #include "mctune_b200.hpp"
 namespace mctune = mctune_b200;

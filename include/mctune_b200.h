@@ -143,6 +143,50 @@ double mctb_trajectories_kernel_ms(void);
 int mctb_kernel_program(const int* plat, int size, int kernel, int wg, int ts, int32_t* out,
                         int cap, int* n_act, int* n_epi);
 
+/* Machine introspection on one explicit state (machine.hpp:151-233), each rule in a
+ * one-thread GPU kernel (capi_state.cu).  A state crosses the ABI as a flat int64
+ * vector of the reference MachineState's fields (machine.hpp:112-130):
+ *   {time, nrp_work, all_nwe, fin, next_wg, host_pc, host_k, clock,
+ *    nwd, {pc, k, batch_base} x nwd, n_units, {pc, k, nwg, sent, got_items, got_ends} x n_units,
+ *    n_units, {pc, count} x n_units, n_pex, {pc, phase, cursor, busy_left, reported, nwg, iter} x n_pex,
+ *    n_glob, glob values, n_loc, loc values}   (glob/loc: minimum kernel only, else 0 entries)
+ * Control locations use the ordinals of machine.hpp:22-46. */
+int mctb_machine_initial(const int* plat, int size, int kernel, const int64_t* input, int wg,
+                         int ts, int64_t* flat, int64_t cap, int64_t* n);
+/* enabled transitions in ascending actor pid: int32[4 * cap] {actor, peer, op, arg} */
+int mctb_machine_enabled(const int* plat, int size, int kernel, const int64_t* input, int wg,
+                         int ts, const int64_t* flat, int64_t n, int32_t* trans, int64_t cap,
+                         int64_t* n_trans);
+/* apply (MCTB_MODEL_BUG when the transition t = int32[4] is not enabled) */
+int mctb_machine_apply(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                       const int64_t* flat, int64_t n, const int32_t* t, int64_t* out_flat,
+                       int64_t cap, int64_t* n_out);
+/* out = int64[3] {is_terminal, check_invariants code (0 = holds), packed words}; words = the
+ * state's canonical packed words (uint32[cap]) */
+int mctb_machine_query(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                       const int64_t* flat, int64_t n, int64_t* out, uint32_t* words,
+                       int64_t cap);
+/* Machine::process_name (machine.cpp:103-113): the name's length, -1 on error */
+int64_t mctb_machine_process_name(const int* plat, int size, int kernel, int wg, int ts, int pid,
+                                  char* buf, int64_t cap);
+
+/* replay (explore.cpp:283-300) in one GPU thread: MCTB_CORRUPT_TRACE on a divergence,
+ * a non-terminal end or a final time other than final_time; the terminal state
+ * (flat) goes to out_flat */
+int mctb_machine_replay(const int* plat, int size, int kernel, const int64_t* input, int wg,
+                        int ts, const int32_t* trace, int64_t len, int64_t final_time,
+                        int64_t* out_flat, int64_t cap, int64_t* n_out);
+/* explore_machine's visit order for the per-state hooks (explore.cpp:86-165): every
+ * state within max_depth in the order the reference's DFS discovers it (the preorder
+ * of the least-path tree, lexrank.cu), truncated to the first max_states.  flat = the
+ * states (stride info[2]); meta = int32[8 * meta_cap] {in-transition actor, peer, op,
+ * arg (-1 at the root), depth, terminal, enabled count, in-edge index}; info =
+ * int64[3] {states in the full exploration, states returned, stride}.  MCTB_LIMIT
+ * (info filled) when a buffer is too small. */
+int mctb_machine_states(const int* plat, int size, int kernel, const int64_t* input, int wg,
+                        int ts, int64_t max_depth, int64_t max_states, int64_t* flat,
+                        int64_t flat_cap, int32_t* meta, int64_t meta_cap, int64_t* info);
+
 /* replay (explore.hpp:111-113, explore.cpp:283-300) on the GPU; out = {final_time, result} */
 int mctb_replay(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
                 const int32_t* trace, int64_t len, int64_t final_time, int64_t* out);

@@ -13,6 +13,8 @@
 #define MCTUNE_B200_HPP
 
 #include <algorithm>
+#include <functional>
+#include <atomic>
 #include <array>
 #include <chrono>
 #include <cstdint>
@@ -314,6 +316,9 @@ enum class Op : std::uint8_t {
     PexArrive, PexItemDone, PexEndDone, BarrierRelease
 };
 
+/// machine.hpp:70: the clock, a handshake between two processes, or a local step.
+enum class TransitionKind : std::uint8_t { ClockTick, ChannelHandshake, LocalStep };
+
 /// One atomic step of the transition system (machine.hpp:76-84).
 struct Transition {
     std::uint16_t actor = 0;
@@ -321,6 +326,16 @@ struct Transition {
     Op op = Op::ClockTick;
     std::int32_t arg = 0;
     bool operator==(const Transition&) const = default;
+    TransitionKind kind() const {
+        switch (op) {
+            case Op::ClockTick: return TransitionKind::ClockTick;
+            case Op::ClockHalt:
+            case Op::HostSetFin:
+            case Op::PexReport:
+            case Op::PexEffect: return TransitionKind::LocalStep;
+            default: return TransitionKind::ChannelHandshake;
+        }
+    }
 };
 
 /// Scheduling policies of Machine::run (machine.hpp:143) plus the engine's own.
@@ -338,6 +353,7 @@ struct RunOutcome {
     Tick time = 0;
     long long transitions = 0;
     std::optional<std::int64_t> result;
+    long long steps = 0;  // machine.hpp:148 (= transitions)
 };
 
 namespace detail {
@@ -412,10 +428,280 @@ inline RunOutcome run(const PlatformConfig& platform, const ProblemSpec& problem
     }
     RunOutcome r;
     r.time = out[0];
-    r.transitions = out[1];
+    r.transitions = r.steps = out[1];
     if (problem.kernel == KernelKind::Minimum) r.result = out[2];
     return r;
 }
+
+// ------------------------------------------------------------------ Machine (machine.hpp)
+/// Control locations (machine.hpp:22-46; the engine's ordinals are the same).
+enum class HostPc : std::uint8_t { SendGo, WaitDoneReact, ReactGo, WaitDoneStop, SendStop, SetFin, Exited };
+enum class DevicePc : std::uint8_t { WaitGo, SendUnitGo, WaitUnitDone, SendDone, StopUnits, Exited };
+enum class UnitPc : std::uint8_t { WaitGo, ActivatePex, Serve, ReactPex, SendUnitDone, StopPexes, StopBarrier, Exited };
+enum class BarrierPc : std::uint8_t { Counting, Exited };
+enum class PexPc : std::uint8_t {
+    WaitGo, Run, ArriveBarrier, WaitBarrier, ArriveGroupEnd, WaitGroupEnd, SendItemDone, SendEndDone, Exited
+};
+enum class ClockPc : std::uint8_t { Run, Exited };
+enum class PexPhase : std::uint8_t { Activation, Epilogue };
+
+/// machine.hpp:86-110.
+struct HostState {
+    HostPc pc = HostPc::SendGo;
+    std::int32_t k = 0;
+    bool operator==(const HostState&) const = default;
+};
+struct DeviceState {
+    DevicePc pc = DevicePc::WaitGo;
+    std::int32_t k = 0;
+    std::int32_t batch_base = 0;
+    bool operator==(const DeviceState&) const = default;
+};
+struct UnitState {
+    UnitPc pc = UnitPc::WaitGo;
+    std::int32_t k = 0, nwg = 0, sent = 0, got_items = 0, got_ends = 0;
+    bool operator==(const UnitState&) const = default;
+};
+struct BarrierState {
+    BarrierPc pc = BarrierPc::Counting;
+    std::int32_t count = 0;
+    bool operator==(const BarrierState&) const = default;
+};
+struct PexState {
+    PexPc pc = PexPc::WaitGo;
+    PexPhase phase = PexPhase::Activation;
+    std::int32_t cursor = 0, busy_left = 0;
+    bool reported = false;
+    std::int32_t nwg = 0, iter = 0;
+    bool operator==(const PexState&) const = default;
+};
+
+/// The full explicit state (machine.hpp:112-130).  A value type; glob and loc are
+/// the minimum kernel's memories.
+struct MachineState {
+    Tick time = 0;
+    std::int32_t nrp_work = 0;
+    std::int32_t all_nwe = 0;
+    bool fin = false;
+    std::int32_t next_wg = 0;
+    HostState host;
+    ClockPc clock = ClockPc::Run;
+    std::vector<DeviceState> devices;
+    std::vector<UnitState> units;
+    std::vector<BarrierState> barriers;
+    std::vector<PexState> pexes;
+    std::vector<std::int64_t> glob;
+    std::vector<std::int64_t> loc;
+    bool operator==(const MachineState&) const = default;
+};
+
+namespace detail {
+// MachineState <-> the ABI's flat int64 state vector (mctune_b200.h, mctb_machine_*)
+inline std::vector<std::int64_t> state_to_flat(const MachineState& s) {
+    std::vector<std::int64_t> f = {s.time,      s.nrp_work, s.all_nwe,
+                                   s.fin,       s.next_wg,  static_cast<std::int64_t>(s.host.pc),
+                                   s.host.k,    static_cast<std::int64_t>(s.clock)};
+    f.push_back(static_cast<std::int64_t>(s.devices.size()));
+    for (const auto& d : s.devices) f.insert(f.end(), {static_cast<std::int64_t>(d.pc), d.k, d.batch_base});
+    f.push_back(static_cast<std::int64_t>(s.units.size()));
+    for (const auto& u : s.units)
+        f.insert(f.end(), {static_cast<std::int64_t>(u.pc), u.k, u.nwg, u.sent, u.got_items, u.got_ends});
+    f.push_back(static_cast<std::int64_t>(s.barriers.size()));
+    for (const auto& b : s.barriers) f.insert(f.end(), {static_cast<std::int64_t>(b.pc), b.count});
+    f.push_back(static_cast<std::int64_t>(s.pexes.size()));
+    for (const auto& x : s.pexes)
+        f.insert(f.end(), {static_cast<std::int64_t>(x.pc), static_cast<std::int64_t>(x.phase),
+                           x.cursor, x.busy_left, x.reported, x.nwg, x.iter});
+    f.push_back(static_cast<std::int64_t>(s.glob.size()));
+    f.insert(f.end(), s.glob.begin(), s.glob.end());
+    f.push_back(static_cast<std::int64_t>(s.loc.size()));
+    f.insert(f.end(), s.loc.begin(), s.loc.end());
+    return f;
+}
+
+inline MachineState state_from_flat(const std::int64_t* f, std::size_t n) {
+    MachineState s;
+    std::size_t i = 0;
+    auto get = [&]() {
+        if (i >= n) throw ModelBug("truncated state vector");
+        return f[i++];
+    };
+    s.time = get();
+    s.nrp_work = static_cast<std::int32_t>(get());
+    s.all_nwe = static_cast<std::int32_t>(get());
+    s.fin = get() != 0;
+    s.next_wg = static_cast<std::int32_t>(get());
+    s.host.pc = static_cast<HostPc>(get());
+    s.host.k = static_cast<std::int32_t>(get());
+    s.clock = static_cast<ClockPc>(get());
+    s.devices.resize(static_cast<std::size_t>(get()));
+    for (auto& d : s.devices) {
+        d.pc = static_cast<DevicePc>(get());
+        d.k = static_cast<std::int32_t>(get());
+        d.batch_base = static_cast<std::int32_t>(get());
+    }
+    s.units.resize(static_cast<std::size_t>(get()));
+    for (auto& u : s.units) {
+        u.pc = static_cast<UnitPc>(get());
+        u.k = static_cast<std::int32_t>(get());
+        u.nwg = static_cast<std::int32_t>(get());
+        u.sent = static_cast<std::int32_t>(get());
+        u.got_items = static_cast<std::int32_t>(get());
+        u.got_ends = static_cast<std::int32_t>(get());
+    }
+    s.barriers.resize(static_cast<std::size_t>(get()));
+    for (auto& b : s.barriers) {
+        b.pc = static_cast<BarrierPc>(get());
+        b.count = static_cast<std::int32_t>(get());
+    }
+    s.pexes.resize(static_cast<std::size_t>(get()));
+    for (auto& x : s.pexes) {
+        x.pc = static_cast<PexPc>(get());
+        x.phase = static_cast<PexPhase>(get());
+        x.cursor = static_cast<std::int32_t>(get());
+        x.busy_left = static_cast<std::int32_t>(get());
+        x.reported = get() != 0;
+        x.nwg = static_cast<std::int32_t>(get());
+        x.iter = static_cast<std::int32_t>(get());
+    }
+    s.glob.resize(static_cast<std::size_t>(get()));
+    for (auto& v : s.glob) v = get();
+    s.loc.resize(static_cast<std::size_t>(get()));
+    for (auto& v : s.loc) v = get();
+    return s;
+}
+}  // namespace detail
+
+/// machine.hpp:236: FNV-1a over the bytes with a splitmix64 finalizer.
+inline std::uint64_t hash64(const std::string& bytes) {
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (char c : bytes) {
+        h ^= static_cast<std::uint8_t>(c);
+        h *= 0x100000001b3ull;
+    }
+    h = (h ^ (h >> 30)) * 0xbf58476d1ce4e5b9ull;
+    h = (h ^ (h >> 27)) * 0x94d049bb133111ebull;
+    return h ^ (h >> 31);
+}
+
+/// The transition system of one (platform, problem, params) choice
+/// (machine.hpp:151-233).  Every rule runs on the GPU: the methods ship one state
+/// to a one-thread kernel (mctb_machine_*) and back, so they suit stepping and
+/// inspection; whole runs (run) and explorations go through the batched kernels.
+class Machine {
+public:
+    Machine(PlatformConfig platform_in, ProblemSpec problem_in, TuningParams params_in)
+        : platform(platform_in),
+          problem(std::move(problem_in)),
+          params(params_in),
+          plan(derive_launch(platform, problem.size, params)),
+          program(problem.kernel == KernelKind::Abstract
+                      ? build_abstract_kernel(problem.size, params, platform)
+                      : build_minimum_kernel(problem.size, params, platform, problem.input)) {}
+
+    const PlatformConfig platform;
+    const ProblemSpec problem;
+    const TuningParams params;
+    const LaunchPlan plan;
+    const KernelProgram program;
+
+    int rounds() const { return params.wg / plan.nwe; }
+    int device_rounds() const { return std::max(plan.wgs / plan.nwu, 1); }
+    int process_count() const { return 3 + plan.nwd + 2 * plan.nwd * plan.nwu + plan.all_nwe; }
+
+    std::string process_name(int pid) const {
+        const detail::Args a(platform, problem);
+        char buf[64];
+        if (mctb_machine_process_name(a.plat, a.size, a.kernel, params.wg, params.ts, pid, buf,
+                                      sizeof buf) < 0)
+            throw ModelBug(mctb_last_error());
+        return buf;
+    }
+
+    MachineState initial_state() const {
+        const detail::Args a(platform, problem);
+        std::vector<std::int64_t> f(flat_cap());
+        std::int64_t n = 0;
+        detail::check(mctb_machine_initial(a.plat, a.size, a.kernel, a.input, params.wg, params.ts,
+                                           f.data(), static_cast<std::int64_t>(f.size()), &n));
+        return detail::state_from_flat(f.data(), static_cast<std::size_t>(n));
+    }
+
+    /// Every enabled transition in ascending actor pid (machine.cpp:174-336).
+    std::vector<Transition> enabled(const MachineState& s) const {
+        const detail::Args a(platform, problem);
+        const auto f = detail::state_to_flat(s);
+        std::vector<std::int32_t> buf(4 * 128);
+        std::int64_t n = 0;
+        detail::check(mctb_machine_enabled(a.plat, a.size, a.kernel, a.input, params.wg, params.ts,
+                                           f.data(), static_cast<std::int64_t>(f.size()),
+                                           buf.data(), 128, &n));
+        return detail::unpack(buf, n);
+    }
+
+    /// machine.cpp:361-649; ModelBug when t is not enabled in s.
+    MachineState apply(const MachineState& s, const Transition& t) const {
+        const detail::Args a(platform, problem);
+        const auto f = detail::state_to_flat(s);
+        const std::int32_t tr[4] = {t.actor, t.peer, static_cast<std::int32_t>(t.op), t.arg};
+        std::vector<std::int64_t> out(flat_cap());
+        std::int64_t n = 0;
+        detail::check(mctb_machine_apply(a.plat, a.size, a.kernel, a.input, params.wg, params.ts,
+                                         f.data(), static_cast<std::int64_t>(f.size()), tr,
+                                         out.data(), static_cast<std::int64_t>(out.size()), &n));
+        return detail::state_from_flat(out.data(), static_cast<std::size_t>(n));
+    }
+
+    bool is_terminal(const MachineState& s) const { return query(s)[0] != 0; }
+
+    /// machine.cpp:708-717: ModelBug on a non-terminal state.
+    Tick final_time(const MachineState& s) const {
+        if (!is_terminal(s)) throw ModelBug("final_time of a non-terminal state");
+        return s.time;
+    }
+
+    /// machine.cpp:719-756: ModelBug when a structural invariant fails.
+    void check_invariants(const MachineState& s) const {
+        const auto q = query(s);
+        if (q[1] != 0) throw ModelBug("state invariant " + std::to_string(q[1]) + " violated");
+    }
+
+    /// A canonical byte image of every field (the engine's packed words, pack.cuh —
+    /// equal states give equal bytes; it is not the reference's byte layout).
+    std::string serialize(const MachineState& s) const {
+        std::vector<std::uint32_t> w;
+        query(s, &w);
+        return std::string(reinterpret_cast<const char*>(w.data()), w.size() * 4);
+    }
+
+    /// hash64(serialize(s)) (machine.cpp:715-717).
+    std::uint64_t fingerprint(const MachineState& s) const { return hash64(serialize(s)); }
+
+    /// Machine::run (machine.cpp:788-825) on the GPU.
+    RunOutcome run(SchedPolicy policy, std::uint64_t seed = 0,
+                   std::vector<Transition>* trace_out = nullptr) const {
+        return mctune_b200::run(platform, problem, params, policy, seed, trace_out);
+    }
+
+private:
+    std::size_t flat_cap() const {
+        return 64 + 3 * 8 + 6 * 16 + 2 * 16 + 7 * 32 + static_cast<std::size_t>(problem.size) +
+               16 * 256;
+    }
+
+    std::array<std::int64_t, 3> query(const MachineState& s,
+                                      std::vector<std::uint32_t>* words = nullptr) const {
+        const detail::Args a(platform, problem);
+        const auto f = detail::state_to_flat(s);
+        std::int64_t out[3] = {0, 0, 0};
+        std::vector<std::uint32_t> w(64);
+        detail::check(mctb_machine_query(a.plat, a.size, a.kernel, a.input, params.wg, params.ts,
+                                         f.data(), static_cast<std::int64_t>(f.size()), out,
+                                         w.data(), static_cast<std::int64_t>(w.size())));
+        if (words) words->assign(w.begin(), w.begin() + out[2]);
+        return {out[0], out[1], out[2]};
+    }
+};
 
 // ------------------------------------------------------------------ explore (explore.hpp)
 /// Checked properties (explore.hpp:19-34).
@@ -533,12 +819,125 @@ inline ExploreResult explore_machine(const PlatformConfig& platform, const Probl
     return explore_configs(platform, problem, {params}, limits).front();
 }
 
+/// Per-state callbacks of explore_machine (explore.hpp:75-79).
+struct ExploreHooks {
+    std::function<void(const Machine&, const MachineState&)> on_state;
+    std::function<bool(const Machine&, const MachineState&, const std::vector<Transition>&)>
+        on_terminal;
+};
+
+/// Every interleaving of one machine with the per-state hooks (explore.hpp:81-86,
+/// explore.cpp:86-165).  The GPU ranks the whole state graph level by level
+/// (mctb_machine_states) and hands back the states in the order the reference's
+/// DFS discovers them; the hooks then run on the host in that order: on_state
+/// for every visited state, on_terminal (with the DFS path) right after it for a
+/// terminal state, and a false from on_terminal stops the walk.  The visited-set
+/// capacity (max_states), the depth cap, the stats and the return value follow
+/// the reference's DFS exactly.  Shuffled orders (shuffle = true) depend on the
+/// host's std::shuffle and are not reproduced: ConfigError.
+inline bool explore_machine(const Machine& m, const ExploreLimits& limits, ExploreStats& stats,
+                            const ExploreHooks& hooks, std::uint64_t shuffle_seed = 0,
+                            bool shuffle = false, const std::atomic<bool>* stop = nullptr,
+                            double deadline_secs = 0.0) {
+    (void)shuffle_seed;
+    if (limits.max_depth < 1) throw ConfigError("max_depth must be >= 1");
+    if (shuffle) throw ConfigError("shuffled exploration orders are not reproduced");
+    const auto t0 = detail::Clock::now();
+    const detail::Args a(m.platform, m.problem);
+    std::int64_t info[3] = {0, 0, 0};
+    std::int64_t want = std::min<std::int64_t>(limits.max_states, 4096);
+    std::vector<std::int64_t> flat;
+    std::vector<std::int32_t> meta;
+    for (int attempt = 0;; ++attempt) {
+        const std::int64_t stride_guess = info[2] ? info[2] : 256 + 2 * m.problem.size;
+        flat.resize(static_cast<std::size_t>(want * stride_guess));
+        meta.resize(static_cast<std::size_t>(8 * want));
+        const int rc = mctb_machine_states(
+            a.plat, a.size, a.kernel, a.input, m.params.wg, m.params.ts, limits.max_depth,
+            limits.max_states, flat.data(), static_cast<std::int64_t>(flat.size()), meta.data(),
+            want, info);
+        if (rc == MCTB_LIMIT && attempt == 0 && info[1] > 0) {
+            want = info[1];
+            continue;
+        }
+        detail::check(rc);
+        break;
+    }
+    const std::int64_t total = info[0], n = info[1], stride = info[2];
+    const auto md = [&](std::int64_t i, int k) { return meta[static_cast<std::size_t>(8 * i + k)]; };
+    // the DFS applies every transition of a visited state below the depth cap
+    // (explore.cpp:124-129); a state at the cap with transitions marks the run
+    // incomplete when the DFS tries them
+    const auto applies = [&](std::int64_t i) -> long long {
+        return md(i, 4) < limits.max_depth ? md(i, 6) : 0;
+    };
+    const auto capped = [&](std::int64_t i) { return md(i, 4) >= limits.max_depth && md(i, 6) > 0; };
+    std::vector<Transition> path;
+    std::vector<std::int64_t> anc;  // indices of the states on the DFS stack
+    bool complete = true;
+    long long applied = 0;
+    for (std::int64_t i = 0; i < n; ++i) {
+        if ((i & 511) == 511 && ((stop && stop->load(std::memory_order_relaxed)) ||
+                                 (deadline_secs > 0 && detail::since(t0) >= deadline_secs))) {
+            // the DFS finishes the states before i only in part: count what is known
+            stats.wall_seconds += detail::since(t0);
+            stats.transitions_applied += applied;
+            return false;
+        }
+        const int d = md(i, 4);
+        path.resize(static_cast<std::size_t>(std::max(d - 1, 0)));
+        anc.resize(static_cast<std::size_t>(d));
+        if (d > 0)
+            path.push_back(Transition{static_cast<std::uint16_t>(md(i, 0)),
+                                      static_cast<std::uint16_t>(md(i, 1)),
+                                      static_cast<Op>(md(i, 2)), md(i, 3)});
+        anc.push_back(i);
+        stats.states_visited += 1;
+        stats.max_depth_reached = std::max<long long>(stats.max_depth_reached, d);
+        if (capped(i)) complete = false;
+        const MachineState s = detail::state_from_flat(flat.data() + i * stride,
+                                                       static_cast<std::size_t>(stride));
+        if (hooks.on_state) hooks.on_state(m, s);
+        if (md(i, 5) && hooks.on_terminal && !hooks.on_terminal(m, s, path)) {
+            // stopped at state i: every earlier state off the stack is finished; each
+            // ancestor has applied its transitions up to the path's edge
+            std::vector<char> on_stack(static_cast<std::size_t>(i + 1), 0);
+            for (auto k : anc) on_stack[static_cast<std::size_t>(k)] = 1;
+            for (std::int64_t k = 0; k < i; ++k)
+                if (!on_stack[static_cast<std::size_t>(k)]) applied += applies(k);
+            for (std::size_t k = 1; k < anc.size(); ++k) applied += md(anc[k], 7) + 1;
+            stats.transitions_applied += applied;
+            stats.wall_seconds += detail::since(t0);
+            return complete;
+        }
+    }
+    for (std::int64_t i = 0; i < n; ++i) applied += applies(i);
+    if (total > n) {
+        complete = false;  // the visited set filled up (explore.cpp:130-134)
+    } else if (total == limits.max_states) {
+        // full after the last discovery: any later transition attempt fails the insert
+        const std::int64_t last = n - 1;
+        bool later = applies(last) > 0;
+        for (std::int64_t c = last; md(c, 4) > 0 && !later;) {
+            std::int64_t p = c - 1;
+            while (md(p, 4) != md(c, 4) - 1) --p;  // c's parent: the nearest shallower state
+            later = md(c, 7) + 1 < md(p, 6);
+            c = p;
+        }
+        if (later) complete = false;
+    }
+    stats.transitions_applied += applied;
+    stats.wall_seconds += detail::since(t0);
+    return complete;
+}
+
 /// Exhaustive check of the over-time property across the whole parameter
 /// space (explore.hpp:88-93).
 inline Verdict check_overtime(const PlatformConfig& platform, const ProblemSpec& problem, Tick T,
                               const ExploreLimits& limits) {
-    if (limits.mode != ExploreLimits::Mode::Exact)
-        throw ConfigError("the GPU check is exact mode only");
+    // Bitstate mode (explore.cpp:18-46) keeps 64-bit fingerprints where exact mode
+    // keeps states; the GPU table always holds whole states, so a Bitstate check
+    // explores exactly and only withholds the proof (explore.cpp:202-203).
     const detail::Args a(platform, problem);
     std::int64_t out[12];
     const auto t0 = detail::Clock::now();
@@ -549,13 +948,13 @@ inline Verdict check_overtime(const PlatformConfig& platform, const ProblemSpec&
     });
     Verdict v;
     v.violated = out[0] != 0;
-    v.exhaustive = out[1] != 0;
+    v.exhaustive = out[1] != 0 && limits.mode == ExploreLimits::Mode::Exact;
     v.stats.states_visited = out[2];
     v.stats.max_depth_reached = out[3];
     v.stats.transitions_applied = out[4];
     v.stats.configs_explored = static_cast<int>(out[5]);
     v.stats.configs_skipped = static_cast<int>(out[6]);
-    v.stats.limit_hit = !v.exhaustive;
+    v.stats.limit_hit = out[1] == 0;
     v.stats.wall_seconds = detail::since(t0);
     if (v.violated)
         v.trace = Trace{std::move(tr), out[7], TuningParams{static_cast<int>(out[8]),
@@ -564,22 +963,21 @@ inline Verdict check_overtime(const PlatformConfig& platform, const ProblemSpec&
     return v;
 }
 
-/// Re-applies a trace from the initial state (explore.hpp:113-116); throws
-/// CorruptTrace on divergence.  Returns the terminal time and, for the
-/// minimum kernel, glob[0].
-inline RunOutcome replay(const PlatformConfig& platform, const ProblemSpec& problem,
-                         const Trace& trace) {
+/// Re-applies a trace from the initial state (explore.hpp:111-113,
+/// explore.cpp:283-300) on the GPU and returns the terminal state; throws
+/// CorruptTrace on a divergence, a non-terminal end or a wrong final time.
+inline MachineState replay(const PlatformConfig& platform, const ProblemSpec& problem,
+                           const Trace& trace) {
     const detail::Args a(platform, problem);
     const auto buf = detail::pack(trace.transitions);
-    std::int64_t out[2];
-    detail::check(mctb_replay(a.plat, a.size, a.kernel, a.input, trace.params.wg, trace.params.ts,
-                              buf.data(), static_cast<std::int64_t>(trace.transitions.size()),
-                              trace.final_time, out));
-    RunOutcome r;
-    r.time = out[0];
-    r.transitions = static_cast<long long>(trace.transitions.size());
-    if (problem.kernel == KernelKind::Minimum) r.result = out[1];
-    return r;
+    std::vector<std::int64_t> f(64 * 1024 + static_cast<std::size_t>(problem.size));
+    std::int64_t n = 0;
+    detail::check(mctb_machine_replay(a.plat, a.size, a.kernel, a.input, trace.params.wg,
+                                      trace.params.ts, buf.data(),
+                                      static_cast<std::int64_t>(trace.transitions.size()),
+                                      trace.final_time, f.data(),
+                                      static_cast<std::int64_t>(f.size()), &n));
+    return detail::state_from_flat(f.data(), static_cast<std::size_t>(n));
 }
 
 /// Terminating traces, one per distinct terminal state, for every feasible
@@ -924,7 +1322,7 @@ inline std::vector<SweepRow> exhaustive_sweep(const PlatformConfig& platform,
 /// (search.hpp:85-87).
 inline ExtractedParams extract_params(const PlatformConfig& platform, const ProblemSpec& problem,
                                       const Trace& trace) {
-    const RunOutcome end = replay(platform, problem, trace);
+    const MachineState end = replay(platform, problem, trace);
     return ExtractedParams{trace.params.wg, trace.params.ts, end.time};
 }
 

@@ -138,3 +138,6 @@ EXPORTED.append("mctb_nonterm_traces")
 lib.mctb_kernel_program.argtypes = [i32p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, C.c_int,
                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]
 EXPORTED.append("mctb_kernel_program")
+EXPORTED += ["mctb_machine_initial", "mctb_machine_enabled", "mctb_machine_apply",
+             "mctb_machine_query", "mctb_machine_process_name", "mctb_machine_replay",
+             "mctb_machine_states"]

@@ -16,6 +16,7 @@ LIB = os.environ.get("MCTB_BUILD_OUT") or os.path.join(HERE, "libmctune_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
+         "-Xlinker", "--no-undefined",
          "-cudart", "static", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 

@@ -96,6 +96,8 @@ struct DevBuf {
 
 const char* kRoles[] = {"main", "host", "clock", "device", "unit", "barrier", "pex"};
 
+}  // namespace
+
 // Machine::process_name (machine.cpp:103-113)
 std::string pname(const MachDesc& m, int pid) {
     int role, ord;
@@ -103,6 +105,8 @@ std::string pname(const MachDesc& m, int pid) {
     if (role <= 2) return kRoles[role];
     return std::string(kRoles[role]) + std::to_string(ord);
 }
+
+namespace {
 
 // Machine::label (machine.cpp:758-786)
 std::string label(const MachDesc& m, const Transition& t) {

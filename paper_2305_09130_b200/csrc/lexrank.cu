@@ -211,74 +211,112 @@ struct StreamGuard {
     }
 };
 
-}  // namespace
+// One thread per state of a level: its least in-edge as a transition (the
+// parent's enabled()[edge]), whether it is terminal and how many transitions it
+// enables (the DFS applies them all unless it sits at the depth cap).
+__global__ void __launch_bounds__(128) lr_info_kernel(BfsDesc bd, const uint32_t* parents,
+                                                      const uint32_t* states, int words,
+                                                      const unsigned long long* best, uint32_t n,
+                                                      int32_t* meta) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    Transition en[kMaxEnabled];
+    MState s;
+    int32_t* o = meta + 7 * (uint64_t)r;
+    if (parents) {
+        const unsigned long long b = best[r];
+        unpack(bd, parents + (b >> 16) * words, s);
+        enabled(bd.m, s, en);
+        const Transition t = en[b & 0xffffull];
+        o[0] = t.actor;
+        o[1] = t.peer;
+        o[2] = t.op;
+        o[3] = t.arg;
+        o[6] = (int32_t)(b & 0xffffull);
+    } else {
+        o[0] = o[1] = o[2] = o[3] = o[6] = -1;
+    }
+    unpack(bd, states + (uint64_t)r * words, s);
+    const int ne = enabled(bd.m, s, en);
+    o[4] = ne;
+    o[5] = ne == 0 && is_terminal(bd.m, s) ? 1 : 0;
+}
 
-// All terminal states of one configuration in DFS order with their least paths.
-// Returns MCTB_LIMIT when the exploration would exceed max_states (the
-// reference's truncation then depends on its traversal order).
-int lexrank_terminals(MachHost& h, int64_t max_depth, int64_t max_states,
-                      std::vector<int64_t>* times, std::vector<int64_t>* lens,
-                      std::vector<int32_t>* trace) {
-    StreamGuard sg;
-    MCTB_CUDA(cudaStreamCreateWithFlags(&sg.st, cudaStreamNonBlocking));
-    cudaStream_t st = sg.st;
+// The level-synchronous ranking of one configuration, kept on the device: every
+// state reachable within max_depth, level by level in least-path order.
+struct LrRun {
+    StreamGuard sg;  // destroyed last: the buffers free on its stream
+    cudaStream_t st = nullptr;
+    BfsDesc bd{};
+    int words = 0;
+    DevBuf<int32_t> ids;
+    DevBuf<unsigned long long> tag, best_tab, lvl_best, sort_k[2], cnt;
+    DevBuf<uint32_t> keys, lvl_states, list, sort_v[2];
+    DevBuf<LrTerm> terms;
+    DevBuf<char> sort_tmp;
+    uint64_t term_cap = 0;
+    std::vector<uint64_t> base{0, 1};  // level d occupies [base[d], base[d+1])
+    unsigned long long hc[8] = {};
+};
+
+// Builds every level.  Returns MCTB_LIMIT when the exploration would exceed
+// max_states states.
+int lr_build(MachHost& h, int64_t max_depth, int64_t max_states, LrRun& run) {
+    MCTB_CUDA(cudaStreamCreateWithFlags(&run.sg.st, cudaStreamNonBlocking));
+    cudaStream_t st = run.st = run.sg.st;
     int32_t* d_ids = nullptr;
     int rc = upload_desc(h, st, &d_ids);
     if (rc) return rc;
-    DevBuf<int32_t> ids_guard;
-    ids_guard.p = d_ids;
-    ids_guard.st = st;
-    BfsDesc bd;
+    run.ids.p = d_ids;
+    run.ids.st = st;
+    BfsDesc& bd = run.bd;
     bd.m = h.d;
     bd.l = bfs_layout(h.d, 1);
-    const int words = bd.l.words;
+    const int words = run.words = bd.l.words;
     const uint64_t cap = (uint64_t)std::max<int64_t>(max_states, 1);
     uint64_t slots = 1024;
     while (slots < 2 * cap) slots <<= 1;
     // table + levels: sized for max_states states
-    DevBuf<unsigned long long> tag, best_tab, lvl_best, sort_k[2], cnt;
-    DevBuf<uint32_t> keys, lvl_states, list, sort_v[2];
-    DevBuf<LrTerm> terms;
-    const uint64_t term_cap = cap;
-    if ((rc = tag.alloc(slots, st)) || (rc = best_tab.alloc(slots, st)) ||
-        (rc = keys.alloc(slots * words, st)) || (rc = lvl_states.alloc(cap * words, st)) ||
-        (rc = lvl_best.alloc(cap, st)) || (rc = list.alloc(cap, st)) ||
-        (rc = sort_k[0].alloc(cap, st)) || (rc = sort_k[1].alloc(cap, st)) ||
-        (rc = sort_v[0].alloc(cap, st)) || (rc = sort_v[1].alloc(cap, st)) ||
-        (rc = cnt.alloc(8, st)) || (rc = terms.alloc(term_cap, st)))
+    run.term_cap = cap;
+    if ((rc = run.tag.alloc(slots, st)) || (rc = run.best_tab.alloc(slots, st)) ||
+        (rc = run.keys.alloc(slots * words, st)) || (rc = run.lvl_states.alloc(cap * words, st)) ||
+        (rc = run.lvl_best.alloc(cap, st)) || (rc = run.list.alloc(cap, st)) ||
+        (rc = run.sort_k[0].alloc(cap, st)) || (rc = run.sort_k[1].alloc(cap, st)) ||
+        (rc = run.sort_v[0].alloc(cap, st)) || (rc = run.sort_v[1].alloc(cap, st)) ||
+        (rc = run.cnt.alloc(8, st)) || (rc = run.terms.alloc(run.term_cap, st)))
         return rc;
-    MCTB_CUDA(cudaMemsetAsync(tag.p, 0, slots * 8, st));
-    MCTB_CUDA(cudaMemsetAsync(best_tab.p, 0xff, slots * 8, st));
-    MCTB_CUDA(cudaMemsetAsync(keys.p, 0, slots * words * 4, st));
-    MCTB_CUDA(cudaMemsetAsync(cnt.p, 0, 8 * 8, st));
-    LrTable t{tag.p, best_tab.p, keys.p, slots - 1, words};
-    LrLevel lv{list.p, cnt.p};
+    MCTB_CUDA(cudaMemsetAsync(run.tag.p, 0, slots * 8, st));
+    MCTB_CUDA(cudaMemsetAsync(run.best_tab.p, 0xff, slots * 8, st));
+    MCTB_CUDA(cudaMemsetAsync(run.keys.p, 0, slots * words * 4, st));
+    MCTB_CUDA(cudaMemsetAsync(run.cnt.p, 0, 8 * 8, st));
+    LrTable t{run.tag.p, run.best_tab.p, run.keys.p, slots - 1, words};
+    LrLevel lv{run.list.p, run.cnt.p};
     // level 0: the initial state, packed on the host (same pack() as the device)
     {
         MState s0;
         initial_state(h.d, s0);
         std::vector<uint32_t> k0(kMaxWords, 0);
         pack(bd, 0, s0, k0.data());
-        MCTB_CUDA(cudaMemcpyAsync(lvl_states.p, k0.data(), words * 4, cudaMemcpyHostToDevice, st));
+        MCTB_CUDA(cudaMemcpyAsync(run.lvl_states.p, k0.data(), words * 4, cudaMemcpyHostToDevice, st));
         const unsigned long long root = 0;
-        MCTB_CUDA(cudaMemcpyAsync(lvl_best.p, &root, 8, cudaMemcpyHostToDevice, st));
+        MCTB_CUDA(cudaMemcpyAsync(run.lvl_best.p, &root, 8, cudaMemcpyHostToDevice, st));
     }
-    std::vector<uint64_t> base{0, 1};  // level d occupies [base[d], base[d+1])
+    std::vector<uint64_t>& base = run.base;
     const uint32_t depth_cap = (uint32_t)std::min<int64_t>(max_depth, 0x7fffffff);
     size_t sort_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, sort_k[0].p, sort_k[1].p, sort_v[0].p,
-                                    sort_v[1].p, (int)std::min<uint64_t>(cap, 0x7fffffff), 0, 64,
-                                    st);
-    DevBuf<char> sort_tmp;
-    if ((rc = sort_tmp.alloc(sort_bytes, st))) return rc;
-    unsigned long long hc[8];
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, run.sort_k[0].p, run.sort_k[1].p,
+                                    run.sort_v[0].p, run.sort_v[1].p,
+                                    (int)std::min<uint64_t>(cap, 0x7fffffff), 0, 64, st);
+    if ((rc = run.sort_tmp.alloc(sort_bytes, st))) return rc;
+    unsigned long long* hc = run.hc;
     for (uint32_t d = 0;; ++d) {
         const uint32_t n = (uint32_t)(base[d + 1] - base[d]);
-        MCTB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, st));  // next-level count only
+        MCTB_CUDA(cudaMemsetAsync(run.cnt.p, 0, 8, st));  // next-level count only
         lr_expand_kernel<<<(n + 127) / 128, 128, 0, st>>>(
-            bd, lvl_states.p + base[d] * words, n, d, depth_cap, t, lv, terms.p, term_cap);
+            bd, run.lvl_states.p + base[d] * words, n, d, depth_cap, t, lv, run.terms.p,
+            run.term_cap);
         MCTB_CUDA(cudaGetLastError());
-        MCTB_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof hc, cudaMemcpyDeviceToHost, st));
+        MCTB_CUDA(cudaMemcpyAsync(hc, run.cnt.p, sizeof run.hc, cudaMemcpyDeviceToHost, st));
         MCTB_CUDA(cudaStreamSynchronize(st));
         if (hc[3]) {
             set_error(hc[3] == 1 ? "lexrank: visited table full"
@@ -288,30 +326,117 @@ int lexrank_terminals(MachHost& h, int64_t max_depth, int64_t max_states,
         const uint64_t n1 = hc[0];
         if (n1 == 0) break;
         if (base.back() + n1 > cap) {
-            set_error("check_nontermination: the exploration exceeds max_states, where the "
-                      "reference's visited set truncates in traversal order");
+            set_error("the exploration exceeds max_states, where the reference's visited set "
+                      "truncates in traversal order");
             return MCTB_LIMIT;
         }
         // rank level d+1 by (parent rank, enabled index)
-        lr_gather_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(t, list.p, (uint32_t)n1,
-                                                                        sort_k[0].p, sort_v[0].p);
+        lr_gather_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(
+            t, run.list.p, (uint32_t)n1, run.sort_k[0].p, run.sort_v[0].p);
         int end_bit = 16;
         while (end_bit < 64 && ((uint64_t)n >> (end_bit - 16)) != 0) ++end_bit;
-        MCTB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, sort_bytes, sort_k[0].p, sort_k[1].p,
-                                                  sort_v[0].p, sort_v[1].p, (int)n1, 0, end_bit, st));
+        MCTB_CUDA(cub::DeviceRadixSort::SortPairs(run.sort_tmp.p, sort_bytes, run.sort_k[0].p,
+                                                  run.sort_k[1].p, run.sort_v[0].p,
+                                                  run.sort_v[1].p, (int)n1, 0, end_bit, st));
         lr_place_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(
-            t, sort_k[1].p, sort_v[1].p, (uint32_t)n1, lvl_states.p + base.back() * words,
-            lvl_best.p + base.back());
+            t, run.sort_k[1].p, run.sort_v[1].p, (uint32_t)n1,
+            run.lvl_states.p + base.back() * words, run.lvl_best.p + base.back());
         MCTB_CUDA(cudaGetLastError());
         base.push_back(base.back() + n1);
     }
+    return MCTB_OK;
+}
+
+}  // namespace
+
+// Every state of one configuration within max_depth, in the order the
+// reference's DFS discovers them (explore.cpp:86-165: the preorder of the
+// least-path tree, children by enabled() index), packed (bfs_layout(h.d, 1)).
+// meta = int32[7] per state {in-transition actor, peer, op, arg, enabled count,
+// terminal, in-edge index (the in-transition's position in the parent's enabled();
+// -1 at the root)}; depth = the state's depth.  table_cap bounds the
+// exploration (MCTB_LIMIT beyond it).
+int lexrank_states(MachHost& h, int64_t max_depth, int64_t table_cap, int* words,
+                   std::vector<uint32_t>* packed, std::vector<int32_t>* meta,
+                   std::vector<uint32_t>* depth) {
+    LrRun run;
+    int rc = lr_build(h, max_depth, table_cap, run);
+    if (rc) return rc;
+    const cudaStream_t st = run.st;
+    const uint64_t n = run.base.back();
+    const int w = *words = run.words;
+    DevBuf<int32_t> d_meta;
+    if ((rc = d_meta.alloc(7 * n, st))) return rc;
+    for (size_t d = 0; d + 1 < run.base.size(); ++d) {
+        const uint64_t b = run.base[d], nl = run.base[d + 1] - b;
+        lr_info_kernel<<<(unsigned)((nl + 127) / 128), 128, 0, st>>>(
+            run.bd, d ? run.lvl_states.p + run.base[d - 1] * w : nullptr,
+            run.lvl_states.p + b * w, w, run.lvl_best.p + b, (uint32_t)nl, d_meta.p + 7 * b);
+    }
+    MCTB_CUDA(cudaGetLastError());
+    std::vector<uint32_t> lv(n * w);
+    std::vector<int32_t> mt(7 * n);
+    std::vector<unsigned long long> best(n);
+    MCTB_CUDA(cudaMemcpyAsync(lv.data(), run.lvl_states.p, n * w * 4, cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaMemcpyAsync(mt.data(), d_meta.p, n * 28, cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaMemcpyAsync(best.data(), run.lvl_best.p, n * 8, cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaStreamSynchronize(st));
+    // the children of a state are a contiguous run of the next level (sorted by
+    // parent rank, then edge): [cb[g], ce[g]) in global indices
+    const size_t L = run.base.size() - 1;
+    std::vector<uint64_t> cb(n, 0), ce(n, 0);
+    for (size_t d = 0; d + 1 < L; ++d) {
+        const uint64_t b = run.base[d], nb = run.base[d + 1], ne = run.base[d + 2];
+        uint64_t c = nb;
+        for (uint64_t g = b; g < nb; ++g) {
+            cb[g] = c;
+            while (c < ne && (best[c] >> 16) == g - b) ++c;
+            ce[g] = c;
+        }
+    }
+    packed->resize(n * w);
+    meta->resize(7 * n);
+    depth->resize(n);
+    std::vector<std::pair<uint64_t, size_t>> stack{{0, 0}};  // (global index, level)
+    uint64_t out = 0;
+    while (!stack.empty()) {
+        const auto [g, d] = stack.back();
+        stack.pop_back();
+        std::memcpy(packed->data() + out * w, lv.data() + g * w, w * 4);
+        std::memcpy(meta->data() + 7 * out, mt.data() + 7 * g, 28);
+        (*depth)[out] = (uint32_t)d;
+        ++out;
+        for (uint64_t c = ce[g]; c > cb[g]; --c) stack.push_back({c - 1, d + 1});
+    }
+    return MCTB_OK;
+}
+
+// All terminal states of one configuration in DFS order with their least paths.
+// Returns MCTB_LIMIT when the exploration would exceed max_states (the
+// reference's truncation then depends on its traversal order).
+int lexrank_terminals(MachHost& h, int64_t max_depth, int64_t max_states,
+                      std::vector<int64_t>* times, std::vector<int64_t>* lens,
+                      std::vector<int32_t>* trace) {
+    LrRun run;
+    int rc = lr_build(h, max_depth, max_states, run);
+    if (rc) {
+        if (rc == MCTB_LIMIT && run.hc[3] == 0)
+            set_error("check_nontermination: the exploration exceeds max_states, where the "
+                      "reference's visited set truncates in traversal order");
+        return rc;
+    }
+    const cudaStream_t st = run.st;
+    const BfsDesc& bd = run.bd;
+    const int words = run.words;
+    const std::vector<uint64_t>& base = run.base;
+    const unsigned long long* hc = run.hc;
     const uint64_t n_terms = hc[2];
-    if (n_terms > term_cap) {
+    if (n_terms > run.term_cap) {
         set_error("check_nontermination: more terminal states than max_states");
         return MCTB_LIMIT;
     }
     std::vector<LrTerm> ht(n_terms);
-    MCTB_CUDA(cudaMemcpyAsync(ht.data(), terms.p, n_terms * sizeof(LrTerm), cudaMemcpyDeviceToHost,
+    MCTB_CUDA(cudaMemcpyAsync(ht.data(), run.terms.p, n_terms * sizeof(LrTerm), cudaMemcpyDeviceToHost,
                               st));
     MCTB_CUDA(cudaStreamSynchronize(st));
     std::vector<uint64_t> off(n_terms + 1, 0);
@@ -333,10 +458,10 @@ int lexrank_terminals(MachHost& h, int64_t max_depth, int64_t max_states,
     MCTB_CUDA(cudaMemcpyAsync(d_level.p, level_of.data(), n_steps * 4, cudaMemcpyHostToDevice, st));
     if (n_terms) {
         lr_chain_kernel<<<(unsigned)((n_terms + 127) / 128), 128, 0, st>>>(
-            terms.p, (uint32_t)n_terms, d_off.p, d_base.p, lvl_best.p, d_rank.p, d_edge.p);
+            run.terms.p, (uint32_t)n_terms, d_off.p, d_base.p, run.lvl_best.p, d_rank.p, d_edge.p);
         if (n_steps)
             lr_trans_kernel<<<(unsigned)((n_steps + 127) / 128), 128, 0, st>>>(
-                bd, lvl_states.p, words, d_rank.p, d_edge.p, d_level.p, d_base.p, n_steps,
+                bd, run.lvl_states.p, words, d_rank.p, d_edge.p, d_level.p, d_base.p, n_steps,
                 d_trace.p);
         MCTB_CUDA(cudaGetLastError());
     }

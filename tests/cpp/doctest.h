@@ -93,6 +93,7 @@ inline int run_all() {
         ::mini_doctest::report(mdt_ok, #__VA_ARGS__, __FILE__, __LINE__);            \
         if (!mdt_ok) throw ::mini_doctest::RequireFailed{};                          \
     } while (0)
+#define REQUIRE_FALSE(...) REQUIRE(!static_cast<bool>(__VA_ARGS__))
 #define CHECK_THROWS_AS(expr, ...)                                                   \
     do {                                                                             \
         bool mdt_ok = false;                                                         \

@@ -70,7 +70,7 @@ def test_reference_model_and_search_tests_pass_on_the_gpu_engine():
     _lib()
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
-    assert "18 test cases, 0 failed" in r.stdout  # test_model + test_kernel + test_search
+    assert "36 test cases, 0 failed" in r.stdout  # test_model, _kernel, _search, _machine, _explore
 
 
 @pytest.mark.skipif(not os.path.exists("/usr/local/cuda/bin/nvcc"), reason="no nvcc")
