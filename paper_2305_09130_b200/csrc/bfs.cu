@@ -1110,6 +1110,18 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
         // (pinned against explore_machine in tests/test_bfs_gpu.py); under the depth
         // cap the deepest visited states sit at max_depth
         o[3] = s.depth_cut ? max_depth : s.terminals ? proto[c] + s.max_time : -1;
+        if (s.capped) {
+            // a full visited set: the DFS's own prefix decides both (lexrank.cu), for
+            // graphs up to prefix_limit(cap) states
+            int64_t a = 0, md = 0;
+            rc = lexrank_prefix(hs[c], max_depth, cap, prefix_limit(cap), &a, &md);
+            if (rc == MCTB_OK) {
+                o[2] = a;
+                o[3] = md;
+            } else if (rc != MCTB_LIMIT) {
+                return rc;
+            }
+        }
         o[4] = s.terminals ? s.min_time : -1;
         o[5] = s.terminals ? s.max_time : -1;
         o[6] = (int64_t)s.terminals;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "pack.cuh"
@@ -58,6 +59,17 @@ uint64_t depth_bound(const MachDesc& m, int64_t protocol_steps);
 
 // The packed layout the exploration uses for a configuration among n_cfg.
 Layout bfs_layout(const MachDesc& m, int n_cfg);
+
+// The reference DFS's transitions_applied and max_depth_reached when its visited
+// set fills at cap states (lexrank.cu); MCTB_LIMIT when the state graph holds more
+// than `limit` states.
+int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
+                   int64_t* applies, int64_t* max_depth_reached);
+// The graph size up to which a capped sweep derives the DFS prefix's statistics:
+// 64x the cap, at least 2^22 and at most 2^27 states.
+inline uint64_t prefix_limit(uint64_t cap) {
+    return std::min<uint64_t>(std::max<uint64_t>(64 * cap, 1ull << 22), 1ull << 27);
+}
 
 // The reference DFS's counterexample for bound T (lexfirst.cu).
 // sibling_depths (optional): the depth of each abandoned sibling (its position on

@@ -65,6 +65,7 @@ struct Ctx {
     BfsResult bfs;
     std::vector<int64_t> first_time, first_steps;
     std::vector<Walk> walks;
+    std::vector<int64_t> pre_applies, pre_depth;  // the capped DFS's prefix (lexrank_prefix)
     double ms_cost = 0, ms_bfs = 0, ms_first = 0;
 };
 
@@ -109,6 +110,29 @@ int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
     }
     c.walks.push_back(std::move(w));
     *out = &c.walks.back();
+    return MCTB_OK;
+}
+
+// transitions_applied and max_depth_reached of configuration k's DFS when its
+// visited set fills (explore.cpp:26-30), for graphs up to prefix_limit(cap)
+// states; beyond, the sweep's edge count and the cap's depth stand in
+int ensure_prefix(Ctx& c, int k, int64_t* applies, int64_t* depth) {
+    if (c.pre_applies.size() != c.wg.size()) {
+        c.pre_applies.assign(c.wg.size(), -1);
+        c.pre_depth.assign(c.wg.size(), -1);
+    }
+    if (c.pre_applies[k] < 0) {
+        int rc = lexrank_prefix(c.hs[k], c.max_depth, c.cap, prefix_limit(c.cap),
+                                &c.pre_applies[k], &c.pre_depth[k]);
+        if (rc == MCTB_LIMIT) {
+            c.pre_applies[k] = (int64_t)c.bfs.stats[k].transitions;
+            c.pre_depth[k] = 0;
+        } else if (rc) {
+            return rc;
+        }
+    }
+    *applies = c.pre_applies[k];
+    *depth = c.pre_depth[k];
     return MCTB_OK;
 }
 
@@ -316,10 +340,21 @@ VerdictOut verdict(Ctx& c, int64_t T, int* rc_out) {
                 return v;
             }
             // the visited set filled before the satisfying terminal: the reference
-            // goes on to the next configuration with limit_hit (its transitions_applied
-            // here depends on its DFS order; the sweep's count stands in)
+            // goes on to the next configuration with limit_hit
+            int64_t pa = 0, pd = 0;
+            if ((*rc_out = ensure_prefix(c, k, &pa, &pd))) return v;
             v.states += (int64_t)c.cap;
-            v.transitions += (int64_t)b.transitions;
+            v.transitions += pa;
+            v.max_depth = std::max(v.max_depth, pd);
+            limit = true;
+            continue;
+        }
+        if (b.capped) {
+            int64_t pa = 0, pd = 0;
+            if ((*rc_out = ensure_prefix(c, k, &pa, &pd))) return v;
+            v.states += (int64_t)c.cap;
+            v.transitions += pa;
+            v.max_depth = std::max(v.max_depth, pd);
             limit = true;
             continue;
         }

@@ -411,6 +411,72 @@ int lexrank_states(MachHost& h, int64_t max_depth, int64_t table_cap, int* words
     return MCTB_OK;
 }
 
+__global__ void lr_ne_kernel(BfsDesc bd, const uint32_t* states, int words, uint64_t n,
+                             uint16_t* ne) {
+    const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    MState s;
+    unpack(bd, states + r * words, s);
+    Transition en[kMaxEnabled];
+    ne[r] = (uint16_t)enabled(bd.m, s, en);
+}
+
+// The reference DFS's statistics when its visited set fills at `cap` states
+// (explore.cpp:26-30, 124-138): the DFS then visits exactly the first cap
+// states of its discovery order (a full set stops only new states), applies
+// every transition of those below max_depth, and reaches their largest depth.
+// The order is the preorder of the least-path tree (lexrank_states), so the
+// whole graph within max_depth is ranked first: MCTB_LIMIT when it holds more
+// than `limit` states (the callers then keep their sweep's own counts).
+int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
+                   int64_t* applies, int64_t* max_depth_reached) {
+    int rc = MCTB_LIMIT;
+    for (uint64_t tc = std::min(limit, std::max<uint64_t>(2 * cap, 1ull << 16));;
+         tc = std::min(limit, tc * 8)) {
+        LrRun run;
+        rc = lr_build(h, max_depth, (int64_t)tc, run);
+        if (rc == MCTB_LIMIT && tc < limit) continue;
+        if (rc) return rc;
+        const cudaStream_t st = run.st;
+        const uint64_t n = run.base.back();
+        DevBuf<uint16_t> d_ne;
+        if ((rc = d_ne.alloc(n, st))) return rc;
+        lr_ne_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(run.bd, run.lvl_states.p,
+                                                                 run.words, n, d_ne.p);
+        MCTB_CUDA(cudaGetLastError());
+        std::vector<uint16_t> ne(n);
+        std::vector<unsigned long long> best(n);
+        MCTB_CUDA(cudaMemcpyAsync(ne.data(), d_ne.p, n * 2, cudaMemcpyDeviceToHost, st));
+        MCTB_CUDA(cudaMemcpyAsync(best.data(), run.lvl_best.p, n * 8, cudaMemcpyDeviceToHost, st));
+        MCTB_CUDA(cudaStreamSynchronize(st));
+        const size_t L = run.base.size() - 1;
+        std::vector<uint64_t> cb(n, 0), ce(n, 0);
+        for (size_t d = 0; d + 1 < L; ++d) {
+            const uint64_t b = run.base[d], nb = run.base[d + 1], e = run.base[d + 2];
+            uint64_t c = nb;
+            for (uint64_t g = b; g < nb; ++g) {
+                cb[g] = c;
+                while (c < e && (best[c] >> 16) == g - b) ++c;
+                ce[g] = c;
+            }
+        }
+        int64_t a = 0, md = 0;
+        uint64_t seen = 0;
+        std::vector<std::pair<uint64_t, size_t>> stack{{0, 0}};
+        while (!stack.empty() && seen < cap) {
+            const auto [g, d] = stack.back();
+            stack.pop_back();
+            ++seen;
+            if ((int64_t)d < max_depth) a += ne[g];
+            md = std::max<int64_t>(md, (int64_t)d);
+            for (uint64_t c = ce[g]; c > cb[g]; --c) stack.push_back({c - 1, d + 1});
+        }
+        *applies = a;
+        *max_depth_reached = md;
+        return MCTB_OK;
+    }
+}
+
 // All terminal states of one configuration in DFS order with their least paths.
 // Returns MCTB_LIMIT when the exploration would exceed max_states (the
 // reference's truncation then depends on its traversal order).

@@ -41,10 +41,10 @@ def test_random_explorations(engine, ref, seed):
         g = m.explore_machine(m.PlatformConfig(*plat), problem(m, size, kernel, inp), c,
                               max_states=states or 5_000_000, max_depth=depth or 4_000_000)
         key = (plat, size, kernel, c, depth, states)
-        assert (g.complete, g.states_visited) == (bool(x["complete"]), x["states"]), key
-        if x["states"] < (states or 5_000_000):  # the cap did not bind: order-independent
-            assert (g.transitions_applied, g.max_depth_reached, g.terminals) == (
-                x["transitions"], x["max_depth"], x["n_terminal"]), key
+        assert (g.complete, g.states_visited, g.transitions_applied, g.max_depth_reached) == (
+            bool(x["complete"]), x["states"], x["transitions"], x["max_depth"]), key
+        if x["states"] < (states or 5_000_000):  # the cap did not bind: every terminal met
+            assert g.terminals == x["n_terminal"], key
 
 
 @pytest.mark.parametrize("seed", range(16))
@@ -63,6 +63,8 @@ def test_random_checks(engine, ref, seed):
         key = (plat, size, kernel, T, depth, states)
         assert (v.violated, v.exhaustive, v.stats.states_visited) == (
             bool(r["violated"]), bool(r["exhaustive"]), r["states"]), key
+        assert (v.stats.transitions_applied, v.stats.max_depth_reached) == (
+            r["transitions"], r["max_depth"]), key
         if v.violated:
             assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
                 r["final_time"], r["wg"], r["ts"], r["steps"]), key

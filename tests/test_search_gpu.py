@@ -241,6 +241,8 @@ def test_visited_cap_matches_reference(engine, gold):
                              c["T"], max_states=c["max_states"])
         assert (v.violated, v.exhaustive, v.stats.states_visited) == (
             bool(c["violated"]), bool(c["exhaustive"]), c["states"]), key
+        assert (v.stats.transitions_applied, v.stats.max_depth_reached) == (
+            c["transitions"], c["max_depth"]), key
         if v.violated:
             assert (v.trace.final_time, v.trace.params.wg, v.trace.params.ts, v.trace.steps) == (
                 c["final_time"], c["wg"], c["ts"], c["steps"]), key
