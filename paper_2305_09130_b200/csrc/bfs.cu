@@ -84,6 +84,25 @@ namespace {
 #define MCTB_BFS_MAX_SLEEP 1024  // ns: longest back-off of an idle warp's queue poll
 #endif
 
+// Diagnostics build (-DMCTB_BFS_PHASES, with MCTB_BFS_OPHIST set): cycles per
+// phase of an expansion, for queue-popped and chained (kept) states separately.
+#ifdef MCTB_BFS_PHASES
+#define MCTB_PH(k)                                                                   \
+    do {                                                                             \
+        if (a.op_hist) {                                                             \
+            const long long ph_now = clock64();                                      \
+            if (lane == 0)                                                           \
+                atomicAdd(&ph_s[(ph_chain ? 8 : 0) + (k)],                           \
+                          (unsigned long long)(ph_now - ph_t));                      \
+            ph_t = ph_now;                                                           \
+        }                                                                            \
+    } while (0)
+#else
+#define MCTB_PH(k) \
+    do {           \
+    } while (0)
+#endif
+
 #ifndef MCTB_BFS_MINB
 #define MCTB_BFS_MINB 4  // resident blocks per SM the register allocation targets
 #endif
@@ -305,6 +324,12 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     __shared__ uint64_t hk[32];  // hash coefficients K_i
     extern __shared__ uint32_t dyn[];
     if (threadIdx.x < 32) hk[threadIdx.x] = hash_coef(threadIdx.x);
+#ifdef MCTB_BFS_PHASES
+    __shared__ unsigned long long ph_s[16];
+    if (threadIdx.x < 16) ph_s[threadIdx.x] = 0;
+    long long ph_t = clock64();
+    bool ph_chain = false;
+#endif
     // unpack_fields writes the time's low word only
     if ((threadIdx.x & 31) == 0) parent[threadIdx.x >> 5].time = 0;
     __syncthreads();
@@ -342,6 +367,11 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     uint32_t peek = kEmpty;  // lane j: entry h_run + j of the current run, as first read
     uint32_t dep = 0;        // depth of the parent (tracked under a depth cap only)
     for (;;) {
+#ifdef MCTB_BFS_PHASES
+        ph_chain = local;
+        if (a.op_hist && lane == 0) atomicAdd(&ph_s[(ph_chain ? 8 : 0) + 7], 1ull);
+        ph_t = clock64();
+#endif
         if (!local) {
             if (h_next == h_end) {
                 unsigned long long h0 = 0;
@@ -416,6 +446,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             }
             __syncwarp();
         }
+        MCTB_PH(0);  // pop: queue entry, slot line, parent hash
         const int cfg = peek_cfg(pwords, a.cfg_bits);
         if (cfg != cur_cfg) {
             flush();
@@ -435,8 +466,10 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
         const int lognwe = __ffs(d.m.nwe) - 1;
         // table-driven warp-parallel unpack, then one pass of the per-process rules
         // (bfs_rules.cuh) with a warp prefix sum placing every lane's transitions
+        MCTB_PH(1);  // configuration bookkeeping
         unpack_fields(a.ftab + (size_t)cfg * kMaxFields, a.nfields[cfg], pwords, s, lane);
         __syncwarp();
+        MCTB_PH(2);  // unpack
         const int nsl = n_slots(d.m);
         int ne = 0;
         for (int k0 = 0; k0 < nsl; k0 += 32) {
@@ -454,6 +487,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             ne += __shfl_sync(0xffffffffu, incl, 31);
         }
         __syncwarp();
+        MCTB_PH(3);  // enumeration
         BfsStats& st = a.stats[cfg];
         if (a.check_inv && lane == 0) {
             // machine.cpp:719-756, plus tick gating (acceptance criterion 7)
@@ -507,6 +541,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                 }
                 // reconverge the per-op paths before the shared hash / insert code
                 __syncwarp();
+                MCTB_PH(4);  // successor rows
                 if (ok) {
                     const uint64_t hh = fmix64(Hc);
                     if (a.n_parts > 1) owner = owner_of(hh, a.n_parts);
@@ -515,6 +550,10 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                     if (ins >= 0 && a.depth_cap)
                         st_relaxed32<SYS>(a.part[owner].depth + ins, (dep + 1) | kGuard);
                 }
+#ifdef MCTB_BFS_PHASES
+                __syncwarp();
+#endif
+                MCTB_PH(5);  // hash, probe, claim
                 bool fresh = ins >= 0;
                 int keeper = -1;
                 if (!kept && a.keep) {
@@ -541,6 +580,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             }
         }
         __syncwarp();
+        MCTB_PH(6);  // keep / push / copy
         local = kept && !g_err;
         if (local) {
             if (lane < SW - 2) pwords[lane] = kwords[lane];
@@ -552,6 +592,10 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
         }
     }
     flush();
+#ifdef MCTB_BFS_PHASES
+    __syncthreads();
+    if (a.op_hist && threadIdx.x < 16) atomicAdd(&a.op_hist[28 + threadIdx.x], ph_s[threadIdx.x]);
+#endif
 }
 
 template <int SW, bool SYS>
@@ -566,8 +610,8 @@ __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds,
     int cfg = c;
     if (seeds) {
         if (c >= n_seeds) return;
-        cfg = 0;
         for (int k = 0; k < a.words; ++k) key[k] = seeds[(size_t)c * a.words + k];
+        cfg = peek_cfg(key, a.cfg_bits);  // 0 for a single-configuration sweep
     } else {
         if (c >= a.n_cfg) return;
         const BfsDesc& d = a.descs[c];
@@ -592,6 +636,363 @@ __global__ void seed_kernel(BfsArgs a, const uint32_t* seeds, int n_seeds,
         return;
     }
     st_relaxed32<SYS>(&pt.queue[pos], (uint32_t)ins);
+}
+
+// ---------------------------------------------------------------------------
+// Narrow state graphs: one CTA per configuration, level by level in shared
+// memory.  The state graphs are graded (every path to a state has the same
+// length: tests/test_oracle.py), so a state can only equal states
+// of its own level: the visited set of a level-synchronous sweep is the next
+// level alone.  A configuration whose levels stay within kLvlWidth states (the
+// deep, narrow graphs of the tune sweeps: thousands to millions of levels of a
+// few states) runs here with no HBM table, queue or atomics: per level, each
+// warp expands its states exactly like explore_kernel (same unpack, rules and
+// successor code) and inserts the successors into a shared-memory hash table of
+// the next level.  A level that outgrows the table is handed to the global
+// sweep (explore_kernel) as its seeds, with the level's statistics rolled back.
+constexpr int kLvlThreads = 256;
+constexpr int kLvlWidth = 256;  // widest level a CTA holds
+constexpr int kLvlSlots = 512;  // hash slots per level (load <= 1/2)
+
+struct LevelArgs {
+    const BfsDesc* descs;
+    const uint2* ftab;
+    const int* nfields;
+    BfsStats* stats;
+    int words, cfg_bits, check_inv;
+    uint64_t cfg_cap;
+    uint32_t depth_cap;
+    uint32_t* frontier;  // [n_cfg][kLvlWidth * words]: a handed-off level
+    int64_t* fstat;      // [n_cfg][4]: {status (0 done, 1 handed off, 3 model bug), states, level}
+    int skip;            // count pure tick cycles instead of exploring them
+};
+
+// Inserts `row` (hash hh) into the level table; 1 new, 0 present, -1 full.
+__device__ int level_insert(uint32_t* tags, uint32_t* keys, uint16_t* list, unsigned* n_list,
+                            int words, const uint32_t* row, uint64_t hh, int* flags) {
+    const uint32_t tg = (uint32_t)(hh >> 32) | 1u;
+    uint32_t i = (uint32_t)hh & (kLvlSlots - 1);
+    for (int probe = 0; probe < kLvlSlots; ++probe, i = (i + 1) & (kLvlSlots - 1)) {
+        uint32_t t = *(volatile uint32_t*)&tags[i];
+        if (t == 0) {
+            t = atomicCAS(&tags[i], 0u, tg);
+            if (t == 0) {
+                uint32_t* k = keys + i * words;
+                for (int w = 0; w < words; ++w) k[w] = row[w];  // every word carries kGuard
+                const unsigned pos = atomicAdd(n_list, 1u);
+                if (pos < (unsigned)kLvlWidth) list[pos] = (uint16_t)i;
+                else atomicOr(flags, 4);
+                return 1;
+            }
+        }
+        if (t != tg) continue;
+        const volatile uint32_t* k = keys + i * words;
+        bool eq = true;
+        for (int w = 0; w < words; ++w) {
+            uint32_t v;
+            while (!((v = k[w]) & kGuard)) {  // the claimer is still writing the key
+            }
+            eq &= v == row[w];
+        }
+        if (eq) return 0;
+    }
+    atomicOr(flags, 4);
+    return -1;
+}
+
+#ifdef MCTB_BFS_PHASES
+#define MCTB_LPH(k)                                          \
+    do {                                                     \
+        const long long lph_now = clock64();                 \
+        if (threadIdx.x == 0) lph[k] += lph_now - lph_t;     \
+        lph_t = lph_now;                                     \
+    } while (0)
+#else
+#define MCTB_LPH(k) \
+    do {            \
+    } while (0)
+#endif
+
+template <int SW>
+__global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, cfg = blockIdx.x;
+#ifdef MCTB_BFS_PHASES
+    long long lph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long lph_t = clock64();
+#endif
+    const int words = a.words;
+    __shared__ BfsDesc d;
+    __shared__ MState parent[kLvlThreads / 32];
+    __shared__ Transition enabled_s[kLvlThreads / 32][kMaxEnabled];
+    __shared__ uint64_t hk[32];
+    __shared__ uint32_t tags[2][kLvlSlots];
+    __shared__ uint16_t list[2][kLvlWidth];
+    __shared__ unsigned n_list[2];
+    // the level's own statistics (committed when the level completes):
+    // new states, transitions, terminals, deadlocks, invariant violations
+    __shared__ unsigned long long lv[5];
+    __shared__ long long lv_min, lv_max;
+    __shared__ int lv_flags;  // 1 capped, 2 depth cut, 4 too wide, 8 model bug
+    __shared__ uint32_t lv_jump;  // levels counted by a cycle skip beyond the next
+    __shared__ unsigned long long tot_states;
+    extern __shared__ uint32_t dyn[];
+    uint32_t* keys0 = dyn;
+    uint32_t* keys1 = dyn + kLvlSlots * words;
+    uint32_t* pwords = dyn + 2 * kLvlSlots * words + wib * (34 * SW);
+    uint32_t* row = pwords + (2 + lane) * SW;
+    if (threadIdx.x < 32) hk[threadIdx.x] = hash_coef(threadIdx.x);
+    for (int i = threadIdx.x; i < (int)(sizeof(BfsDesc) / 4); i += kLvlThreads)
+        reinterpret_cast<uint32_t*>(&d)[i] = reinterpret_cast<const uint32_t*>(a.descs + cfg)[i];
+    for (int i = threadIdx.x; i < 2 * kLvlSlots; i += kLvlThreads) (&tags[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < 2 * kLvlSlots * words; i += kLvlThreads) dyn[i] = 0;
+    if (lane == 0) parent[wib].time = 0;  // unpack_fields writes the time's low word only
+    if (threadIdx.x == 0) {
+        n_list[0] = n_list[1] = 0;
+        lv_flags = 0;
+    }
+    __syncthreads();
+    MState& s = parent[wib];
+    Transition* en = enabled_s[wib];
+    MState t;
+    const int lognwe = __ffs(d.m.nwe) - 1;
+    const int nsl = n_slots(d.m);
+    const uint2* ftab = a.ftab + (size_t)cfg * kMaxFields;
+    const int nf = a.nfields[cfg];
+    // level 0: the initial state (explore.cpp:98-105)
+    if (wib == 0) {
+        if (lane == 0) {
+            MState s0;
+            initial_state(d.m, s0);
+            for (int k = 0; k < SW; ++k) row[k] = kGuard;
+            pack(d, cfg, s0, row);
+            uint64_t H0 = 0;
+            for (int k = 0; k < words; ++k) H0 += (uint64_t)row[k] * hk[k];
+            level_insert(tags[0], keys0, list[0], &n_list[0], words, row, fmix64(H0), &lv_flags);
+            tot_states = 1;
+        }
+    }
+    unsigned long long acc_trans = 0, acc_terms = 0, acc_dead = 0, acc_viol = 0;
+    long long acc_min = INT64_MAX, acc_max = -1;
+    int acc_flags = 0;
+    int status = 0;
+    unsigned handed = 0;
+    uint32_t level = 0;
+    for (int cur = 0;; cur ^= 1, ++level) {
+        const int nx = cur ^ 1;
+        uint32_t* kc = cur ? keys1 : keys0;
+        uint32_t* kn = cur ? keys0 : keys1;
+        __syncthreads();
+        MCTB_LPH(3);  // commit + loop top
+        const unsigned n = n_list[cur];
+        if (n == 0) break;
+        // clear the next level's table: the slots of two levels ago
+        const unsigned n_old = min(n_list[nx], (unsigned)kLvlWidth);
+        for (unsigned i = threadIdx.x; i < n_old * words; i += kLvlThreads)
+            kn[list[nx][i / words] * words + i % words] = 0;
+        for (unsigned i = threadIdx.x; i < n_old; i += kLvlThreads) tags[nx][list[nx][i]] = 0;
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < 5; ++k) lv[k] = 0;
+            lv_min = INT64_MAX;
+            lv_max = -1;
+            lv_flags = 0;
+            lv_jump = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) n_list[nx] = 0;
+        __syncthreads();
+        MCTB_LPH(0);  // clear + reset
+        for (unsigned i = wib; i < n; i += kLvlThreads / 32) {
+            if (*(volatile int*)&lv_flags & 12) break;  // the level is handed off anyway
+            const uint32_t* src = kc + list[cur][i] * words;
+            const uint32_t w = lane < words ? src[lane] : kGuard;
+            if (lane < SW - 2) pwords[lane] = w;
+            const uint64_t H = warp_sum64(lane < words ? (uint64_t)w * hk[lane] : 0ull);
+            __syncwarp();
+            unpack_fields(ftab, nf, pwords, s, lane);
+            __syncwarp();
+            MCTB_LPH(4);  // load + unpack
+            int ne = 0;
+            for (int k0 = 0; k0 < nsl; k0 += 32) {
+                Transition mine[2];
+                const int cnt = k0 + lane < nsl ? bfs_slot_rules(d.m, s, k0 + lane, lognwe, mine) : 0;
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int pos = ne + incl - cnt;
+                if (cnt > 0) en[pos] = mine[0];
+                if (cnt > 1) en[pos + 1] = mine[1];
+                ne += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            __syncwarp();
+            MCTB_LPH(5);  // enumeration
+#ifdef MCTB_BFS_PHASES
+            if (threadIdx.x == 0) lph[8] += 1;
+#endif
+            // Pure tick cycles.  When the level is this one state X, every launched
+            // element is busy and unreported (nrp_work = 0, ne = all_nwe reports)
+            // and nothing else is enabled, the next levels are fixed: the b = ne
+            // reports in every order (the 2^b subsets, machine.cpp:680-689: a report
+            // only sets its element's flag and nrp_work, which no rule but the tick
+            // reads), then the tick (machine.cpp:531-546), which decrements every
+            // element's busy_left and clears the flags.  While the least busy_left
+            // stays >= 2 after it, the tick leads to X with time + 1 and every
+            // busy_left - 1: the same structure again.  Graded graphs put nothing
+            // else on those levels, so c such cycles are counted, not explored:
+            // c * 2^b states and c * (b * 2^(b-1) + 1) transitions over c * (b + 1)
+            // levels, ending at the state X' they reach (inserted for the next level).
+            if (n == 1 && a.skip && !a.check_inv) {
+                long long cyc = 0;
+                if (lane == 0 && ne >= 1 && ne <= 16 && ne == s.all_nwe && s.nrp_work == 0 &&
+                    (a.depth_cap == 0 || level < a.depth_cap)) {
+                    int mb = 0x7fffffff;
+                    bool pure = true;
+                    for (int e = 0; e < ne; ++e) {
+                        if (en[e].op != OP_PEXREPORT) {
+                            pure = false;
+                            break;
+                        }
+                        mb = min(mb, (int)s.pex[en[e].actor].busy_left);
+                    }
+                    if (pure && mb >= 2) {
+                        cyc = mb - 1;
+                        // every counted level below the depth cap (its states are
+                        // all expanded), and room under the visited cap
+                        if (a.depth_cap) cyc = min(cyc, (long long)(a.depth_cap - level) / (ne + 1));
+                        const unsigned long long cap = a.cfg_cap, tot = tot_states;
+                        const unsigned long long r = cap - (tot < cap ? tot : cap);
+                        const long long room = r > (1ull << 62) ? (1ll << 62) : (long long)r;
+                        cyc = min(cyc, room / (1ll << ne) - 1);
+                    }
+                }
+                cyc = __shfl_sync(0xffffffffu, cyc, 0);
+                if (cyc > 0) {
+                    if (lane == 0) {
+                        s.time += cyc;
+                        for (int e = 0; e < ne; ++e) s.pex[en[e].actor].busy_left -= (uint16_t)cyc;
+                        for (int k = 0; k < SW; ++k) row[k] = kGuard;
+                        pack(d, cfg, s, row);
+                        uint64_t Hx = 0;
+                        for (int k = 0; k < words; ++k) Hx += (uint64_t)row[k] * hk[k];
+                        level_insert(tags[nx], kn, list[nx], &n_list[nx], words, row, fmix64(Hx),
+                                     &lv_flags);
+                        lv[0] += (unsigned long long)cyc << ne;
+                        lv[1] += (unsigned long long)cyc * (((unsigned long long)ne << (ne - 1)) + 1);
+                        lv_jump = (uint32_t)(cyc * (ne + 1) - 1);
+                    }
+                    __syncwarp();
+                    continue;
+                }
+            }
+            if (a.check_inv && lane == 0) {
+                bool bad = check_invariants(d.m, s) != 0;
+                for (int e = 0; e < ne; ++e)
+                    bad |= en[e].op == OP_CLOCKTICK && (s.nrp_work != s.all_nwe || s.all_nwe == 0);
+                if (bad) atomicAdd(&lv[4], 1ull);
+            }
+            if (ne == 0) {
+                if (lane == 0) {
+                    if (is_terminal(d.m, s)) {
+                        atomicAdd(&lv[2], 1ull);
+                        atomicMin(&lv_min, (long long)s.time);
+                        atomicMax(&lv_max, (long long)s.time);
+                    } else {
+                        atomicAdd(&lv[3], 1ull);
+                        atomicOr(&lv_flags, 8);
+                    }
+                }
+            } else if (tot_states + *(volatile unsigned long long*)&lv[0] >= a.cfg_cap) {
+                if (lane == 0) atomicOr(&lv_flags, 1);  // explore.cpp:28
+            } else if (a.depth_cap && level >= a.depth_cap) {
+                if (lane == 0) atomicOr(&lv_flags, 2);  // explore.cpp:124-127
+            } else {
+                if (lane == 0) atomicAdd(&lv[1], (unsigned long long)ne);
+                for (int base = 0; base < ne; base += 32) {
+                    const int e = base + lane;
+                    uint64_t Hc = H;
+                    bool ok = false;
+                    if (e < ne) {
+                        copy_key<SW>(row, pwords);
+                        ok = true;
+                        if (!fast_successor(d, s, en[e], row, hk, Hc)) {
+                            copy_state(d.m, t, s);
+                            ok = apply(d.m, t, to_pid(d.m, en[e]));
+                            if (ok) {
+                                pack(d, cfg, t, row);
+                                Hc = 0;
+                                for (int k = 0; k < words; ++k) Hc += (uint64_t)row[k] * hk[k];
+                            } else {
+                                atomicOr(&lv_flags, 8);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    MCTB_LPH(6);  // successor rows
+                    int r = 0;
+                    if (ok) r = level_insert(tags[nx], kn, list[nx], &n_list[nx], words, row,
+                                             fmix64(Hc), &lv_flags);
+                    const unsigned nn = __popc(__ballot_sync(0xffffffffu, r == 1));
+                    if (lane == 0 && nn) atomicAdd(&lv[0], (unsigned long long)nn);
+                    MCTB_LPH(7);  // insert
+                }
+            }
+            __syncwarp();
+        }
+        MCTB_LPH(1);  // warp 0's other work
+        __syncthreads();
+        MCTB_LPH(2);  // waiting for the level's other warps
+        if (lv_flags & 8) {
+            status = 3;
+            break;
+        }
+        if (lv_flags & 4) {
+            // too wide: this level goes to the global sweep, unexpanded
+            for (unsigned i = threadIdx.x; i < n * words; i += kLvlThreads)
+                a.frontier[(size_t)cfg * kLvlWidth * words + i] = kc[list[cur][i / words] * words + i % words];
+            status = 1;
+            handed = n;
+            break;
+        }
+        if (threadIdx.x == 0) tot_states += lv[0];
+        level += lv_jump;
+        acc_trans += lv[1];
+        acc_terms += lv[2];
+        acc_dead += lv[3];
+        acc_viol += lv[4];
+        acc_min = min(acc_min, lv_min);
+        acc_max = max(acc_max, lv_max);
+        acc_flags |= lv_flags;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        BfsStats& st = a.stats[cfg];
+        // the global sweep counts a handed-off level again as its seeds
+        st.states = tot_states - handed;
+        st.transitions = acc_trans;
+        st.terminals = acc_terms;
+        st.min_time = acc_min;
+        st.max_time = acc_max;
+        st.deadlocks = acc_dead;
+        st.capped = (acc_flags & 1) ? 1 : 0;
+        st.violations = acc_viol;
+        st.depth_cut = (acc_flags & 2) ? 1 : 0;
+        int64_t* fs = a.fstat + 4 * cfg;
+        fs[0] = status;
+        fs[1] = handed;
+        fs[2] = level;
+#ifdef MCTB_BFS_PHASES
+        if (level > 100000) {
+            printf("[level] cfg %d levels %u warp0 expansions %lld cycles per level: clear %.0f "
+                   "other %.0f wait %.0f commit %.0f | per warp-0 expansion: unpack %.0f enum %.0f "
+                   "rows %.0f insert %.0f\n",
+                   cfg, level, lph[8], (double)lph[0] / level, (double)lph[1] / level,
+                   (double)lph[2] / level, (double)lph[3] / level, (double)lph[4] / lph[8],
+                   (double)lph[5] / lph[8], (double)lph[6] / lph[8], (double)lph[7] / lph[8]);
+        }
+#endif
+    }
 }
 
 }  // namespace
@@ -855,6 +1256,79 @@ struct AsyncFree {
     }
 };
 
+// The narrow-graph pass (level_kernel): one CTA per configuration.  Returns the
+// statistics of the levels it completed and, for every configuration that
+// outgrew it, the level handed to the global sweep (keys and depths).
+struct LevelPass {
+    std::vector<BfsStats> stats;
+    std::vector<uint32_t> seeds, seed_depths;
+    int handed = 0;   // configurations handed off
+    int error = 0;    // 3: model bug (deadlock or inapplicable transition)
+    double ms = 0;
+};
+
+static int level_pass(const BfsPlan& pl, uint64_t cfg_cap, uint32_t depth_cap, bool check_inv,
+                      cudaStream_t st, LevelPass* out) {
+    const int n_cfg = pl.n_cfg, words = pl.words;
+    char* blk = nullptr;
+    const size_t sb = (shared_bytes(pl) + 255) & ~(size_t)255;
+    const size_t fb = (size_t)n_cfg * kLvlWidth * words * 4;
+    MCTB_CUDA(cudaMallocAsync(&blk, sb + fb + (size_t)n_cfg * 32, st));
+    const AsyncFree guard{blk, st};
+    BfsArgs ba{};
+    int rc = shared_init(pl, blk, &ba, st);
+    if (rc) return rc;
+    LevelArgs la{};
+    la.descs = ba.descs;
+    la.ftab = ba.ftab;
+    la.nfields = ba.nfields;
+    la.stats = ba.stats;
+    la.words = words;
+    la.cfg_bits = ba.cfg_bits;
+    la.check_inv = check_inv ? 1 : 0;
+    la.cfg_cap = cfg_cap;
+    la.depth_cap = depth_cap;
+    la.frontier = (uint32_t*)(blk + sb);
+    la.fstat = (int64_t*)(blk + sb + fb);
+    la.skip = getenv("MCTB_BFS_NOSKIP") ? 0 : 1;
+    const size_t dyn = (2 * (size_t)kLvlSlots * words + (kLvlThreads / 32) * 34 * (size_t)pl.sw) * 4;
+    auto kern = pl.sw == 16 ? level_kernel<16> : level_kernel<32>;
+    MCTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    cudaEvent_t e0, e1;
+    MCTB_CUDA(cudaEventCreate(&e0));
+    MCTB_CUDA(cudaEventCreate(&e1));
+    cudaEventRecord(e0, st);
+    kern<<<n_cfg, kLvlThreads, dyn, st>>>(la);
+    cudaEventRecord(e1, st);
+    MCTB_CUDA(cudaGetLastError());
+    out->stats.resize(n_cfg);
+    std::vector<int64_t> fs(4 * (size_t)n_cfg);
+    MCTB_CUDA(cudaMemcpyAsync(out->stats.data(), ba.stats, sizeof(BfsStats) * n_cfg,
+                              cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaMemcpyAsync(fs.data(), la.fstat, fs.size() * 8, cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    out->ms = ms;
+    out->handed = 0;
+    out->error = 0;
+    for (int c = 0; c < n_cfg; ++c) {
+        if (fs[4 * c] == 3) out->error = 3;
+        if (fs[4 * c] != 1) continue;
+        const size_t n = (size_t)fs[4 * c + 1];
+        const size_t o = out->seeds.size();
+        out->seeds.resize(o + n * words);
+        MCTB_CUDA(cudaMemcpyAsync(out->seeds.data() + o, la.frontier + (size_t)c * kLvlWidth * words,
+                                  n * words * 4, cudaMemcpyDeviceToHost, st));
+        out->seed_depths.insert(out->seed_depths.end(), n, (uint32_t)fs[4 * c + 2]);
+        ++out->handed;
+    }
+    MCTB_CUDA(cudaStreamSynchronize(st));
+    return MCTB_OK;
+}
+
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds, int n_parts,
             bool sys_scope, uint64_t first_cap, uint32_t depth_cap,
@@ -902,6 +1376,33 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
     }
     cap = std::min(cap, cap_limit);
     const bool trace = getenv("MCTB_BFS_TRACE") != nullptr;
+    // narrow graphs first, level by level in shared memory (level_kernel); the
+    // configurations that outgrow it continue in the global sweep from the level
+    // they reached
+    LevelPass lp;
+    const bool use_level = !seeds && n_parts == 1 && !sys_scope && !getenv("MCTB_BFS_NOLEVEL");
+    if (use_level) {
+        if ((rc = level_pass(pl, cfg_cap, depth_cap, check_invariants, st, &lp))) return rc;
+        if (trace)
+            fprintf(stderr, "[bfs] level pass: %.3f ms, %d of %d configurations handed off\n",
+                    lp.ms, lp.handed, n_cfg);
+        if (lp.error || lp.handed == 0) {
+            res->stats = lp.stats;
+            res->states = 0;
+            for (auto& x : res->stats) {
+                if (x.states >= cfg_cap) x.capped = 1;
+                res->states += x.states;
+            }
+            res->ms = lp.ms;
+            res->levels = 0;
+            res->error = lp.error;
+            res->words = pl.words;
+            res->capacity = 0;
+            return MCTB_OK;
+        }
+        seeds = &lp.seeds;
+        seed_depths = &lp.seed_depths;
+    }
     for (;;) {
         BfsArgs a{};
         a.cap_mask = cap - 1;
@@ -929,6 +1430,9 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
             if ((rc = part_clear(b + pb * p, cap, sw, st, dep))) return rc;
         }
         if ((rc = shared_init(pl, b + pb * n_parts, &a, st))) return rc;
+        if (use_level)  // the narrow pass's counts; the global sweep adds its own
+            MCTB_CUDA(cudaMemcpyAsync(a.stats, lp.stats.data(), sizeof(BfsStats) * n_cfg,
+                                      cudaMemcpyHostToDevice, st));
         if ((rc = seed_launch(pl, a, sys_scope, seeds, st, seed_depths))) return rc;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
@@ -947,15 +1451,15 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         for (int p = 0; p < n_parts; ++p)
             MCTB_CUDA(cudaMemcpyAsync(misc_h.data() + 32 * p, b + pb * p + misc_off, 256,
                                       cudaMemcpyDeviceToHost, st));
-        unsigned long long hist[32] = {};
+        unsigned long long hist[64] = {};
         if (a.op_hist)
-            MCTB_CUDA(cudaMemcpyAsync(hist, b + pb * n_parts, 256, cudaMemcpyDeviceToHost, st));
+            MCTB_CUDA(cudaMemcpyAsync(hist, b + pb * n_parts, 512, cudaMemcpyDeviceToHost, st));
         MCTB_CUDA(cudaStreamSynchronize(st));
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        res->ms = ms;
+        res->ms = ms + lp.ms;
         res->states = 0;
         for (const auto& x : res->stats) res->states += x.states;
         res->levels = 0;
@@ -987,6 +1491,17 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
             for (int o = 0; o < 19; ++o)
                 if (hist[4 + o]) fprintf(stderr, " op%d=%llu", o, hist[4 + o]);
             fprintf(stderr, "\n");
+#ifdef MCTB_BFS_PHASES
+            static const char* names[7] = {"pop", "cfg", "unpack", "enum", "rows", "insert", "keep"};
+            for (int c = 0; c < 2; ++c) {
+                const unsigned long long* ph = hist + 32 + 8 * c;
+                fprintf(stderr, "[explore] %s expansions %llu, cycles each:",
+                        c ? "chained" : "popped", ph[7]);
+                for (int k = 0; k < 7; ++k)
+                    fprintf(stderr, " %s=%.0f", names[k], ph[7] ? (double)ph[k] / ph[7] : 0.0);
+                fprintf(stderr, "\n");
+            }
+#endif
         }
         res->words = pl.words;
         res->capacity = cap * n_parts;
@@ -1074,7 +1589,7 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
     const int n_parts = std::max(1, (flags >> 8) & 15);
     // protocol transitions of every run (steps - time of the cost model): a terminal
     // state of time t sits at depth protocol + t
-    std::vector<int64_t> proto(n_configs);
+    std::vector<int64_t> proto(n_configs), cm_time(n_configs);
     uint32_t depth_cap = 0;
     for (int c = 0; c < n_configs; ++c) {
         int logn = 0, lw = 0, lt = 0, lp = 0;
@@ -1084,6 +1599,7 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
         while ((1 << lp) < plat[2]) ++lp;
         const Cost cm = lockstep_cost(kernel, logn, plat[3], Config{plat[0], plat[1], lp, lw, lt});
         proto[c] = cm.steps - cm.time;
+        cm_time[c] = cm.time;
         if (depth_bound(hs[c].d, proto[c]) > (uint64_t)max_depth)
             depth_cap = (uint32_t)std::min<int64_t>(max_depth, 0x7fffffff);
     }
@@ -1114,7 +1630,8 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
             // a full visited set: the DFS's own prefix decides both (lexrank.cu), for
             // graphs up to prefix_limit(cap) states
             int64_t a = 0, md = 0;
-            rc = lexrank_prefix(hs[c], max_depth, cap, prefix_limit(cap), &a, &md);
+            rc = lexrank_prefix(hs[c], max_depth, cap, prefix_limit(cap), proto[c] + cm_time[c],
+                                &a, &md);
             if (rc == MCTB_OK) {
                 o[2] = a;
                 o[3] = md;

@@ -62,11 +62,12 @@ Layout bfs_layout(const MachDesc& m, int n_cfg);
 
 // The reference DFS's transitions_applied and max_depth_reached when its visited
 // set fills at cap states (lexrank.cu); MCTB_LIMIT when the state graph holds more
-// than `limit` states.
+// than `limit` states or its runs (run_len transitions, the lock-step run) are
+// 16,384 transitions or longer.
 int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
-                   int64_t* applies, int64_t* max_depth_reached);
+                   int64_t run_len, int64_t* applies, int64_t* max_depth_reached);
 // The graph size up to which a capped sweep derives the DFS prefix's statistics:
-// 64x the cap, at least 2^22 and at most 2^27 states.
+// 64x the cap, at least 2^22 and at most 2^27 states (and at most 16,384 levels).
 inline uint64_t prefix_limit(uint64_t cap) {
     return std::min<uint64_t>(std::max<uint64_t>(64 * cap, 1ull << 22), 1ull << 27);
 }

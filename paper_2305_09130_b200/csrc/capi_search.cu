@@ -66,7 +66,7 @@ struct Ctx {
     std::vector<int64_t> first_time, first_steps;
     std::vector<Walk> walks;
     std::vector<int64_t> pre_applies, pre_depth;  // the capped DFS's prefix (lexrank_prefix)
-    double ms_cost = 0, ms_bfs = 0, ms_first = 0;
+    double ms_cost = 0, ms_bfs = 0, ms_first = 0, ms_prefix = 0;
 };
 
 int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
@@ -113,6 +113,12 @@ int ensure_walk(Ctx& c, int k, int64_t T, const Walk** out) {
     return MCTB_OK;
 }
 
+double now_ms() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return t.tv_sec * 1e3 + t.tv_nsec * 1e-6;
+}
+
 // transitions_applied and max_depth_reached of configuration k's DFS when its
 // visited set fills (explore.cpp:26-30), for graphs up to prefix_limit(cap)
 // states; beyond, the sweep's edge count and the cap's depth stand in
@@ -122,8 +128,10 @@ int ensure_prefix(Ctx& c, int k, int64_t* applies, int64_t* depth) {
         c.pre_depth.assign(c.wg.size(), -1);
     }
     if (c.pre_applies[k] < 0) {
-        int rc = lexrank_prefix(c.hs[k], c.max_depth, c.cap, prefix_limit(c.cap),
+        const double t0 = now_ms();
+        int rc = lexrank_prefix(c.hs[k], c.max_depth, c.cap, prefix_limit(c.cap), c.cm_steps[k],
                                 &c.pre_applies[k], &c.pre_depth[k]);
+        c.ms_prefix += now_ms() - t0;
         if (rc == MCTB_LIMIT) {
             c.pre_applies[k] = (int64_t)c.bfs.stats[k].transitions;
             c.pre_depth[k] = 0;
@@ -144,11 +152,6 @@ struct VerdictOut {
     const std::vector<int32_t>* path = nullptr;  // guided-walk counterexample, if any
 };
 
-double now_ms() {
-    timespec t;
-    clock_gettime(CLOCK_MONOTONIC, &t);
-    return t.tv_sec * 1e3 + t.tv_nsec * 1e-6;
-}
 
 int prepare(Ctx& c, int64_t max_states, int64_t max_depth) {
     int rc = check_platform(c.plat);
@@ -254,8 +257,21 @@ int prepare(Ctx& c, int64_t max_states, int64_t max_depth) {
 }
 
 // The first path of explore_machine's DFS for configuration k (GPU run, en[0] policy).
+// Every run of a lock-step configuration (one device, or no device serving two
+// batches) ends at the cost model's time after the same number of transitions
+// (the reference's own test_machine.cpp checks seeded runs against it).
+bool lockstep(const Ctx& c, int k) {
+    const MachDesc& d = c.hs[k].d;
+    return d.nwd == 1 || (int64_t)d.wgs <= (int64_t)c.plat[0] * c.plat[1];
+}
+
 int ensure_first(Ctx& c, int k) {
     if (c.first_time[k] >= 0) return MCTB_OK;
+    if (lockstep(c, k)) {
+        c.first_time[k] = c.cm_time[k];
+        c.first_steps[k] = c.cm_steps[k];
+        return MCTB_OK;
+    }
     const BfsStats& b = c.bfs.stats[k];
     if (!b.capped && !b.depth_cut && b.terminals > 0 && b.min_time == b.max_time) {
         // every run of this configuration was explored and ends at one time, so
@@ -471,6 +487,8 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
             // one time, so the seeded run ends there too: no serial simulation
             // (a lone GPU thread steps ~2 us per transition; 124 ms at size 128)
             t_hi = b.min_time;
+        } else if (lockstep(c, k)) {
+            t_hi = c.cm_time[k];  // every run ends at the lock-step time
         } else {
             TrajOut o;
             if ((rc = gpu_run(c.hs[k], MCTB_POLICY_MT19937, seed, 0, 200000000LL, &o, nullptr, 0)))
@@ -549,8 +567,9 @@ int mctb_tune(const int* plat, int size, int kernel, const int64_t* input, int64
     const double tp3 = now_ms();
     rc = emit_trace(c, best, trace, cap, trace_len);
     if (tt)
-        fprintf(stderr, "[tune] prepare %.2f (cost %.2f, bfs %.2f) estimate %.2f bisect %.2f (first %.2f) trace %.2f ms\n",
-                tp1 - tp0, c.ms_cost, c.ms_bfs, tp2 - tp1, tp3 - tp2, c.ms_first, now_ms() - tp3);
+        fprintf(stderr, "[tune] prepare %.2f (cost %.2f, bfs %.2f) estimate %.2f bisect %.2f (first %.2f, capped prefixes %.2f) trace %.2f ms\n",
+                tp1 - tp0, c.ms_cost, c.ms_bfs, tp2 - tp1, tp3 - tp2, c.ms_first, c.ms_prefix,
+                now_ms() - tp3);
     return rc;
 }
 

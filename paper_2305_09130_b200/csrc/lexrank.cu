@@ -261,7 +261,8 @@ struct LrRun {
 
 // Builds every level.  Returns MCTB_LIMIT when the exploration would exceed
 // max_states states.
-int lr_build(MachHost& h, int64_t max_depth, int64_t max_states, LrRun& run) {
+int lr_build(MachHost& h, int64_t max_depth, int64_t max_states, LrRun& run,
+             uint64_t max_levels = UINT64_MAX) {
     MCTB_CUDA(cudaStreamCreateWithFlags(&run.sg.st, cudaStreamNonBlocking));
     cudaStream_t st = run.st = run.sg.st;
     int32_t* d_ids = nullptr;
@@ -325,6 +326,10 @@ int lr_build(MachHost& h, int64_t max_depth, int64_t max_states, LrRun& run) {
         }
         const uint64_t n1 = hc[0];
         if (n1 == 0) break;
+        if (base.size() > max_levels) {
+            set_error("the state graph is deeper than the ranking's level bound");
+            return MCTB_LIMIT;
+        }
         if (base.back() + n1 > cap) {
             set_error("the exploration exceeds max_states, where the reference's visited set "
                       "truncates in traversal order");
@@ -429,12 +434,20 @@ __global__ void lr_ne_kernel(BfsDesc bd, const uint32_t* states, int words, uint
 // whole graph within max_depth is ranked first: MCTB_LIMIT when it holds more
 // than `limit` states (the callers then keep their sweep's own counts).
 int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
-                   int64_t* applies, int64_t* max_depth_reached) {
+                   int64_t run_len, int64_t* applies, int64_t* max_depth_reached) {
     int rc = MCTB_LIMIT;
+    // one host round trip per level: deep graphs (the tune sweeps' chains of
+    // 1e5-1e6 levels) keep their sweep's counts instead
+    constexpr uint64_t kMaxLevels = 16384;
+    if ((uint64_t)std::min<int64_t>(run_len, max_depth) >= kMaxLevels) {
+        set_error("the state graph is deeper than the ranking's level bound");
+        return MCTB_LIMIT;
+    }
     for (uint64_t tc = std::min(limit, std::max<uint64_t>(2 * cap, 1ull << 16));;
          tc = std::min(limit, tc * 8)) {
         LrRun run;
-        rc = lr_build(h, max_depth, (int64_t)tc, run);
+        rc = lr_build(h, max_depth, (int64_t)tc, run, kMaxLevels);
+        if (rc == MCTB_LIMIT && run.base.size() > kMaxLevels) return rc;
         if (rc == MCTB_LIMIT && tc < limit) continue;
         if (rc) return rc;
         const cudaStream_t st = run.st;
