@@ -734,6 +734,12 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
     __shared__ long long lv_min, lv_max;
     __shared__ int lv_flags;  // 1 capped, 2 depth cut, 4 too wide, 8 model bug
     __shared__ uint32_t lv_jump;  // levels counted by a cycle skip beyond the next
+    // the last rep-start state (abstract kernel), for the rep skip below
+    __shared__ uint32_t rep_key[kMaxWords];
+    __shared__ int rep_valid;
+    __shared__ uint32_t rep_level;
+    __shared__ unsigned long long rep_states, rep_trans, rep_events;
+    __shared__ long long rep_time;
     __shared__ unsigned long long tot_states;
     extern __shared__ uint32_t dyn[];
     uint32_t* keys0 = dyn;
@@ -749,6 +755,7 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
     if (threadIdx.x == 0) {
         n_list[0] = n_list[1] = 0;
         lv_flags = 0;
+        rep_valid = 0;
     }
     __syncthreads();
     MState& s = parent[wib];
@@ -843,6 +850,94 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
             // else on those levels, so c such cycles are counted, not explored:
             // c * 2^b states and c * (b * 2^(b-1) + 1) transitions over c * (b + 1)
             // levels, ending at the state X' they reach (inserted for the next level).
+            // Whole reps (abstract kernel).  An element's phase-0 program repeats
+            // busy(gmt*ts), barrier, busy(ts), barrier for reps = size/ts reps
+            // (kernel.cpp:33-43); the rules read its cursor only through instr_at(),
+            // which is periodic with period 4 there, and no rule reads the time.  At
+            // a rep start (the level is this one state; every launched element runs,
+            // unreported, at a cursor = 0 mod 4 with a fresh busy(gmt*ts)) the state
+            // is compared with the previous rep start X: if it equals X with the
+            // time advanced and every running cursor + 4 (the packed words decide),
+            // the levels between them form a period that the following reps repeat
+            // exactly while their cursors stay in the rep range.  k periods are
+            // counted: k times the period's states, transitions and levels.
+            if (n == 1 && a.skip && !a.check_inv && d.m.kernel == 0) {
+                long long k = 0;
+                if (lane == 0) {
+                    bool start = s.nrp_work == 0 && s.all_nwe > 0;
+                    int running = 0;
+                    for (int p = 0; p < d.m.n_pex && start; ++p) {
+                        const PexS& px = s.pex[p];
+                        if (px.pc == P_WAITGO || px.pc == P_EXITED) continue;
+                        start = px.pc == P_RUN && px.phase == 0 && (px.cursor & 3) == 0 &&
+                                (int)px.cursor <= 4 * d.m.reps - 4 &&
+                                px.busy_left == d.m.gmt * d.m.ts && !px.reported;
+                        ++running;
+                    }
+                    start = start && running == s.all_nwe;
+                    if (start) {
+                        const unsigned long long ev = acc_terms + acc_dead;
+                        bool period = false;
+                        if (rep_valid && ev == rep_events && !(acc_flags & 3)) {
+                            copy_state(d.m, t, s);
+                            t.time = rep_time;
+                            for (int p = 0; p < d.m.n_pex; ++p)
+                                if (t.pex[p].pc == P_RUN) t.pex[p].cursor -= 4;
+                            for (int w = 0; w < SW; ++w) row[w] = kGuard;
+                            pack(d, cfg, t, row);
+                            period = true;
+                            for (int w = 0; w < words; ++w) period &= row[w] == rep_key[w];
+                        }
+                        if (period) {
+                            const long long P = level - rep_level;
+                            const unsigned long long Sp = tot_states - rep_states;
+                            const unsigned long long Tp = acc_trans - rep_trans;
+                            const long long dt = s.time - rep_time;
+                            k = 0x7fffffff;
+                            for (int p = 0; p < d.m.n_pex; ++p)
+                                if (s.pex[p].pc == P_RUN)
+                                    k = min(k, (long long)(4 * d.m.reps - 4 - s.pex[p].cursor) / 4);
+                            if (a.depth_cap) k = min(k, (long long)(a.depth_cap - level) / P);
+                            const unsigned long long cap = a.cfg_cap, tot = tot_states;
+                            const unsigned long long r = cap - (tot < cap ? tot : cap);
+                            k = min(k, (long long)(r / Sp) - 1);
+                            if (k > 0) {
+                                s.time += k * dt;
+                                for (int p = 0; p < d.m.n_pex; ++p)
+                                    if (s.pex[p].pc == P_RUN) s.pex[p].cursor += (uint16_t)(4 * k);
+                                for (int w = 0; w < SW; ++w) row[w] = kGuard;
+                                pack(d, cfg, s, row);
+                                uint64_t Hx = 0;
+                                for (int w = 0; w < words; ++w) Hx += (uint64_t)row[w] * hk[w];
+                                level_insert(tags[nx], kn, list[nx], &n_list[nx], words, row,
+                                             fmix64(Hx), &lv_flags);
+                                lv[0] += (unsigned long long)k * Sp;
+                                lv[1] += (unsigned long long)k * Tp;
+                                lv_jump = (uint32_t)(k * P - 1);
+                                rep_valid = 0;
+                            }
+                        }
+                        if (k <= 0) {
+                            k = 0;
+                            for (int w = 0; w < SW; ++w) row[w] = kGuard;
+                            pack(d, cfg, s, row);
+                            for (int w = 0; w < words; ++w) rep_key[w] = row[w];
+                            rep_valid = 1;
+                            rep_level = level;
+                            rep_states = tot_states;
+                            rep_trans = acc_trans;
+                            rep_events = ev;
+                            rep_time = s.time;
+                        }
+                    }
+                }
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k > 0) {
+                    __syncwarp();
+                    continue;
+                }
+                __syncwarp();
+            }
             if (n == 1 && a.skip && !a.check_inv) {
                 long long cyc = 0;
                 if (lane == 0 && ne >= 1 && ne <= 16 && ne == s.all_nwe && s.nrp_work == 0 &&

@@ -239,3 +239,57 @@ def test_large_explorations_match_independent_counts(engine, gold):
         assert x.complete and (x.states_visited, x.transitions_applied, x.terminals) == (
             c["states"], c["transitions"], c["terminals"]), c
         assert x.max_depth_reached == c["levels"] - 1, c
+
+
+LEVEL_CASES = [
+    # (platform, kernel, size, max_states, max_depth)
+    ((1, 1, 4, 4), 0, 64, 5_000_000, 4_000_000),
+    ((1, 1, 4, 4), 0, 256, 5_000_000, 4_000_000),
+    ((1, 1, 4, 4), 0, 256, 5_000_000, 3000),      # depth cap inside the chains
+    ((1, 1, 4, 4), 1, 64, 5_000_000, 4_000_000),  # minimum kernel: tick cycles only
+    ((1, 1, 4, 4), 1, 64, 5_000_000, 500),
+    ((2, 1, 2, 4), 0, 32, 5_000_000, 4_000_000),  # two devices: handover skew
+    ((1, 2, 2, 4), 0, 64, 5_000_000, 4_000_000),
+    ((1, 1, 8, 2), 0, 64, 5_000_000, 4_000_000),
+    ((3, 1, 1, 1), 1, 32, 5_000_000, 4_000_000),
+]
+
+
+@pytest.mark.parametrize("case", LEVEL_CASES)
+def test_level_pass_equals_global_sweep(engine, monkeypatch, case):
+    """The narrow-graph pass (level_kernel: one CTA per configuration, level by
+    level in shared memory, pure tick cycles and whole reps counted in closed form)
+    against the global sweep alone (MCTB_BFS_NOLEVEL) and the level pass without
+    the closed-form skips (MCTB_BFS_NOSKIP): every statistic of every configuration
+    equal, with and without a depth cap."""
+    m = engine
+    plat, kernel, size, states, depth = case
+    cfgs = [c for c in m.enumerate_configs(size) if kernel == 0 or c.wg * c.ts <= size]
+    args = (m.PlatformConfig(*plat), problem(m, size, kernel), cfgs)
+    kw = dict(max_states=states, max_depth=depth)
+    got = m.explore_configs(*args, **kw)
+    monkeypatch.setenv("MCTB_BFS_NOSKIP", "1")
+    noskip = m.explore_configs(*args, **kw)
+    monkeypatch.setenv("MCTB_BFS_NOLEVEL", "1")
+    glob = m.explore_configs(*args, **kw)
+    for c, g, n, x in zip(cfgs, got, noskip, glob):
+        if g.states_visited >= states:
+            # a binding visited cap on a graph too deep to rank (lexrank_prefix):
+            # the edge count is then the sweep's own, which depends on its order
+            assert (g.complete, g.states_visited) == (x.complete, x.states_visited), (case, c)
+            continue
+        assert g == x == n, (case, c)
+
+
+def test_level_pass_tune_equals_global_sweep(engine, monkeypatch):
+    """tune through the level pass and through the global sweep alone: the same
+    t_min, parameters, proof, checks and states_visited_total (sizes where the
+    reference's goldens stop; tests/golden/tune_large.json pins size 512)."""
+    m = engine
+    for plat, size in (((1, 1, 4, 4), 128), ((2, 2, 2, 4), 64), ((1, 1, 2, 1), 128)):
+        a = m.tune(m.PlatformConfig(*plat), m.ProblemSpec.abstract(size))
+        monkeypatch.setenv("MCTB_BFS_NOLEVEL", "1")
+        b = m.tune(m.PlatformConfig(*plat), m.ProblemSpec.abstract(size))
+        monkeypatch.delenv("MCTB_BFS_NOLEVEL")
+        assert (a.t_min, a.params, a.proven, a.stats.checks_run, a.stats.states_visited_total) == (
+            b.t_min, b.params, b.proven, b.stats.checks_run, b.stats.states_visited_total), (plat, size)

@@ -230,9 +230,9 @@ def test_visited_cap_matches_reference(engine, gold):
     terminal lies beyond the visited set's capacity in the DFS's order (its first
     path, or the guided walk's path behind the abandoned siblings' subtrees) ends
     capped with no verdict and the check moves on, as the reference does.  The
-    verdicts, states_visited, counterexamples and tune results match;
-    transitions_applied under a binding cap depends on the DFS order and is not
-    compared."""
+    verdicts, states_visited, counterexamples and tune results match, and so do
+    transitions_applied and max_depth_reached, which under a binding cap depend on
+    the DFS order (derived from the least-path ranking, lexrank_prefix)."""
     m = engine
     g = gold("cap.json")
     for c in g["checks"]:
