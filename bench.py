@@ -598,6 +598,35 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
                                  r.stats.checks_run, r.stats.states_visited_total, r.trace.steps)
                              and sha(rr["trace"]) == sha(r.trace.transitions))
     out["tune"] = tune
+    # (1b) tune at the paper's largest sizes (BASELINE configs[1]), the result checked
+    # against the reference's own run recorded in tests/golden/tune_large.json
+    with open(os.path.join(ROOT, "tests", "golden", "tune_large.json")) as f:
+        gold = {g["size"]: g for g in json.load(f)}
+    large = []
+    for size in (512, 1024):
+        pl = m.ProblemSpec.abstract(size)
+        m.tune(plat, pl)  # warm
+        t0 = time.perf_counter()
+        r = m.tune(plat, pl, seed=1)
+        row = {"size": size, "gpu_seconds": time.perf_counter() - t0, "t_min": r.t_min,
+               "wg": r.params.wg, "ts": r.params.ts, "proven": r.proven,
+               "checks_run": r.stats.checks_run,
+               "states_visited_total": r.stats.states_visited_total}
+        g = gold.get(size)
+        if g is not None:
+            row["reference_seconds_recorded"] = g["reference_seconds"]
+            row["reference_cores"] = 1
+            row["identical_to_reference"] = (
+                (r.t_min, r.params.wg, r.params.ts, r.t_ini, r.proven, r.stats.checks_run,
+                 r.stats.states_visited_total, r.trace.steps)
+                == (g["t_min"], g["wg"], g["ts"], g["t_ini"], bool(g["proven"]), g["checks_run"],
+                    g["states_visited_total"], g["steps"]))
+        large.append(row)
+    out["tune_large"] = {
+        "workload": "tune, abstract kernel, platform (1,1,4,4), seed 1, sizes 512 and 1024 "
+                    "(Table 1's largest); reference_seconds_recorded: the reference's tune "
+                    "on one core of the build container (tests/golden/make_golden_tune_large.py)",
+        "runs": large}
     # (2) exploration of one configuration's full interleaving space (configs[3]:
     # ~10^8 states with the visited-state hash table in HBM)
     plat16 = m.PlatformConfig(1, 1, 16, 4)
