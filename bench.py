@@ -630,6 +630,9 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
     # (2) exploration of one configuration's full interleaving space (configs[3]:
     # ~10^8 states with the visited-state hash table in HBM)
     plat16 = m.PlatformConfig(1, 1, 16, 4)
+    # the global sweep alone (explore_kernel with its HBM table): the level pass's
+    # closed-form counts would otherwise cover part of the space
+    os.environ["MCTB_BFS_NOLEVEL"] = "1"
     # one warm-up sweep of the same workload: the first call in a process maps the
     # table's HBM into the stream-ordered pool (reported as cold_api_seconds)
     t0 = time.perf_counter()
@@ -661,6 +664,7 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
           "cold_api_seconds": cold,
           "states_per_s": rate, "states_per_s_api": x.states_visited / wall,
           "key_words": words, "slot_bytes": line_bytes, "table_slots": info[0].table_slots,
+          "path": "global sweep only (MCTB_BFS_NOLEVEL): every state expanded by explore_kernel",
           "roofline": {
               "bound": "latency: dependent L2/HBM round trips per state (probe, claim, queue)",
               "hbm": {"achieved": bps * rate / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -692,6 +696,7 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
         ex["reference_states_per_s"] = rx["states"] / el
         ex["reference_sample"] = ("explore_machine (1,1,8,4) size 32 (8,2): "
                                   f"{rx['states']} states in {el:.2f} s, 1 core")
+    os.environ.pop("MCTB_BFS_NOLEVEL", None)
     out["explore"] = ex
     # (3) swarm trajectories: 10^6 Philox schedules over every configuration, size 16
     import ctypes as C

@@ -108,7 +108,10 @@ namespace {
 #endif
 
 constexpr uint32_t kEmpty = 0xffffffffu;
-constexpr int kBfsThreads = 256;
+#ifndef MCTB_BFS_THREADS
+#define MCTB_BFS_THREADS 256
+#endif
+constexpr int kBfsThreads = MCTB_BFS_THREADS;
 
 // Memory operations on the shared structures (tables, queues, counters).
 // SYS = the partitions span GPUs (peer memory): system scope; else GPU scope.
