@@ -67,10 +67,10 @@ Layout bfs_layout(const MachDesc& m, int n_cfg);
 int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
                    int64_t run_len, int64_t* applies, int64_t* max_depth_reached);
 // The graph size up to which a capped sweep derives the DFS prefix's statistics:
-// 64x the cap, at least 2^22 and at most 2^27 states (and at most 16,384 levels).
-inline uint64_t prefix_limit(uint64_t cap) {
-    return std::min<uint64_t>(std::max<uint64_t>(64 * cap, 1ull << 22), 1ull << 27);
-}
+// 2^22 states (and 16,384 levels).  Ranking a graph that turns out larger is
+// wasted work, so a cap of 2^22 or more (the default 5e6 among them) keeps the
+// sweep's counts without trying.
+inline uint64_t prefix_limit(uint64_t) { return 1ull << 22; }
 
 // The reference DFS's counterexample for bound T (lexfirst.cu).
 // sibling_depths (optional): the depth of each abandoned sibling (its position on

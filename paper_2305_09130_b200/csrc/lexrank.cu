@@ -439,6 +439,10 @@ int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
     // one host round trip per level: deep graphs (the tune sweeps' chains of
     // 1e5-1e6 levels) keep their sweep's counts instead
     constexpr uint64_t kMaxLevels = 16384;
+    if (cap >= limit) {  // the graph holds more than cap states
+        set_error("the capped state graph exceeds the ranking's size bound");
+        return MCTB_LIMIT;
+    }
     if ((uint64_t)std::min<int64_t>(run_len, max_depth) >= kMaxLevels) {
         set_error("the state graph is deeper than the ranking's level bound");
         return MCTB_LIMIT;
