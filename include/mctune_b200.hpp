@@ -986,8 +986,10 @@ inline MachineState replay(const PlatformConfig& platform, const ProblemSpec& pr
 /// terminal states are one (every schedule ends in the same state — all the
 /// Table-1 platforms) contributes the end of the DFS's first path, which is
 /// where the reference's DFS first meets it: the FirstEnabled run.  A
-/// configuration with several terminal states (multi-device handover skew)
-/// raises LimitError: their DFS order is not reproduced here.
+/// configuration with several terminal states (multi-device handover skew) gets
+/// every terminal with its DFS path in the DFS's order (mctb_nonterm_traces,
+/// lexrank.cu), and one whose visited set fills up the terminals among the first
+/// max_states states of that order (graphs up to 2^22 states; LimitError beyond).
 inline std::vector<Trace> check_nontermination(const PlatformConfig& platform,
                                                const ProblemSpec& problem,
                                                const ExploreLimits& limits,
@@ -1009,22 +1011,39 @@ inline std::vector<Trace> check_nontermination(const PlatformConfig& platform,
             const ExploreResult& r = res[k];
             stats.absorb(r.stats);
             if (r.deadlocks) throw ModelBug("deadlock reached during exploration");
-            if (r.stats.states_visited >= limits.max_states)
-                throw LimitError("check_nontermination: the visited set fills up, where "
-                                 "the reference's DFS truncates in traversal order");
-            if (r.terminal_states == 0) continue;
+            // a full visited set: the DFS meets only the terminals among the first
+            // max_states states of its order (explore.cpp:26-30), which the engine
+            // cuts there (graphs up to 2^22 states; LimitError beyond)
+            const bool capped = r.stats.states_visited >= limits.max_states;
+            if (r.terminal_states == 0 && !capped) continue;
             if (r.terminal_states > 1 || !r.complete) {
                 // every terminal state with its DFS path, in DFS order (lexrank.cu)
                 const detail::Args a(platform, problem);
                 std::int64_t n = 0, len = 0;
-                std::vector<std::int64_t> rows(2 * static_cast<std::size_t>(r.terminal_states));
-                std::vector<std::int32_t> buf(4 * static_cast<std::size_t>(r.terminal_states) *
-                                              static_cast<std::size_t>(r.stats.max_depth_reached + 1));
-                detail::check(mctb_nonterm_traces(
-                    a.plat, a.size, a.kernel, a.input, configs[k].wg, configs[k].ts,
-                    limits.max_depth, std::min(limits.max_states, r.stats.states_visited + 1), &n,
-                    rows.data(), static_cast<std::int64_t>(rows.size() / 2), buf.data(),
-                    static_cast<std::int64_t>(buf.size() / 4), &len));
+                std::size_t rows_cap = std::max<std::size_t>(16, r.terminal_states);
+                std::size_t trace_cap = std::max<std::size_t>(
+                    4096, static_cast<std::size_t>(r.terminal_states) *
+                              static_cast<std::size_t>(r.stats.max_depth_reached + 1));
+                std::vector<std::int64_t> rows;
+                std::vector<std::int32_t> buf;
+                for (int attempt = 0;; ++attempt) {
+                    rows.assign(2 * rows_cap, 0);
+                    buf.assign(4 * trace_cap, 0);
+                    const int rc = mctb_nonterm_traces(
+                        a.plat, a.size, a.kernel, a.input, configs[k].wg, configs[k].ts,
+                        limits.max_depth, std::min(limits.max_states, r.stats.states_visited + 1),
+                        &n, rows.data(), static_cast<std::int64_t>(rows_cap), buf.data(),
+                        static_cast<std::int64_t>(trace_cap), &len);
+                    if (rc == MCTB_LIMIT && attempt == 0 &&
+                        (static_cast<std::size_t>(n) > rows_cap ||
+                         static_cast<std::size_t>(len) > trace_cap)) {
+                        rows_cap = std::max(rows_cap, static_cast<std::size_t>(n));
+                        trace_cap = std::max(trace_cap, static_cast<std::size_t>(len));
+                        continue;
+                    }
+                    detail::check(rc);
+                    break;
+                }
                 std::size_t pos = 0;
                 for (std::int64_t i = 0; i < n; ++i) {
                     Trace t;

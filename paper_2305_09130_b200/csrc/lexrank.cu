@@ -27,6 +27,7 @@
 // reports as MCTB_LIMIT instead of guessing.
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -500,14 +501,25 @@ int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
 int lexrank_terminals(MachHost& h, int64_t max_depth, int64_t max_states,
                       std::vector<int64_t>* times, std::vector<int64_t>* lens,
                       std::vector<int32_t>* trace) {
-    LrRun run;
-    int rc = lr_build(h, max_depth, max_states, run);
+    std::unique_ptr<LrRun> runp(new LrRun);
+    int rc = lr_build(h, max_depth, max_states, *runp);
+    // The visited set fills (explore.cpp:26-30): the DFS then meets only the
+    // terminals among the first max_states states of its order.  The whole graph
+    // is ranked (up to 2^22 states) and the terminals are cut at that prefix.
+    uint64_t visit_cap = 0;
+    constexpr int64_t kRankBound = 1ll << 22;
+    if (rc == MCTB_LIMIT && runp->hc[3] == 0 && max_states < kRankBound) {
+        runp.reset(new LrRun);
+        rc = lr_build(h, max_depth, kRankBound, *runp);
+        visit_cap = (uint64_t)max_states;
+    }
     if (rc) {
-        if (rc == MCTB_LIMIT && run.hc[3] == 0)
-            set_error("check_nontermination: the exploration exceeds max_states, where the "
-                      "reference's visited set truncates in traversal order");
+        if (rc == MCTB_LIMIT && runp->hc[3] == 0)
+            set_error("check_nontermination: the visited set fills up and the state graph "
+                      "exceeds the 2^22 states the DFS order is ranked over");
         return rc;
     }
+    LrRun& run = *runp;
     const cudaStream_t st = run.st;
     const BfsDesc& bd = run.bd;
     const int words = run.words;
@@ -569,10 +581,41 @@ int lexrank_terminals(MachHost& h, int64_t max_depth, int64_t max_states,
         }
         return da < db;  // unreachable for distinct terminals
     });
+    // under a full visited set: the terminals among the first visit_cap states of
+    // the preorder of the least-path tree (the DFS's discovery order)
+    std::vector<char> seen;
+    if (visit_cap) {
+        const uint64_t n = base.back();
+        std::vector<unsigned long long> best(n);
+        MCTB_CUDA(cudaMemcpyAsync(best.data(), run.lvl_best.p, n * 8, cudaMemcpyDeviceToHost, st));
+        MCTB_CUDA(cudaStreamSynchronize(st));
+        const size_t L = base.size() - 1;
+        std::vector<uint64_t> cb(n, 0), ce(n, 0);
+        for (size_t d = 0; d + 1 < L; ++d) {
+            const uint64_t b = base[d], nb = base[d + 1], e = base[d + 2];
+            uint64_t c = nb;
+            for (uint64_t g = b; g < nb; ++g) {
+                cb[g] = c;
+                while (c < e && (best[c] >> 16) == g - b) ++c;
+                ce[g] = c;
+            }
+        }
+        seen.assign(n, 0);
+        uint64_t visited = 0;
+        std::vector<uint64_t> stack{0};
+        while (!stack.empty() && visited < visit_cap) {
+            const uint64_t g = stack.back();
+            stack.pop_back();
+            seen[g] = 1;
+            ++visited;
+            for (uint64_t c = ce[g]; c > cb[g]; --c) stack.push_back(c - 1);
+        }
+    }
     times->clear();
     lens->clear();
     trace->clear();
     for (uint64_t j : order) {
+        if (visit_cap && !seen[base[ht[j].depth] + ht[j].rank]) continue;
         times->push_back(ht[j].time);
         lens->push_back(ht[j].depth);
         trace->insert(trace->end(), tr.begin() + 4 * off[j], tr.begin() + 4 * off[j + 1]);

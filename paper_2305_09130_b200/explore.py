@@ -104,8 +104,11 @@ def check_nontermination(platform: PlatformConfig, problem: ProblemSpec, max_dep
     configuration with one terminal state contributes its FIRST-policy run (where
     the reference's DFS first meets it); one with several gets every terminal with
     its DFS path in DFS order from the level-synchronous least-path ranking
-    (nonterm_traces).  Returns (traces, stats of the sweep per configuration)."""
-    from ._lib import ConfigError, LimitError, ModelBug
+    (nonterm_traces), and one whose visited set fills up gets the terminals among
+    the first max_states states of that order (explore.cpp:26-30; graphs up to
+    2^22 states, LimitError beyond).  Returns (traces, stats of the sweep per
+    configuration)."""
+    from ._lib import ConfigError, ModelBug
     from .machine import FIRST, Machine, Trace
     from .model import config_feasible, enumerate_configs
     if max_depth < 1:
@@ -119,10 +122,10 @@ def check_nontermination(platform: PlatformConfig, problem: ProblemSpec, max_dep
     for c, st in zip(configs, stats):
         if st.deadlocks:
             raise ModelBug("deadlock reached during exploration")
-        if st.states_visited >= max_states:
-            raise LimitError("check_nontermination: the visited set fills up, where the "
-                             "reference's DFS truncates in traversal order")
-        if st.terminals == 0:
+        # a full visited set: the DFS meets only the terminals among the first
+        # max_states states of its order (nonterm_traces cuts them there)
+        capped = st.states_visited >= max_states
+        if st.terminals == 0 and not capped:
             continue
         if st.terminals == 1 and st.complete:
             tr = []

@@ -222,10 +222,24 @@ def test_check_nontermination_matches_reference(engine, gold):
         assert sum(s.transitions_applied for s in stats) == c["transitions"], key
         assert max(s.max_depth_reached for s in stats) == c["max_depth"], key
         assert any(not s.complete for s in stats) == bool(c["limit_hit"]), key
-    # a visited set that fills up: the reference's truncation follows its traversal
-    # order, which the engine refuses to guess
-    with pytest.raises(m.LimitError):
-        m.check_nontermination(m.PlatformConfig(3, 1, 1, 1), m.ProblemSpec.minimum(32),
+    # a visited set that fills up: the DFS meets only the terminals among the first
+    # max_states states of its order (explore.cpp:26-30)
+    for c in gold("nonterm_cap.json"):
+        key = (tuple(c["plat"]), c["size"], c["kernel"], c["max_states"])
+        traces, stats = m.check_nontermination(m.PlatformConfig(*c["plat"]),
+                                               problem(m, c["size"], c["kernel"]),
+                                               max_states=c["max_states"])
+        assert len(traces) == c["n"], key
+        for t, g in zip(traces, c["traces"]):
+            assert (t.params.wg, t.params.ts, t.final_time, t.steps) == \
+                (g["wg"], g["ts"], g["final_time"], g["steps"]), key
+            assert sha(t.transitions) == g["sha"], key
+        assert sum(s.states_visited for s in stats) == c["states"], key
+        assert sum(s.transitions_applied for s in stats) == c["transitions"], key
+        assert max(s.max_depth_reached for s in stats) == c["max_depth"], key
+        assert any(not s.complete for s in stats) == bool(c["limit_hit"]), key
+    with pytest.raises(m.LimitError):  # beyond the 2^22 states the order is ranked over
+        m.check_nontermination(m.PlatformConfig(1, 1, 16, 4), m.ProblemSpec.abstract(64),
                                max_states=100_000)
 
 

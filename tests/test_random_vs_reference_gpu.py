@@ -82,10 +82,13 @@ def test_random_nontermination(engine, ref, seed):
     for _ in range(3):
         plat, size, kernel, _ = _case(rng)
         depth = rng.choice((0, 0, rng.randint(20, 300)))
-        r = ref_nonterm(ref, plat, size, kernel, max_depth=depth, rows_cap=4096)
+        states = rng.choice((0, 0, rng.randint(100, 20_000)))
+        r = ref_nonterm(ref, plat, size, kernel, max_depth=depth, max_states=states,
+                        rows_cap=4096)
         traces, stats = m.check_nontermination(m.PlatformConfig(*plat), problem(m, size, kernel),
-                                               max_depth=depth or 4_000_000)
-        key = (plat, size, kernel, depth)
+                                               max_depth=depth or 4_000_000,
+                                               max_states=states or 5_000_000)
+        key = (plat, size, kernel, depth, states)
         assert len(traces) == r["n"], key
         for t, g in zip(traces, r["traces"]):
             assert (t.params.wg, t.params.ts, t.final_time, t.steps) == (
