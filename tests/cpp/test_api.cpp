@@ -224,3 +224,46 @@ TEST_CASE("a binding visited cap moves the counterexample") {
     CHECK(r.params == TuningParams{2, 8});  // (4, 8) without the cap
     CHECK(r.stats.states_visited_total == 20980);
 }
+
+TEST_CASE("explore_machine with hooks agrees with the batched sweep, caps included") {
+    // the DFS-order walk (mctb_machine_states) and the sweep's statistics
+    // (mctb_explore, pinned to the reference) on every configuration, with a
+    // binding visited cap and a depth cap
+    const PlatformConfig plats[] = {{1, 1, 4, 4}, {2, 1, 2, 4}};
+    for (const auto& plat : plats) {
+        const ProblemSpec problem = ProblemSpec::abstract(16);
+        for (long long cap : {5'000'000LL, 500LL}) {
+            for (long long depth : {4'000'000LL, 60LL}) {
+                ExploreLimits limits;
+                limits.max_states = cap;
+                limits.max_depth = depth;
+                const auto cfgs = enumerate_configs(problem.size);
+                const auto want = explore_configs(plat, problem, cfgs, limits);
+                for (std::size_t k = 0; k < cfgs.size(); ++k) {
+                    Machine m(plat, problem, cfgs[k]);
+                    ExploreStats st;
+                    long long on_state = 0, on_term = 0;
+                    ExploreHooks hooks;
+                    hooks.on_state = [&](const Machine&, const MachineState&) { ++on_state; };
+                    hooks.on_terminal = [&](const Machine& mm, const MachineState& s,
+                                            const std::vector<Transition>& path) {
+                        ++on_term;
+                        // the path replays to this terminal state
+                        CHECK(replay(mm.platform, mm.problem,
+                                     Trace{path, s.time, mm.params,
+                                           static_cast<long long>(path.size())})
+                                  .time == s.time);
+                        return true;
+                    };
+                    const bool complete = explore_machine(m, limits, st, hooks);
+                    CHECK(complete == want[k].complete);
+                    CHECK(st.states_visited == want[k].stats.states_visited);
+                    CHECK(on_state == st.states_visited);
+                    CHECK(st.transitions_applied == want[k].stats.transitions_applied);
+                    CHECK(st.max_depth_reached == want[k].stats.max_depth_reached);
+                    if (want[k].complete) CHECK(on_term == want[k].terminal_states);
+                }
+            }
+        }
+    }
+}
