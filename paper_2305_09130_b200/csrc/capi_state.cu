@@ -183,6 +183,8 @@ int from_flat(const MachHost& h, const int64_t* f, int64_t n, MState& s) {
 }
 
 // One machine (the last one asked for on this thread, kept) and its device view.
+// Its few device buffers (one state, one enabled list) live as long as the
+// thread; they are not freed at exit, when the CUDA runtime may already be gone.
 struct Ctx {
     int key[6] = {-1, -1, -1, -1, -1, -1};
     std::vector<int64_t> input;
