@@ -369,7 +369,19 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
     unsigned claim = 1;
     uint32_t peek = kEmpty;  // lane j: entry h_run + j of the current run, as first read
     uint32_t dep = 0;        // depth of the parent (tracked under a depth cap only)
+#ifdef MCTB_BFS_DEBUG
+    unsigned long long dbg_it = 0;
+#endif
     for (;;) {
+#ifdef MCTB_BFS_DEBUG
+        if (++dbg_it == (1ull << 22)) {
+            if (lane == 0)
+                printf("[dbg] warp %d blk %d: %llu iterations, local %d cfg %d g_states %llu n_states %u "
+                       "h_next %u h_end %u since %u dep %u err %d\n",
+                       wib, blockIdx.x, dbg_it, (int)local, cur_cfg, g_states, n_states, h_next,
+                       h_end, since, dep, g_err);
+        }
+#endif
 #ifdef MCTB_BFS_PHASES
         ph_chain = local;
         if (a.op_hist && lane == 0) atomicAdd(&ph_s[(ph_chain ? 8 : 0) + 7], 1ull);
@@ -1427,6 +1439,35 @@ static int level_pass(const BfsPlan& pl, uint64_t cfg_cap, uint32_t depth_cap, b
     return MCTB_OK;
 }
 
+int dfs_prefix_stats(MachHost& h, int64_t max_depth, uint64_t cap, int64_t run_len,
+                     int64_t* applies, int64_t* max_depth_reached) {
+    constexpr uint64_t kLimit = 1ull << 22;    // states ranked at most
+    constexpr int64_t kMaxLevels = 16384;      // one host round trip per level
+    if (cap >= kLimit || std::min(run_len, max_depth) >= kMaxLevels) {
+        set_error("the capped state graph is beyond the ranking's bounds");
+        return MCTB_LIMIT;
+    }
+    // the graph's size within max_depth, from the (fast) sweep capped at the bound:
+    // ranking a graph that turns out too large would be wasted work
+    std::vector<MachHost> one(1, h);
+    BfsResult r;
+    cudaStream_t st;
+    MCTB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int rc = run_bfs(one, kLimit + 64, kLimit, &r, st, false, nullptr, 1, false, 0,
+                     (uint32_t)std::min<int64_t>(max_depth, 0x7fffffff));
+    cudaStreamDestroy(st);
+    if (rc) return rc;
+    if (r.error == 3) {
+        set_error("model bug: deadlock or inapplicable transition during exploration");
+        return MCTB_MODEL_BUG;
+    }
+    if (r.error || r.stats[0].states >= kLimit) {
+        set_error("the capped state graph exceeds the ranking's size bound");
+        return MCTB_LIMIT;
+    }
+    return lexrank_prefix(h, max_depth, cap, r.stats[0].states, applies, max_depth_reached);
+}
+
 int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, BfsResult* res,
             cudaStream_t st, bool check_invariants, const std::vector<uint32_t>* seeds, int n_parts,
             bool sys_scope, uint64_t first_cap, uint32_t depth_cap,
@@ -1726,10 +1767,9 @@ int mctb_explore(const int* plat, int size, int kernel, const int64_t* input,
         o[3] = s.depth_cut ? max_depth : s.terminals ? proto[c] + s.max_time : -1;
         if (s.capped) {
             // a full visited set: the DFS's own prefix decides both (lexrank.cu), for
-            // graphs up to prefix_limit(cap) states
+            // graphs of fewer than 2^22 states
             int64_t a = 0, md = 0;
-            rc = lexrank_prefix(hs[c], max_depth, cap, prefix_limit(cap), proto[c] + cm_time[c],
-                                &a, &md);
+            rc = dfs_prefix_stats(hs[c], max_depth, cap, proto[c] + cm_time[c], &a, &md);
             if (rc == MCTB_OK) {
                 o[2] = a;
                 o[3] = md;

@@ -61,16 +61,15 @@ uint64_t depth_bound(const MachDesc& m, int64_t protocol_steps);
 Layout bfs_layout(const MachDesc& m, int n_cfg);
 
 // The reference DFS's transitions_applied and max_depth_reached when its visited
-// set fills at cap states (lexrank.cu); MCTB_LIMIT when the state graph holds more
-// than `limit` states or its runs (run_len transitions, the lock-step run) are
-// 16,384 transitions or longer.
-int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
-                   int64_t run_len, int64_t* applies, int64_t* max_depth_reached);
-// The graph size up to which a capped sweep derives the DFS prefix's statistics:
-// 2^22 states (and 16,384 levels).  Ranking a graph that turns out larger is
-// wasted work, so a cap of 2^22 or more (the default 5e6 among them) keeps the
-// sweep's counts without trying.
-inline uint64_t prefix_limit(uint64_t) { return 1ull << 22; }
+// set fills at cap states: lexrank_prefix (lexrank.cu) ranks the graph of
+// graph_states states; dfs_prefix_stats (bfs.cu) first sizes the graph with a
+// sweep and returns MCTB_LIMIT (nothing ranked) when it holds 2^22 states or
+// more, spans 16,384 levels or more (run_len: the lock-step run's transitions),
+// or the cap is itself 2^22 or more.
+int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t graph_states,
+                   int64_t* applies, int64_t* max_depth_reached);
+int dfs_prefix_stats(MachHost& h, int64_t max_depth, uint64_t cap, int64_t run_len,
+                     int64_t* applies, int64_t* max_depth_reached);
 
 // The reference DFS's counterexample for bound T (lexfirst.cu).
 // sibling_depths (optional): the depth of each abandoned sibling (its position on

@@ -120,8 +120,8 @@ double now_ms() {
 }
 
 // transitions_applied and max_depth_reached of configuration k's DFS when its
-// visited set fills (explore.cpp:26-30), for graphs up to prefix_limit(cap)
-// states; beyond, the sweep's edge count and the cap's depth stand in
+// visited set fills (explore.cpp:26-30), for graphs of fewer than 2^22 states;
+// beyond, the sweep's edge count stands in
 int ensure_prefix(Ctx& c, int k, int64_t* applies, int64_t* depth) {
     if (c.pre_applies.size() != c.wg.size()) {
         c.pre_applies.assign(c.wg.size(), -1);
@@ -129,8 +129,8 @@ int ensure_prefix(Ctx& c, int k, int64_t* applies, int64_t* depth) {
     }
     if (c.pre_applies[k] < 0) {
         const double t0 = now_ms();
-        int rc = lexrank_prefix(c.hs[k], c.max_depth, c.cap, prefix_limit(c.cap), c.cm_steps[k],
-                                &c.pre_applies[k], &c.pre_depth[k]);
+        int rc = dfs_prefix_stats(c.hs[k], c.max_depth, c.cap, c.cm_steps[k], &c.pre_applies[k],
+                                  &c.pre_depth[k]);
         c.ms_prefix += now_ms() - t0;
         if (rc == MCTB_LIMIT) {
             c.pre_applies[k] = (int64_t)c.bfs.stats[k].transitions;

@@ -64,7 +64,10 @@ __device__ void lr_insert(const LrTable& t, const LrLevel& lv, const uint32_t* k
                           unsigned long long bestv) {
     const unsigned long long fp = h | 1ull;
     uint64_t i = h & t.mask;
-    for (uint64_t probe = 0; probe <= t.mask; ++probe, i = (i + 1) & t.mask) {
+    // the table holds 2x the states it is sized for: a probe sequence this long
+    // means it is overfull (a level outgrew the bound) — report it instead of
+    // scanning the whole table per insert
+    for (uint64_t probe = 0; probe < 1024 && probe <= t.mask; ++probe, i = (i + 1) & t.mask) {
         unsigned long long tg = *(volatile unsigned long long*)&t.tag[i];
         if (tg == 0) {
             tg = atomicCAS(&t.tag[i], 0ull, fp);
@@ -432,67 +435,50 @@ __global__ void lr_ne_kernel(BfsDesc bd, const uint32_t* states, int words, uint
 // states of its discovery order (a full set stops only new states), applies
 // every transition of those below max_depth, and reaches their largest depth.
 // The order is the preorder of the least-path tree (lexrank_states), so the
-// whole graph within max_depth is ranked first: MCTB_LIMIT when it holds more
-// than `limit` states (the callers then keep their sweep's own counts).
-int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t limit,
-                   int64_t run_len, int64_t* applies, int64_t* max_depth_reached) {
-    int rc = MCTB_LIMIT;
-    // one host round trip per level: deep graphs (the tune sweeps' chains of
-    // 1e5-1e6 levels) keep their sweep's counts instead
-    constexpr uint64_t kMaxLevels = 16384;
-    if (cap >= limit) {  // the graph holds more than cap states
-        set_error("the capped state graph exceeds the ranking's size bound");
-        return MCTB_LIMIT;
-    }
-    if ((uint64_t)std::min<int64_t>(run_len, max_depth) >= kMaxLevels) {
-        set_error("the state graph is deeper than the ranking's level bound");
-        return MCTB_LIMIT;
-    }
-    for (uint64_t tc = std::min(limit, std::max<uint64_t>(2 * cap, 1ull << 16));;
-         tc = std::min(limit, tc * 8)) {
-        LrRun run;
-        rc = lr_build(h, max_depth, (int64_t)tc, run, kMaxLevels);
-        if (rc == MCTB_LIMIT && run.base.size() > kMaxLevels) return rc;
-        if (rc == MCTB_LIMIT && tc < limit) continue;
-        if (rc) return rc;
-        const cudaStream_t st = run.st;
-        const uint64_t n = run.base.back();
-        DevBuf<uint16_t> d_ne;
-        if ((rc = d_ne.alloc(n, st))) return rc;
-        lr_ne_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(run.bd, run.lvl_states.p,
-                                                                 run.words, n, d_ne.p);
-        MCTB_CUDA(cudaGetLastError());
-        std::vector<uint16_t> ne(n);
-        std::vector<unsigned long long> best(n);
-        MCTB_CUDA(cudaMemcpyAsync(ne.data(), d_ne.p, n * 2, cudaMemcpyDeviceToHost, st));
-        MCTB_CUDA(cudaMemcpyAsync(best.data(), run.lvl_best.p, n * 8, cudaMemcpyDeviceToHost, st));
-        MCTB_CUDA(cudaStreamSynchronize(st));
-        const size_t L = run.base.size() - 1;
-        std::vector<uint64_t> cb(n, 0), ce(n, 0);
-        for (size_t d = 0; d + 1 < L; ++d) {
-            const uint64_t b = run.base[d], nb = run.base[d + 1], e = run.base[d + 2];
-            uint64_t c = nb;
-            for (uint64_t g = b; g < nb; ++g) {
-                cb[g] = c;
-                while (c < e && (best[c] >> 16) == g - b) ++c;
-                ce[g] = c;
-            }
+// whole graph within max_depth is ranked: graph_states is its size (known from a
+// sweep, dfs_prefix_stats in bfs.cu).
+int lexrank_prefix(MachHost& h, int64_t max_depth, uint64_t cap, uint64_t graph_states,
+                   int64_t* applies, int64_t* max_depth_reached) {
+    LrRun run;
+    int rc = lr_build(h, max_depth, (int64_t)std::max<uint64_t>(graph_states, 1), run);
+    if (rc) return rc;
+    const cudaStream_t st = run.st;
+    const uint64_t n = run.base.back();
+    DevBuf<uint16_t> d_ne;
+    if ((rc = d_ne.alloc(n, st))) return rc;
+    lr_ne_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(run.bd, run.lvl_states.p, run.words,
+                                                             n, d_ne.p);
+    MCTB_CUDA(cudaGetLastError());
+    std::vector<uint16_t> ne(n);
+    std::vector<unsigned long long> best(n);
+    MCTB_CUDA(cudaMemcpyAsync(ne.data(), d_ne.p, n * 2, cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaMemcpyAsync(best.data(), run.lvl_best.p, n * 8, cudaMemcpyDeviceToHost, st));
+    MCTB_CUDA(cudaStreamSynchronize(st));
+    const size_t L = run.base.size() - 1;
+    std::vector<uint64_t> cb(n, 0), ce(n, 0);
+    for (size_t d = 0; d + 1 < L; ++d) {
+        const uint64_t b = run.base[d], nb = run.base[d + 1], e = run.base[d + 2];
+        uint64_t c = nb;
+        for (uint64_t g = b; g < nb; ++g) {
+            cb[g] = c;
+            while (c < e && (best[c] >> 16) == g - b) ++c;
+            ce[g] = c;
         }
-        int64_t a = 0, md = 0;
-        uint64_t seen = 0;
-        std::vector<std::pair<uint64_t, size_t>> stack{{0, 0}};
-        while (!stack.empty() && seen < cap) {
-            const auto [g, d] = stack.back();
-            stack.pop_back();
-            ++seen;
-            if ((int64_t)d < max_depth) a += ne[g];
-            md = std::max<int64_t>(md, (int64_t)d);
-            for (uint64_t c = ce[g]; c > cb[g]; --c) stack.push_back({c - 1, d + 1});
-        }
-        *applies = a;
-        *max_depth_reached = md;
-        return MCTB_OK;
     }
+    int64_t a = 0, md = 0;
+    uint64_t seen = 0;
+    std::vector<std::pair<uint64_t, size_t>> stack{{0, 0}};
+    while (!stack.empty() && seen < cap) {
+        const auto [g, d] = stack.back();
+        stack.pop_back();
+        ++seen;
+        if ((int64_t)d < max_depth) a += ne[g];
+        md = std::max<int64_t>(md, (int64_t)d);
+        for (uint64_t c = ce[g]; c > cb[g]; --c) stack.push_back({c - 1, d + 1});
+    }
+    *applies = a;
+    *max_depth_reached = md;
+    return MCTB_OK;
 }
 
 // All terminal states of one configuration in DFS order with their least paths.
