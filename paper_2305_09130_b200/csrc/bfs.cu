@@ -680,6 +680,15 @@ struct LevelArgs {
     uint32_t* frontier;  // [n_cfg][kLvlWidth * words]: a handed-off level
     int64_t* fstat;      // [n_cfg][4]: {status (0 done, 1 handed off, 3 model bug), states, level}
     int skip;            // count pure tick cycles instead of exploring them
+    unsigned max_width;  // a wider level goes to the global sweep (<= kLvlWidth)
+    // so does a run of wide_run consecutive levels wider than wide: eight warps
+    // take ceil(n / 8) expansions per level, where the global sweep's thousands
+    // of warps take one; a short burst stays (the skips need the level pass)
+    unsigned wide, wide_run;
+    // and a window of `window` levels with no closed-form skip and at least
+    // window_states states: several states per level wait for the slowest one
+    // at every level barrier, where the global sweep's warps run ahead
+    unsigned window, window_states;
 };
 
 // Inserts `row` (hash hh) into the level table; 1 new, 0 present, -1 full.
@@ -798,6 +807,8 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
     int acc_flags = 0;
     int status = 0;
     unsigned handed = 0;
+    unsigned wide_levels = 0;  // consecutive levels wider than a.wide
+    unsigned win_levels = 0, win_states = 0;  // the current window (no skip in it yet)
     uint32_t level = 0;
     for (int cur = 0;; cur ^= 1, ++level) {
         const int nx = cur ^ 1;
@@ -1057,7 +1068,17 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
             status = 3;
             break;
         }
-        if (lv_flags & 4) {
+        wide_levels = n > a.wide ? wide_levels + 1 : 0;
+        if (lv_jump) {
+            win_levels = win_states = 0;
+        } else {
+            ++win_levels;
+            win_states += n;
+        }
+        const bool slow_window = win_levels >= a.window && win_states >= a.window_states;
+        if (win_levels >= a.window) win_levels = win_states = 0;
+        if ((lv_flags & 4) || n_list[nx] > a.max_width || wide_levels >= a.wide_run ||
+            slow_window) {
             // too wide: this level goes to the global sweep, unexpanded
             for (unsigned i = threadIdx.x; i < n * words; i += kLvlThreads)
                 a.frontier[(size_t)cfg * kLvlWidth * words + i] = kc[list[cur][i / words] * words + i % words];
@@ -1401,6 +1422,18 @@ static int level_pass(const BfsPlan& pl, uint64_t cfg_cap, uint32_t depth_cap, b
     la.frontier = (uint32_t*)(blk + sb);
     la.fstat = (int64_t*)(blk + sb + fb);
     la.skip = getenv("MCTB_BFS_NOSKIP") ? 0 : 1;
+    la.max_width = kLvlWidth;
+    la.wide = 24;
+    la.wide_run = 32;
+    if (const char* e = getenv("MCTB_BFS_LEVEL_WIDTH"))
+        la.max_width = (unsigned)std::min(std::max(atoi(e), 1), kLvlWidth);
+    if (const char* e = getenv("MCTB_BFS_LEVEL_WIDE")) la.wide = (unsigned)std::max(atoi(e), 1);
+    if (const char* e = getenv("MCTB_BFS_LEVEL_RUN")) la.wide_run = (unsigned)std::max(atoi(e), 1);
+    la.window = 1024;
+    la.window_states = 2048;
+    if (const char* e = getenv("MCTB_BFS_LEVEL_WINDOW")) la.window = (unsigned)std::max(atoi(e), 1);
+    if (const char* e = getenv("MCTB_BFS_LEVEL_WSTATES"))
+        la.window_states = (unsigned)std::max(atoi(e), 1);
     const size_t dyn = (2 * (size_t)kLvlSlots * words + (kLvlThreads / 32) * 34 * (size_t)pl.sw) * 4;
     auto kern = pl.sw == 16 ? level_kernel<16> : level_kernel<32>;
     MCTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
