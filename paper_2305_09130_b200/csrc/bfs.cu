@@ -76,6 +76,7 @@ struct BfsArgs {
     int check_inv;                // check Machine::check_invariants on every state
     unsigned flush_states;        // publish a warp's state count once it holds this many
     uint32_t depth_cap;           // ExploreLimits::max_depth (0: no state reaches it)
+    int canon;                    // insert a report's successor from its canonical parent only
 };
 
 namespace {
@@ -313,6 +314,33 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
     return v;
 }
 
+// Canonical successors (explore_kernel's comment): false for a report by an
+// element below the parent's highest reported one and for a barrier arrival
+// below the highest element already waiting at that barrier — their successors
+// are inserted by their canonical parents.  max_rep / waiting come from
+// canon_masks.
+__device__ __forceinline__ bool canonical_successor(const Transition& tr, int max_rep,
+                                                    unsigned waiting, int lognwe) {
+    if (tr.op == OP_PEXREPORT) return (int)tr.actor >= max_rep;
+    if (tr.op == OP_PEXARRIVE) {
+        const int p = tr.actor, end = ((p >> lognwe) + 1) << lognwe;
+        const unsigned below_end = end >= 32 ? 0xffffffffu : (1u << end) - 1u;
+        return (waiting & below_end & ~((2u << p) - 1u)) == 0;
+    }
+    return true;
+}
+
+// The parent's highest reported element (-1: none) and its waiting elements
+// (bit p: element p waits at its barrier); n_pex <= 32, one ballot each.
+__device__ __forceinline__ void canon_masks(const MachDesc& m, const MState& s, int lane,
+                                            int* max_rep, unsigned* waiting) {
+    const PexS* px = lane < m.n_pex ? &s.pex[lane] : nullptr;
+    const unsigned rb = __ballot_sync(0xffffffffu, px && px->reported);
+    *max_rep = rb ? 31 - __clz(rb) : -1;
+    *waiting = __ballot_sync(0xffffffffu,
+                             px && (px->pc == P_WAITBARRIER || px->pc == P_WAITGROUPEND));
+}
+
 template <int SW, bool SYS>
 __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(BfsArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -532,13 +560,31 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             if (lane == 0) st.depth_cut = 1;
         } else {
             n_trans += (unsigned)ne;
+            // Canonical report parents.  A report only sets its element's flag and
+            // nrp_work, which no rule but the tick reads (machine.cpp:680-689), so
+            // it commutes with every transition but the tick: a state whose
+            // reported elements are R' is reached from the state without the
+            // report of max(R') (reachable: that report can always be moved to
+            // the end of a path).  Only that parent inserts it; a report by an
+            // element below the parent's highest reported one is counted (it is a
+            // transition) but its successor — present anyway — is neither built
+            // nor probed.  In a lattice of b elements that skips all but
+            // 2 / b of the report successors.  Barrier arrivals likewise
+            // (machine.cpp arrive/release): an arrival only moves its element to
+            // wait and counts it, which only the release (count = nwe, after every
+            // arrival of the episode) and the other arrivals (count < nwe) read,
+            // so within one barrier the arrival of the highest waiting element is
+            // the canonical last one.  (n_pex <= 32: one ballot each.)
+            int max_rep = -1;
+            unsigned waiting = 0;
+            if (a.canon) canon_masks(d.m, s, lane, &max_rep, &waiting);
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
                 long long ins = -1;
                 int owner = mp;
                 uint64_t Hc = H;
                 bool ok = false;
-                if (e < ne) {
+                if (e < ne && (!a.canon || canonical_successor(en[e], max_rep, waiting, lognwe))) {
                     copy_key<SW>(row, pwords);
                     ok = true;
                     if (!fast_successor(d, s, en[e], row, hk, Hc)) {
@@ -689,6 +735,7 @@ struct LevelArgs {
     // window_states states: several states per level wait for the slowest one
     // at every level barrier, where the global sweep's warps run ahead
     unsigned window, window_states;
+    int canon;  // canonical successors only (explore_kernel)
 };
 
 // Inserts `row` (hash hh) into the level table; 1 new, 0 present, -1 full.
@@ -1030,11 +1077,14 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
                 if (lane == 0) atomicOr(&lv_flags, 2);  // explore.cpp:124-127
             } else {
                 if (lane == 0) atomicAdd(&lv[1], (unsigned long long)ne);
+                int max_rep = -1;  // canonical successors only (explore_kernel)
+                unsigned waiting = 0;
+                if (a.canon) canon_masks(d.m, s, lane, &max_rep, &waiting);
                 for (int base = 0; base < ne; base += 32) {
                     const int e = base + lane;
                     uint64_t Hc = H;
                     bool ok = false;
-                    if (e < ne) {
+                    if (e < ne && (!a.canon || canonical_successor(en[e], max_rep, waiting, lognwe))) {
                         copy_key<SW>(row, pwords);
                         ok = true;
                         if (!fast_successor(d, s, en[e], row, hk, Hc)) {
@@ -1422,6 +1472,7 @@ static int level_pass(const BfsPlan& pl, uint64_t cfg_cap, uint32_t depth_cap, b
     la.frontier = (uint32_t*)(blk + sb);
     la.fstat = (int64_t*)(blk + sb + fb);
     la.skip = getenv("MCTB_BFS_NOSKIP") ? 0 : 1;
+    la.canon = getenv("MCTB_BFS_NOCANON") ? 0 : 1;
     la.max_width = kLvlWidth;
     la.wide = 24;
     la.wide_run = 32;
@@ -1581,6 +1632,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.queue_cap = cap / 2;
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
+        a.canon = getenv("MCTB_BFS_NOCANON") ? 0 : 1;
         a.check_inv = check_invariants ? 1 : 0;
         // the visited cap must bound the sweep: every warp publishes its count at
         // least every 64 expansions, and sooner under a small cap, so the states
@@ -1883,6 +1935,7 @@ int mctb_explore_mp_open(const int* plat, int size, int kernel, const int64_t* i
     a.queue_cap = cap / 2;
     a.cfg_cap = c->cfg_cap;
     a.keep = 1;
+    a.canon = getenv("MCTB_BFS_NOCANON") ? 0 : 1;
     a.check_inv = (flags & 1) ? 1 : 0;
     // as run_bfs: publish warp counts often enough for the visited cap to bind
     a.flush_states = (unsigned)std::min<uint64_t>(

@@ -273,9 +273,11 @@ LEVEL_CASES = [
 def test_level_pass_equals_global_sweep(engine, monkeypatch, case):
     """The narrow-graph pass (level_kernel: one CTA per configuration, level by
     level in shared memory, pure tick cycles and whole reps counted in closed form)
-    against the global sweep alone (MCTB_BFS_NOLEVEL) and the level pass without
-    the closed-form skips (MCTB_BFS_NOSKIP): every statistic of every configuration
-    equal, with and without a depth cap."""
+    against the global sweep alone (MCTB_BFS_NOLEVEL), the level pass without
+    the closed-form skips (MCTB_BFS_NOSKIP) and the global sweep building every
+    successor (MCTB_BFS_NOCANON: no canonical-parent pruning of report and
+    arrival successors): every statistic of every configuration equal, with and
+    without a depth cap."""
     m = engine
     plat, kernel, size, states, depth = case
     cfgs = [c for c in m.enumerate_configs(size) if kernel == 0 or c.wg * c.ts <= size]
@@ -286,13 +288,15 @@ def test_level_pass_equals_global_sweep(engine, monkeypatch, case):
     noskip = m.explore_configs(*args, **kw)
     monkeypatch.setenv("MCTB_BFS_NOLEVEL", "1")
     glob = m.explore_configs(*args, **kw)
-    for c, g, n, x in zip(cfgs, got, noskip, glob):
+    monkeypatch.setenv("MCTB_BFS_NOCANON", "1")  # every successor built and probed
+    plain = m.explore_configs(*args, **kw)
+    for c, g, n, x, y in zip(cfgs, got, noskip, glob, plain):
         if g.states_visited >= states:
             # a binding visited cap on a graph too deep to rank (lexrank_prefix):
             # the edge count is then the sweep's own, which depends on its order
             assert (g.complete, g.states_visited) == (x.complete, x.states_visited), (case, c)
             continue
-        assert g == x == n, (case, c)
+        assert g == x == n == y, (case, c)
 
 
 def test_level_pass_tune_equals_global_sweep(engine, monkeypatch):

@@ -1,5 +1,6 @@
-"""Randomised equality check of the narrow-graph level pass against the global sweep
-alone (MCTB_BFS_NOLEVEL): random platforms, sizes 8-64, both kernels, random depth
+"""Randomised equality check of the narrow-graph level pass (with canonical-parent
+pruning) against the global sweep alone building every successor
+(MCTB_BFS_NOLEVEL + MCTB_BFS_NOCANON): random platforms, sizes 8-64, both kernels, random depth
 caps; every statistic of every configuration compared (states and completeness only
 where the 2e6 visited cap binds).  Usage: python tools/level_eqcheck.py SEED SECONDS"""
 import os, random, sys, time
@@ -25,7 +26,9 @@ while time.time() < t_end:
         continue
     t1 = time.time()
     os.environ["MCTB_BFS_NOLEVEL"] = "1"
+    os.environ["MCTB_BFS_NOCANON"] = "1"
     b = m.explore_configs(m.PlatformConfig(*plat), prob, cfgs, max_states=states, max_depth=depth)
+    os.environ.pop("MCTB_BFS_NOCANON", None)
     t2 = time.time()
     print("case", plat, size, kernel, depth, "level %.2f s global %.2f s" % (t1 - t0, t2 - t1), flush=True)
     for c, x, y in zip(cfgs, a, b):
