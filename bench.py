@@ -648,10 +648,10 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
     line_bytes = 64 if words <= 14 else 128
     kern_s = info[0].kernel_us * 1e-6
     rate = x.states_visited / kern_s
-    outdeg = x.transitions_applied / max(1, x.states_visited)
     # algorithmic bytes per state: its slot line written once and read once at
-    # expansion, one slot line read per generated successor (the probe), 8 B of queue
-    bps = line_bytes * (2 + outdeg) + 8
+    # expansion, one slot line read per probed successor (the canonical ones,
+    # EXPLORE_PROBES_PER_STATE of the outdegree's ~9.7), 8 B of queue
+    bps = line_bytes * (2 + EXPLORE_PROBES_PER_STATE) + 8
     hbm_peak, hbm_src = hbm_peak_gbps()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     clk = sm_clock_mhz
@@ -666,7 +666,9 @@ def secondary_metrics(m, with_reference=True, sm_clock_mhz=1965.0, flush=None, p
           "key_words": words, "slot_bytes": line_bytes, "table_slots": info[0].table_slots,
           "path": "global sweep only (MCTB_BFS_NOLEVEL): every state expanded by explore_kernel",
           "roofline": {
-              "bound": "latency: dependent L2/HBM round trips per state (probe, claim, queue)",
+              "bound": "instruction issue and dependent L2/HBM round trips per state "
+                       "(probe, claim, queue); not HBM bandwidth",
+              "probes_per_state": EXPLORE_PROBES_PER_STATE,
               "hbm": {"achieved": bps * rate / 1e9, "peak": hbm_peak, "unit": "GB/s",
                       "frac": bps * rate / 1e9 / hbm_peak, "peak_source": hbm_src,
                       "algorithmic_bytes_per_state": bps,
@@ -785,8 +787,11 @@ SWARM_INST_SOURCE = "ncu smsp__inst_executed.sum x 32 / trajectories (profiles/r
 EXPLORE_SIZE = 64
 EXPLORE_PARAMS = (16, 2)
 EXPLORE_STATES = 137_145_999  # pinned by the independent CPU count (tests/golden/large_counts.json)
-EXPLORE_INST_PER_STATE = 1071.9  # profiles/r01_explore_v8_ncu.txt
-EXPLORE_DRAM_BYTES_PER_STATE = 1038.8
+EXPLORE_INST_PER_STATE = 1007.9  # profiles/r02_explore_canon_ncu.txt
+EXPLORE_DRAM_BYTES_PER_STATE = 619.4
+# table probes per state (MCTB_BFS_OPHIST diagnostics): canonical-parent pruning
+# builds and probes 598,604,791 of the 1,326,882,267 successors
+EXPLORE_PROBES_PER_STATE = 4.365
 
 
 def main():

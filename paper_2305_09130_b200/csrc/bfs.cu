@@ -607,6 +607,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
                     const uint64_t hh = fmix64(Hc);
                     if (a.n_parts > 1) owner = owner_of(hh, a.n_parts);
                     ins = table_insert<SW, SYS>(a, a.part[owner], row, hh);
+                    if (a.op_hist) atomicAdd(&a.op_hist[24], 1ull);  // diagnostics: probes
                     if (ins == -2) set_error<SYS>(me.error, 1);
                     if (ins >= 0 && a.depth_cap)
                         st_relaxed32<SYS>(a.part[owner].depth + ins, (dep + 1) | kGuard);
@@ -1714,7 +1715,8 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
             fprintf(stderr, "[explore] generic successors by op:");
             for (int o = 0; o < 19; ++o)
                 if (hist[4 + o]) fprintf(stderr, " op%d=%llu", o, hist[4 + o]);
-            fprintf(stderr, "\n");
+            fprintf(stderr, "\n[explore] table probes (successors built and inserted): %llu\n",
+                    hist[4 + 24]);
 #ifdef MCTB_BFS_PHASES
             static const char* names[7] = {"pop", "cfg", "unpack", "enum", "rows", "insert", "keep"};
             for (int c = 0; c < 2; ++c) {
