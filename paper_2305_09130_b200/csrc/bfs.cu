@@ -315,30 +315,50 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 }
 
 // Canonical successors (explore_kernel's comment): false for a report by an
-// element below the parent's highest reported one and for a barrier arrival
-// below the highest element already waiting at that barrier — their successors
-// are inserted by their canonical parents.  max_rep / waiting come from
-// canon_masks.
-__device__ __forceinline__ bool canonical_successor(const Transition& tr, int max_rep,
-                                                    unsigned waiting, int lognwe) {
-    if (tr.op == OP_PEXREPORT) return (int)tr.actor >= max_rep;
-    if (tr.op == OP_PEXARRIVE) {
-        const int p = tr.actor, end = ((p >> lognwe) + 1) << lognwe;
-        const unsigned below_end = end >= 32 ? 0xffffffffu : (1u << end) - 1u;
-        return (waiting & below_end & ~((2u << p) - 1u)) == 0;
-    }
+// element below the parent's highest reported one, for a barrier arrival below
+// the highest element already waiting at that barrier and for an activation
+// below the highest element of the unit untouched since its own — their
+// successors are inserted by their canonical parents.
+struct CanonMasks {
+    int max_rep;        // highest reported element, -1: none
+    unsigned waiting;   // bit p: element p waits at its barrier
+    unsigned pristine;  // bit p: element p untouched since its activation (abstract kernel)
+};
+
+// true unless a set bit of `mask` lies above element p within p's unit
+__device__ __forceinline__ bool highest_in_unit(unsigned mask, int p, int lognwe) {
+    const int end = ((p >> lognwe) + 1) << lognwe;
+    const unsigned below_end = end >= 32 ? 0xffffffffu : (1u << end) - 1u;
+    return (mask & below_end & ~((2u << p) - 1u)) == 0;
+}
+
+__device__ __forceinline__ bool canonical_successor(const Transition& tr, const CanonMasks& c,
+                                                    int lognwe) {
+    if (tr.op == OP_PEXREPORT) return (int)tr.actor >= c.max_rep;
+    if (tr.op == OP_PEXARRIVE) return highest_in_unit(c.waiting, tr.actor, lognwe);
+    if (tr.op == OP_UNITPEXGO) return highest_in_unit(c.pristine, tr.peer, lognwe);
     return true;
 }
 
-// The parent's highest reported element (-1: none) and its waiting elements
-// (bit p: element p waits at its barrier); n_pex <= 32, one ballot each.
-__device__ __forceinline__ void canon_masks(const MachDesc& m, const MState& s, int lane,
-                                            int* max_rep, unsigned* waiting) {
+// The parent's masks; n_pex <= 32, one ballot each.  An activation (unit ->
+// element go, machine.cpp UNITPEXGO) commutes with what can follow it while its
+// element has not moved (the other activations of the round and the other
+// elements' reports: no tick, barrier or item hand-back can pass an unmoved
+// element), so the highest element still untouched since its activation marks
+// the canonical last activation.  Untouched, for the abstract kernel: running
+// its first busy(gmt*ts) at cursor 0, unreported.
+__device__ __forceinline__ CanonMasks canon_masks(const MachDesc& m, const MState& s, int lane) {
     const PexS* px = lane < m.n_pex ? &s.pex[lane] : nullptr;
+    CanonMasks c;
     const unsigned rb = __ballot_sync(0xffffffffu, px && px->reported);
-    *max_rep = rb ? 31 - __clz(rb) : -1;
-    *waiting = __ballot_sync(0xffffffffu,
-                             px && (px->pc == P_WAITBARRIER || px->pc == P_WAITGROUPEND));
+    c.max_rep = rb ? 31 - __clz(rb) : -1;
+    c.waiting = __ballot_sync(0xffffffffu,
+                              px && (px->pc == P_WAITBARRIER || px->pc == P_WAITGROUPEND));
+    c.pristine = __ballot_sync(0xffffffffu, m.kernel == 0 && px && px->pc == P_RUN &&
+                                                px->phase == 0 && px->cursor == 0 &&
+                                                !px->reported &&
+                                                px->busy_left == m.gmt * m.ts);
+    return c;
 }
 
 template <int SW, bool SYS>
@@ -575,16 +595,15 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             // arrival of the episode) and the other arrivals (count < nwe) read,
             // so within one barrier the arrival of the highest waiting element is
             // the canonical last one.  (n_pex <= 32: one ballot each.)
-            int max_rep = -1;
-            unsigned waiting = 0;
-            if (a.canon) canon_masks(d.m, s, lane, &max_rep, &waiting);
+            CanonMasks cm{-1, 0u, 0u};
+            if (a.canon) cm = canon_masks(d.m, s, lane);
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
                 long long ins = -1;
                 int owner = mp;
                 uint64_t Hc = H;
                 bool ok = false;
-                if (e < ne && (!a.canon || canonical_successor(en[e], max_rep, waiting, lognwe))) {
+                if (e < ne && (!a.canon || canonical_successor(en[e], cm, lognwe))) {
                     copy_key<SW>(row, pwords);
                     ok = true;
                     if (!fast_successor(d, s, en[e], row, hk, Hc)) {
@@ -1078,14 +1097,13 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
                 if (lane == 0) atomicOr(&lv_flags, 2);  // explore.cpp:124-127
             } else {
                 if (lane == 0) atomicAdd(&lv[1], (unsigned long long)ne);
-                int max_rep = -1;  // canonical successors only (explore_kernel)
-                unsigned waiting = 0;
-                if (a.canon) canon_masks(d.m, s, lane, &max_rep, &waiting);
+                CanonMasks cm{-1, 0u, 0u};  // canonical successors only (explore_kernel)
+                if (a.canon) cm = canon_masks(d.m, s, lane);
                 for (int base = 0; base < ne; base += 32) {
                     const int e = base + lane;
                     uint64_t Hc = H;
                     bool ok = false;
-                    if (e < ne && (!a.canon || canonical_successor(en[e], max_rep, waiting, lognwe))) {
+                    if (e < ne && (!a.canon || canonical_successor(en[e], cm, lognwe))) {
                         copy_key<SW>(row, pwords);
                         ok = true;
                         if (!fast_successor(d, s, en[e], row, hk, Hc)) {
