@@ -323,6 +323,7 @@ struct CanonMasks {
     int max_rep;        // highest reported element, -1: none
     unsigned waiting;   // bit p: element p waits at its barrier
     unsigned pristine;  // bit p: element p untouched since its activation (abstract kernel)
+    unsigned batch;     // bit g: unit g activates a batch (U_ACTIVATEPEX, not a re-arm)
 };
 
 // true unless a set bit of `mask` lies above element p within p's unit
@@ -336,17 +337,20 @@ __device__ __forceinline__ bool canonical_successor(const Transition& tr, const 
                                                     int lognwe) {
     if (tr.op == OP_PEXREPORT) return (int)tr.actor >= c.max_rep;
     if (tr.op == OP_PEXARRIVE) return highest_in_unit(c.waiting, tr.actor, lognwe);
-    if (tr.op == OP_UNITPEXGO) return highest_in_unit(c.pristine, tr.peer, lognwe);
+    if (tr.op == OP_UNITPEXGO)
+        return !((c.batch >> tr.actor) & 1u) || highest_in_unit(c.pristine, tr.peer, lognwe);
     return true;
 }
 
-// The parent's masks; n_pex <= 32, one ballot each.  An activation (unit ->
-// element go, machine.cpp UNITPEXGO) commutes with what can follow it while its
-// element has not moved (the other activations of the round and the other
-// elements' reports: no tick, barrier or item hand-back can pass an unmoved
-// element), so the highest element still untouched since its activation marks
-// the canonical last activation.  Untouched, for the abstract kernel: running
-// its first busy(gmt*ts) at cursor 0, unreported.
+// The parent's masks; n_pex <= 32, one ballot each.  An activation of a batch
+// (unit -> element go in U_ACTIVATEPEX, machine.cpp UNITPEXGO) commutes with what
+// can follow it while its element has not moved (the other activations of the
+// batch and the other elements' reports: no tick, barrier or item hand-back can
+// pass an unmoved element), so the highest element still untouched since its
+// activation marks the canonical last activation.  Untouched, for the abstract
+// kernel: running its first busy(gmt*ts) at cursor 0, unreported.  A re-arm
+// (U_REACTPEX, after a hand-back) is not pruned: the hand-backs that follow it
+// need the unit it returns to serving.
 __device__ __forceinline__ CanonMasks canon_masks(const MachDesc& m, const MState& s, int lane) {
     const PexS* px = lane < m.n_pex ? &s.pex[lane] : nullptr;
     CanonMasks c;
@@ -358,6 +362,7 @@ __device__ __forceinline__ CanonMasks canon_masks(const MachDesc& m, const MStat
                                                 px->phase == 0 && px->cursor == 0 &&
                                                 !px->reported &&
                                                 px->busy_left == m.gmt * m.ts);
+    c.batch = __ballot_sync(0xffffffffu, lane < m.n_units && s.unit[lane].pc == U_ACTIVATEPEX);
     return c;
 }
 
@@ -595,7 +600,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             // arrival of the episode) and the other arrivals (count < nwe) read,
             // so within one barrier the arrival of the highest waiting element is
             // the canonical last one.  (n_pex <= 32: one ballot each.)
-            CanonMasks cm{-1, 0u, 0u};
+            CanonMasks cm{-1, 0u, 0u, 0u};
             if (a.canon) cm = canon_masks(d.m, s, lane);
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
@@ -1097,7 +1102,7 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
                 if (lane == 0) atomicOr(&lv_flags, 2);  // explore.cpp:124-127
             } else {
                 if (lane == 0) atomicAdd(&lv[1], (unsigned long long)ne);
-                CanonMasks cm{-1, 0u, 0u};  // canonical successors only (explore_kernel)
+                CanonMasks cm{-1, 0u, 0u, 0u};  // canonical successors only (explore_kernel)
                 if (a.canon) cm = canon_masks(d.m, s, lane);
                 for (int base = 0; base < ne; base += 32) {
                     const int e = base + lane;
