@@ -320,10 +320,11 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 // below the highest element of the unit untouched since its own — their
 // successors are inserted by their canonical parents.
 struct CanonMasks {
-    int max_rep;        // highest reported element, -1: none
+    // bits 0-7: highest reported element + 1 (0: none); bits 8-23: bit 8 + g set
+    // when unit g activates a batch (U_ACTIVATEPEX, not a re-arm) — one register
+    unsigned rep_batch;
     unsigned waiting;   // bit p: element p waits at its barrier
     unsigned pristine;  // bit p: element p untouched since its activation (abstract kernel)
-    unsigned batch;     // bit g: unit g activates a batch (U_ACTIVATEPEX, not a re-arm)
 };
 
 // true unless a set bit of `mask` lies above element p within p's unit
@@ -335,10 +336,11 @@ __device__ __forceinline__ bool highest_in_unit(unsigned mask, int p, int lognwe
 
 __device__ __forceinline__ bool canonical_successor(const Transition& tr, const CanonMasks& c,
                                                     int lognwe) {
-    if (tr.op == OP_PEXREPORT) return (int)tr.actor >= c.max_rep;
+    if (tr.op == OP_PEXREPORT) return (int)tr.actor + 1 >= (int)(c.rep_batch & 0xffu);
     if (tr.op == OP_PEXARRIVE) return highest_in_unit(c.waiting, tr.actor, lognwe);
     if (tr.op == OP_UNITPEXGO)
-        return !((c.batch >> tr.actor) & 1u) || highest_in_unit(c.pristine, tr.peer, lognwe);
+        return !((c.rep_batch >> (8 + tr.actor)) & 1u) ||
+               highest_in_unit(c.pristine, tr.peer, lognwe);
     return true;
 }
 
@@ -355,14 +357,15 @@ __device__ __forceinline__ CanonMasks canon_masks(const MachDesc& m, const MStat
     const PexS* px = lane < m.n_pex ? &s.pex[lane] : nullptr;
     CanonMasks c;
     const unsigned rb = __ballot_sync(0xffffffffu, px && px->reported);
-    c.max_rep = rb ? 31 - __clz(rb) : -1;
+    c.rep_batch = rb ? 32 - __clz(rb) : 0;
     c.waiting = __ballot_sync(0xffffffffu,
                               px && (px->pc == P_WAITBARRIER || px->pc == P_WAITGROUPEND));
     c.pristine = __ballot_sync(0xffffffffu, m.kernel == 0 && px && px->pc == P_RUN &&
                                                 px->phase == 0 && px->cursor == 0 &&
                                                 !px->reported &&
                                                 px->busy_left == m.gmt * m.ts);
-    c.batch = __ballot_sync(0xffffffffu, lane < m.n_units && s.unit[lane].pc == U_ACTIVATEPEX);
+    c.rep_batch |= (__ballot_sync(0xffffffffu, lane < m.n_units && s.unit[lane].pc == U_ACTIVATEPEX)
+                    & 0xffffu) << 8;
     return c;
 }
 
@@ -600,7 +603,7 @@ __global__ void __launch_bounds__(kBfsThreads, MCTB_BFS_MINB) explore_kernel(Bfs
             // arrival of the episode) and the other arrivals (count < nwe) read,
             // so within one barrier the arrival of the highest waiting element is
             // the canonical last one.  (n_pex <= 32: one ballot each.)
-            CanonMasks cm{-1, 0u, 0u, 0u};
+            CanonMasks cm{0u, 0u, 0u};
             if (a.canon) cm = canon_masks(d.m, s, lane);
             for (int base = 0; base < ne; base += 32) {
                 const int e = base + lane;
@@ -1102,7 +1105,7 @@ __global__ void __launch_bounds__(kLvlThreads, 1) level_kernel(LevelArgs a) {
                 if (lane == 0) atomicOr(&lv_flags, 2);  // explore.cpp:124-127
             } else {
                 if (lane == 0) atomicAdd(&lv[1], (unsigned long long)ne);
-                CanonMasks cm{-1, 0u, 0u, 0u};  // canonical successors only (explore_kernel)
+                CanonMasks cm{0u, 0u, 0u};  // canonical successors only (explore_kernel)
                 if (a.canon) cm = canon_masks(d.m, s, lane);
                 for (int base = 0; base < ne; base += 32) {
                     const int e = base + lane;
