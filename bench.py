@@ -787,8 +787,8 @@ SWARM_INST_SOURCE = "ncu smsp__inst_executed.sum x 32 / trajectories (profiles/r
 EXPLORE_SIZE = 64
 EXPLORE_PARAMS = (16, 2)
 EXPLORE_STATES = 137_145_999  # pinned by the independent CPU count (tests/golden/large_counts.json)
-EXPLORE_INST_PER_STATE = 926.4  # profiles/r02_explore_canon_ncu.txt
-EXPLORE_DRAM_BYTES_PER_STATE = 324.9
+EXPLORE_INST_PER_STATE = 938.1  # profiles/r02_explore_canon_ncu.txt
+EXPLORE_DRAM_BYTES_PER_STATE = 325.0
 # table probes per state (MCTB_BFS_OPHIST diagnostics): canonical-parent pruning
 # builds and probes 225,402,137 of the 1,326,882,267 successors
 EXPLORE_PROBES_PER_STATE = 1.644
