@@ -1584,6 +1584,11 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
             bool sys_scope, uint64_t first_cap, uint32_t depth_cap,
             const std::vector<uint32_t>* seed_depths) {
     const bool dep = depth_cap > 0;
+    // Canonical-parent pruning needs every state's canonical parent in the sweep:
+    // true from the initial states and from a complete level (the level pass's
+    // hand-off), not from arbitrary seeds (the guided walk's abandoned siblings,
+    // whose canonical parents can lie outside their reach).
+    const bool canon = !seeds && !getenv("MCTB_BFS_NOCANON");
     if (n_parts < 1 || n_parts > kMaxParts) {
         set_error("partitions must be in [1, 8]");
         return MCTB_CONFIG_ERROR;
@@ -1659,7 +1664,7 @@ int run_bfs(std::vector<MachHost>& hs, uint64_t max_states, uint64_t cfg_cap, Bf
         a.queue_cap = cap / 2;
         a.cfg_cap = cfg_cap;
         a.keep = getenv("MCTB_BFS_NOKEEP") ? 0 : 1;
-        a.canon = getenv("MCTB_BFS_NOCANON") ? 0 : 1;
+        a.canon = canon ? 1 : 0;
         a.check_inv = check_invariants ? 1 : 0;
         // the visited cap must bound the sweep: every warp publishes its count at
         // least every 64 expansions, and sooner under a small cap, so the states

@@ -256,3 +256,32 @@ def test_visited_cap_matches_reference(engine, gold):
         assert (r.stats.checks_run, r.stats.states_visited_total) == (
             c["checks_run"], c["states_visited_total"]), key
         assert r.trace.steps == c["steps"] and sha(r.trace.transitions) == c["trace_sha"], key
+
+
+def test_guided_walk_sweeps_equal_without_pruning(engine, monkeypatch):
+    """The guided walk's sibling sweep starts from arbitrary states, where the
+    canonical-parent pruning of explore_kernel would lose states whose canonical
+    parent lies outside the siblings' reach: it runs unpruned.  Verdicts and
+    statistics over a range of bounds on schedule-dependent spaces equal those of
+    the engine with pruning switched off everywhere (MCTB_BFS_NOCANON)."""
+    m = engine
+    cases = [((2, 1, 2, 4), m.ProblemSpec.abstract(16)), ((3, 1, 1, 1), m.ProblemSpec.minimum(16)),
+             ((2, 1, 2, 4), m.ProblemSpec.abstract(32)), ((3, 1, 1, 4), m.ProblemSpec.minimum(16))]
+    for plat, prob in cases:
+        t = m.tune(m.PlatformConfig(*plat), prob)
+        for T in range(t.t_min - 2, t.t_ini + 1, max(1, (t.t_ini - t.t_min) // 12)):
+            monkeypatch.delenv("MCTB_BFS_NOCANON", raising=False)
+            a = m.check_overtime(m.PlatformConfig(*plat), prob, T)
+            monkeypatch.setenv("MCTB_BFS_NOCANON", "1")
+            b = m.check_overtime(m.PlatformConfig(*plat), prob, T)
+            key = (plat, prob.size, T)
+            assert (a.violated, a.exhaustive, a.stats.states_visited) == (
+                b.violated, b.exhaustive, b.stats.states_visited), key
+            if a.exhaustive:
+                # (otherwise a configuration capped on a graph beyond the ranking's
+                # bound may contribute its sweep's own, order-dependent edge count)
+                assert (a.stats.transitions_applied, a.stats.max_depth_reached) == (
+                    b.stats.transitions_applied, b.stats.max_depth_reached), key
+            if a.violated:
+                assert (a.trace.final_time, a.trace.steps, a.trace.transitions) == (
+                    b.trace.final_time, b.trace.steps, b.trace.transitions), key
