@@ -231,6 +231,77 @@ int ref_explore(const int* plat, int size, int kernel, const int64_t* input, int
     });
 }
 
+// explore_machine's discovery order (explore.cpp:86-165): FNV-1a 64 of every
+// visited state, in on_state order, over its fields as int64 values in the order
+// of the engine's flat state vector (include/mctune_b200.h, mctb_machine_*):
+// time, nrp_work, all_nwe, fin, next_wg, host {pc, k}, clock, then counted
+// device, unit, barrier and element records, glob and loc.
+int ref_explore_order(const int* plat, int size, int kernel, const int64_t* input, int wg, int ts,
+                      long long max_depth, long long max_states, uint64_t* hashes, long long cap,
+                      long long* n) {
+    return guarded([&] {
+        Machine m(plat_of(plat), problem_of(size, kernel, input), TuningParams{wg, ts});
+        ExploreStats stats;
+        long long count = 0;
+        ExploreHooks hooks;
+        hooks.on_state = [&](const Machine&, const MachineState& s) {
+            uint64_t h = 0xcbf29ce484222325ull;
+            auto put = [&](int64_t v) {
+                for (int b = 0; b < 8; ++b) {
+                    h ^= static_cast<uint64_t>(v >> (8 * b)) & 0xffu;
+                    h *= 0x100000001b3ull;
+                }
+            };
+            put(s.time);
+            put(s.nrp_work);
+            put(s.all_nwe);
+            put(s.fin);
+            put(s.next_wg);
+            put(static_cast<int64_t>(s.host.pc));
+            put(s.host.k);
+            put(static_cast<int64_t>(s.clock));
+            put(static_cast<int64_t>(s.devices.size()));
+            for (const auto& d : s.devices) {
+                put(static_cast<int64_t>(d.pc));
+                put(d.k);
+                put(d.batch_base);
+            }
+            put(static_cast<int64_t>(s.units.size()));
+            for (const auto& u : s.units) {
+                put(static_cast<int64_t>(u.pc));
+                put(u.k);
+                put(u.nwg);
+                put(u.sent);
+                put(u.got_items);
+                put(u.got_ends);
+            }
+            put(static_cast<int64_t>(s.barriers.size()));
+            for (const auto& b : s.barriers) {
+                put(static_cast<int64_t>(b.pc));
+                put(b.count);
+            }
+            put(static_cast<int64_t>(s.pexes.size()));
+            for (const auto& x : s.pexes) {
+                put(static_cast<int64_t>(x.pc));
+                put(static_cast<int64_t>(x.phase));
+                put(x.cursor);
+                put(x.busy_left);
+                put(x.reported);
+                put(x.nwg);
+                put(x.iter);
+            }
+            put(static_cast<int64_t>(s.glob.size()));
+            for (auto v : s.glob) put(v);
+            put(static_cast<int64_t>(s.loc.size()));
+            for (auto v : s.loc) put(v);
+            if (count < cap) hashes[count] = h;
+            ++count;
+        };
+        explore_machine(m, limits_of(max_depth, max_states, 0, 0.0), stats, hooks);
+        *n = count;
+    });
+}
+
 // check_overtime (explore.cpp:167-205).
 // out = [violated, exhaustive, states_visited, max_depth_reached, transitions_applied,
 //        configs_explored, configs_skipped, final_time, wg, ts, steps]

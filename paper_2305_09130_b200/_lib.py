@@ -141,3 +141,6 @@ EXPORTED.append("mctb_kernel_program")
 EXPORTED += ["mctb_machine_initial", "mctb_machine_enabled", "mctb_machine_apply",
              "mctb_machine_query", "mctb_machine_process_name", "mctb_machine_replay",
              "mctb_machine_states"]
+# explore_machine's visit order (the C++ drop-in's ExploreHooks; the parity tests)
+lib.mctb_machine_states.argtypes = [i32p, C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_int64,
+                                    C.c_int64, i64p, C.c_int64, i32p, C.c_int64, i64p]

@@ -233,6 +233,18 @@ class Ref(_Base):
         return dict(zip(["complete", "states", "transitions", "max_depth", "min_time",
                          "max_time", "n_terminal", "n_distinct"], out))
 
+    def explore_order(self, plat, size, kernel, wg, ts, inp=None, max_depth=0, max_states=0,
+                      cap=1 << 20):
+        """FNV-1a 64 of every state explore_machine visits, in on_state order
+        (ref_explore_order: the fields in the engine's flat-vector order)."""
+        hashes = (C.c_uint64 * cap)()
+        n = C.c_longlong()
+        self._chk(self.lib.ref_explore_order(_plat(plat), size, kernel, _inp(size, kernel, inp),
+                                             wg, ts, C.c_longlong(max_depth),
+                                             C.c_longlong(max_states), hashes, C.c_longlong(cap),
+                                             C.byref(n)))
+        return list(hashes[:min(n.value, cap)]), n.value
+
     def check_overtime(self, plat, size, kernel, T, inp=None, max_depth=0, max_states=0):
         out = (C.c_int64 * 11)()
         buf = (C.c_int32 * (4 * TRACE_CAP))()

@@ -149,3 +149,48 @@ def test_random_sweeps_and_runs(engine, ref, seed):
             r = ref.simulate(plat, size, kernel, c.wg, c.ts, policy, s, inp, trace=True)
             assert (g.time, g.steps, g.result) == (r["time"], r["steps"], r["result"]), (plat, c)
             assert sha(tr) == sha(r["trace"]), (plat, c)
+
+
+def _fnv_flat(vals):
+    h = 0xcbf29ce484222325
+    for v in vals:
+        for b in range(8):
+            h ^= (v >> (8 * b)) & 0xff
+            h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_explore_order_matches_reference(engine, ref, seed):
+    """ExploreHooks parity: the states explore_machine visits, in the order its DFS
+    discovers them (on_state), against the reference's own explore_machine
+    (ref_explore_order), state by state — with depth and visited caps (a full
+    visited set keeps the first max_states of that order)."""
+    import ctypes as C
+    from paper_2305_09130_b200._lib import lib
+    m = engine
+    rng = random.Random(6000 + seed)
+    for _ in range(4):
+        plat, size, kernel, inp = _case(rng)
+        size = min(size, 8)
+        inp = inp[:size] if inp else None
+        cfgs = [c for c in m.enumerate_configs(size) if kernel == 0 or c.wg * c.ts <= size]
+        c = rng.choice(cfgs)
+        depth = rng.choice((0, 0, rng.randint(5, 200)))
+        states = rng.choice((0, 0, rng.randint(10, 3000)))
+        want, n_want = ref.explore_order(plat, size, kernel, c.wg, c.ts, inp, max_depth=depth,
+                                         max_states=states)
+        prob = problem(m, size, kernel, inp)
+        cap = max(n_want, 1)
+        flat = (C.c_int64 * (cap * 1024))()
+        meta = (C.c_int32 * (8 * cap))()
+        info = (C.c_int64 * 3)()
+        rc = lib.mctb_machine_states(m.PlatformConfig(*plat).as_array(), size, kernel,
+                                     prob.input_array(), c.wg, c.ts, depth or 4_000_000,
+                                     states or 5_000_000, flat, cap * 1024, meta, cap, info)
+        assert rc == 0, (plat, size, kernel, c)
+        n, stride = info[1], info[2]
+        got = [_fnv_flat(flat[i * stride:(i + 1) * stride]) for i in range(n)]
+        key = (plat, size, kernel, c, depth, states)
+        assert n == n_want, key
+        assert got == want, key
